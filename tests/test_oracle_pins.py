@@ -1,0 +1,398 @@
+"""Pins for the CPU oracle (oracle/) against what the paper and mathematics fix.
+
+Nothing here re-types the oracle's formulas: every expected value comes from
+an independent statement (the transform's definition evaluated directly,
+the O(n^2) schoolbook product, a big-integer implementation without RNS,
+a different mod-switch algorithm, closed forms such as "decryption equals
+the plaintext dot product mod t", special cases, brute force).
+
+Paper citations: PAPER.md P:L244-256 (ring, ciphertext, decryption,
+budget), P:L1000 / P:L1314-1317 (NTT), P:L1003 / P:L1318-1324 (modulus
+switching to q_0), P:L1310-1313 (RNS/CRT).  Readings S1-S19: DESIGN.md.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import capi, tiny_ref
+
+pytestmark = pytest.mark.filterwarnings("ignore")
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# --------------------------------------------------------------------------
+# independent helpers (not the oracle's code)
+# --------------------------------------------------------------------------
+
+def mr_is_prime(x: int) -> bool:
+    """Deterministic Miller-Rabin for x < 3.4e14 (bases 2,3,5,7,11,13,17)."""
+    if x < 2:
+        return False
+    small = [2, 3, 5, 7, 11, 13, 17]
+    for p in small:
+        if x % p == 0:
+            return x == p
+    d, r = x - 1, 0
+    while d % 2 == 0:
+        d //= 2
+        r += 1
+    for a in small:
+        y = pow(a, d, x)
+        if y in (1, x - 1):
+            continue
+        for _ in range(r - 1):
+            y = y * y % x
+            if y == x - 1:
+                break
+        else:
+            return False
+    return True
+
+
+def numpy_schoolbook(a, b, q):
+    """O(n^2) negacyclic product mod q with numpy rows (independent of the oracle)."""
+    a = np.asarray(a, dtype=np.uint64)
+    b = np.asarray(b, dtype=np.uint64)
+    n = a.size
+    B = np.concatenate([(np.uint64(q) - b) % np.uint64(q), b])   # B[n + m] = b[m], B[n + m] = -b[m + n] for m < 0
+    r = np.zeros(n, dtype=np.uint64)
+    for i in range(n):
+        if a[i]:
+            r = (r + a[i] * B[n - i: 2 * n - i]) % np.uint64(q)
+    return r
+
+
+def load_golden_moduli():
+    out = {}
+    with open(os.path.join(GOLDEN, "moduli.txt")) as f:
+        for line in f:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            n, L, *qs = line.split()
+            out[(int(n), int(L))] = [int(x) for x in qs]
+    return out
+
+
+# --------------------------------------------------------------------------
+# o1: parameters
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n,L", [(4096, 2), (4096, 3), (8192, 4), (64, 2), (16, 3)])
+def test_primes_are_the_largest_ntt_friendly_30bit(n, L):
+    qs = capi.find_primes(n, L)
+    assert qs == sorted(qs) and len(set(qs)) == L
+    for q in qs:
+        assert q < 2 ** 30 and q % (2 * n) == 1 and mr_is_prime(q)
+    # completeness: no other prime = 1 mod 2n lies in [q_0, 2^30)
+    others = [c for c in range(qs[0], 2 ** 30, 2 * n) if mr_is_prime(c)]
+    assert others == qs
+    # reading S6: q_{l} < 2 q_0 so one conditional subtract reduces r mod q_i
+    assert qs[-1] < 2 * qs[0]
+
+
+def test_golden_moduli():
+    gold = load_golden_moduli()
+    for (n, L), qs in gold.items():
+        assert capi.find_primes(n, L) == qs
+
+
+@pytest.mark.parametrize("n", [8, 64, 4096, 8192])
+def test_min_primitive_root(n):
+    q = capi.find_primes(n, 1)[0]
+    psi = capi.min_root_2n(q, n)
+    assert pow(psi, n, q) == q - 1          # primitive 2n-th root: psi^n = -1
+    assert pow(psi, 2 * n, q) == 1
+    # minimality: every primitive 2n-th root is psi^k, k odd; none is smaller
+    roots = [pow(psi, k, q) for k in range(1, 2 * n, 2)]
+    assert min(roots) == psi
+    assert len(set(roots)) == n
+
+
+# --------------------------------------------------------------------------
+# o6: NTT
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [2, 4, 8, 16, 32, 64])
+def test_ntt_matches_definition(n):
+    """Forward transform = evaluation at the odd powers psi^(2k+1) (negacyclic)."""
+    q = capi.find_primes(n, 1)[0]
+    psi = capi.min_root_2n(q, n)
+    rng = np.random.default_rng(n)
+    a = rng.integers(0, q, size=n)
+    got = capi.ntt_forward(a, q)
+    want = [sum(int(a[j]) * pow(psi, (2 * k + 1) * j, q) for j in range(n)) % q for k in range(n)]
+    assert [int(x) for x in got] == want
+    back = capi.ntt_inverse(got, q)
+    assert np.array_equal(back, a.astype(np.uint64))
+
+
+@pytest.mark.parametrize("n", [4096, 8192])
+def test_ntt_roundtrip_and_trivial_cases(n):
+    for q in capi.find_primes(n, 2):
+        rng = np.random.default_rng(q)
+        a = rng.integers(0, q, size=n).astype(np.uint64)
+        assert np.array_equal(capi.ntt_inverse(capi.ntt_forward(a, q), q), a)
+        z = np.zeros(n, dtype=np.uint64)
+        assert not capi.ntt_forward(z, q).any()
+        c = np.zeros(n, dtype=np.uint64)
+        c[0] = 12345
+        fc = capi.ntt_forward(c, q)
+        assert (fc == 12345).all()                 # a constant evaluates to itself everywhere
+        assert np.array_equal(capi.ntt_inverse(fc, q), c)
+
+
+@pytest.mark.parametrize("n", [1, 2, 4, 8, 16, 32, 64])
+def test_polymul_equals_schoolbook_small(n):
+    if n == 1:
+        pytest.skip("n=1 has no negacyclic NTT")
+    for q in capi.find_primes(n, 2):
+        rng = np.random.default_rng(1000 + n)
+        for _ in range(5):
+            a = rng.integers(0, q, size=n)
+            b = rng.integers(0, q, size=n)
+            ref = tiny_ref.negacyclic_mul([int(x) for x in a], [int(x) for x in b], q)
+            assert [int(x) for x in capi.polymul_ntt(a, b, q)] == ref
+            assert [int(x) for x in capi.polymul_schoolbook(a, b, q)] == ref
+
+
+@pytest.mark.parametrize("n", [4096, 8192])
+def test_polymul_equals_schoolbook_large(n):
+    q = capi.find_primes(n, 1)[0]
+    rng = np.random.default_rng(n + 7)
+    reps = 2 if n == 4096 else 1
+    for _ in range(reps):
+        a = rng.integers(0, q, size=n)
+        b = rng.integers(0, q, size=n)
+        assert np.array_equal(capi.polymul_ntt(a, b, q).astype(np.uint64), numpy_schoolbook(a, b, q))
+
+
+# --------------------------------------------------------------------------
+# CRT and o7: modulus switching
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("L", [1, 2, 3, 4])
+def test_crt_against_sum_formula(L):
+    qs = capi.find_primes(8192, L)
+    rng = np.random.default_rng(L)
+    for _ in range(200):
+        r = [int(rng.integers(0, q)) for q in qs]
+        assert capi.crt(r, qs) == tiny_ref.crt_sum(r, qs)
+    assert capi.crt([0] * L, qs) == 0
+    assert capi.crt([1] * L, qs) == 1
+
+
+def _residues(c, qs):
+    return [c % q for q in qs]
+
+
+def _sequential_drop_last(c, qs):
+    """A different algorithm (reading S7): drop q_{L-1}, ..., q_1 one at a time,
+    each time rounding to nearest:  c <- floor((c + floor(q_l/2)) / q_l)."""
+    for q in reversed(qs[1:]):
+        c = (c + q // 2) // q
+    return c % qs[0]
+
+
+@pytest.mark.parametrize("L", [2, 3, 4])
+def test_modswitch_special_cases_and_sequential_identity(L):
+    qs = capi.find_primes(4096 if L < 4 else 8192, L)
+    Q = math.prod(qs)
+    P = Q // qs[0]
+    q0 = qs[0]
+    rng = np.random.default_rng(10 + L)
+    # c = k P  ->  k mod q0 (exact division, no rounding)
+    for k in [0, 1, 2, q0 - 1, int(rng.integers(0, q0))]:
+        assert capi.modswitch_coeff(_residues(k * P, qs), qs) == k % q0
+    # c in [0, P/2) -> 0 ; c in (P/2, P) -> 1   (round to nearest, no ties: P odd)
+    for c in [0, 1, P // 2]:
+        assert capi.modswitch_coeff(_residues(c, qs), qs) == 0
+    for c in [P // 2 + 1, P - 1]:
+        assert capi.modswitch_coeff(_residues(c, qs), qs) == 1
+    # the largest values round up to q0 == 0 mod q0
+    assert capi.modswitch_coeff(_residues(Q - 1, qs), qs) == 0
+    # random: |c' P - c| <= P/2 and equality with sequential drop-last
+    for _ in range(300):
+        c = int(rng.integers(0, 2 ** 62)) * int(rng.integers(0, 2 ** 62)) % Q
+        got = capi.modswitch_coeff(_residues(c, qs), qs)
+        k = (c + P // 2) // P        # nearest integer to c / P (independent statement)
+        assert got == k % q0
+        assert abs(k * P - c) <= P // 2
+        assert got == _sequential_drop_last(c, qs)
+
+
+# --------------------------------------------------------------------------
+# o5: packing identity (reading S1) -- closed form over Z
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [16, 32, 64])
+def test_packing_identity_bruteforce(n):
+    rng = np.random.default_rng(n)
+    for d in range(1, n + 1):
+        E = n // d
+        ents = rng.integers(-15, 16, size=(E, d))
+        qv = rng.integers(-15, 16, size=d)
+        p = capi.encode_plaintext(ents.astype(np.int8), d, n)
+        assert [int(x) for x in p] == tiny_ref.encode_plaintext(ents, d, n)
+        qpoly = [0] * n
+        qpoly[:d] = [int(x) for x in qv]
+        big = 1 << 80  # large modulus: the product is the exact integer product
+        prod = tiny_ref.negacyclic_mul(qpoly, [int(x) for x in p], big)
+        prod = [x - big if x > big // 2 else x for x in prod]
+        for j in range(E):
+            assert prod[j * d + d - 1] == int(np.dot(qv, ents[j]))
+
+
+def test_encode_rejects_overfull_plaintext():
+    with pytest.raises(ValueError):
+        capi.encode_plaintext(np.zeros((5, 4), dtype=np.int8), 4, 16)
+
+
+# --------------------------------------------------------------------------
+# whole pipeline: oracle (RNS + NTT + Garner) == big-integer tiny reference
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n,L,d", [(16, 2, 4), (16, 3, 5), (32, 2, 7), (32, 3, 32), (64, 2, 8), (64, 4, 13)])
+def test_server_pair_bit_exact_with_bigint_reference(n, L, d):
+    qs = capi.find_primes(n, L)
+    t = 65537
+    rng = np.random.default_rng(n * 10 + L)
+    w = synth.scaled(synth.WORKLOADS["c1"], n=n, num_limbs=L, d=d)
+    E = n // d
+    for trial in range(3):
+        ents = rng.integers(-15, 16, size=(E, d)).astype(np.int8)
+        qv = rng.integers(-15, 16, size=d).astype(np.int8)
+        km = synth.key_material(w, trial, qs)
+        msg = synth.query_message(w, qv)
+        ct = capi.encrypt(qs, t, msg, km.s, km.a, km.e)
+        # tiny_ref encryption over Z_Q gives the same ciphertext residues
+        c0, c1 = tiny_ref.encrypt(qs, t, msg, km.s, km.a, km.e)
+        assert np.array_equal(ct[0], np.array(tiny_ref.to_residues(c0, qs), dtype=np.uint32))
+        assert np.array_equal(ct[1], np.array(tiny_ref.to_residues(c1, qs), dtype=np.uint32))
+        p = capi.encode_plaintext(ents, d, n)
+        resp = capi.server_pair(qs, ct, p)
+        ref = tiny_ref.server_pair(qs, c0, c1, p)
+        assert np.array_equal(resp, np.array(ref, dtype=np.uint32))
+        dec = capi.decrypt_q0(qs[0], t, resp, km.s)
+        assert [int(x) for x in dec] == tiny_ref.decrypt_q0(qs[0], t, ref[0], ref[1], km.s)
+        for j in range(E):
+            assert int(dec[j * d + d - 1]) == int(np.dot(qv.astype(np.int64), ents[j].astype(np.int64))) % t
+
+
+def test_lift_convention_is_small_integer_mod_q():
+    """Reading S8: a negative entry x is lifted as x mod q_i (not [x]_t): a
+    plaintext with one coefficient -1 multiplies the ciphertext by -X^k."""
+    n, L = 32, 2
+    qs = capi.find_primes(n, L)
+    rng = np.random.default_rng(3)
+    ct = np.stack([np.stack([rng.integers(0, q, size=n) for q in qs]) for _ in range(2)]).astype(np.uint32)
+    p = np.zeros(n, dtype=np.int32)
+    p[0] = -1
+    neg = ct.copy()
+    for l, q in enumerate(qs):
+        neg[:, l] = (q - ct[:, l].astype(np.int64)) % q
+    resp_neg = capi.server_pair(qs, ct, p)
+    p[0] = 1
+    resp_negated_input = capi.server_pair(qs, neg, p)
+    assert np.array_equal(resp_neg, resp_negated_input)
+
+
+# --------------------------------------------------------------------------
+# o8/o9: decryption equals the plaintext dot products mod t; budget > 0
+# --------------------------------------------------------------------------
+
+SHAPES = {
+    "c1_c5": dict(n=4096, L=2, d=128, bound=15),
+    "c2": dict(n=4096, L=3, d=128, bound=15),
+    "c3": dict(n=4096, L=3, d=192, bound=15),
+    "c4": dict(n=8192, L=4, d=512, bound=7),
+}
+
+
+@pytest.mark.parametrize("shape", list(SHAPES))
+def test_decrypt_equals_dot_products_and_budget_positive(shape):
+    s = SHAPES[shape]
+    n, L, d, b = s["n"], s["L"], s["d"], s["bound"]
+    qs = capi.find_primes(n, L)
+    t = 65537
+    w = synth.scaled(synth.WORKLOADS["c1"], n=n, num_limbs=L, d=d)
+    rng = np.random.default_rng(n + L + d)
+    E = n // d
+    ents = rng.integers(-b, b + 1, size=(E + 3, d)).astype(np.int8)     # two plaintexts, last partial
+    pcs = capi.encode_cluster(ents, d, n)
+    qv = rng.integers(-b, b + 1, size=d).astype(np.int8)
+    km = synth.key_material(w, 0, qs)
+    ct = capi.encrypt(qs, t, synth.query_message(w, qv), km.s, km.a, km.e)
+    assert capi.noise_budget_Q(qs, t, ct, km.s) > 0
+    for k in range(pcs.shape[0]):
+        resp = capi.server_pair(qs, ct, pcs[k])
+        assert capi.noise_budget_q0(qs[0], t, resp, km.s) > 0
+        dec = capi.decrypt_q0(qs[0], t, resp, km.s)
+        cnt = min(E, ents.shape[0] - k * E)
+        for j in range(E):
+            want = int(np.dot(qv.astype(np.int64), ents[k * E + j].astype(np.int64))) % t if j < cnt else 0
+            assert int(dec[j * d + d - 1]) == want
+
+
+def test_fake_and_unit_queries():
+    """S14: a zero (fake) query decrypts to all zeros; query e_0 returns e_j[0]."""
+    n, L, d = 4096, 2, 128
+    qs = capi.find_primes(n, L)
+    t = 65537
+    w = synth.scaled(synth.WORKLOADS["c1"], n=n, num_limbs=L, d=d)
+    rng = np.random.default_rng(5)
+    ents = rng.integers(-15, 16, size=(n // d, d)).astype(np.int8)
+    p = capi.encode_plaintext(ents, d, n)
+    km = synth.key_material(w, 1, qs)
+    zero = capi.encrypt(qs, t, np.zeros(n, dtype=np.int32), km.s, km.a, km.e)
+    dec = capi.decrypt_q0(qs[0], t, capi.server_pair(qs, zero, p), km.s)
+    assert not dec.any()
+    unit = np.zeros(n, dtype=np.int32)
+    unit[0] = 1
+    ct = capi.encrypt(qs, t, unit, km.s, km.a, km.e)
+    dec = capi.decrypt_q0(qs[0], t, capi.server_pair(qs, ct, p), km.s)
+    for j in range(n // d):
+        assert int(dec[j * d + d - 1]) == int(ents[j][0]) % t
+
+
+def test_bruteforce_all_ternary_secrets_tiny_ring():
+    """N=8, d=4, two 30-bit primes, t=65537: every one of the 3^8 secrets."""
+    n, L, d, t = 8, 2, 4, 65537
+    qs = capi.find_primes(n, L)
+    rng = np.random.default_rng(8)
+    ents = rng.integers(-15, 16, size=(2, d)).astype(np.int8)
+    p = capi.encode_plaintext(ents, d, n)
+    qv = rng.integers(-15, 16, size=d).astype(np.int8)
+    msg = np.zeros(n, dtype=np.int32)
+    msg[:d] = qv
+    a = np.stack([rng.integers(0, q, size=n) for q in qs]).astype(np.uint32)
+    e = rng.integers(-6, 7, size=n).astype(np.int32)
+    want = [int(np.dot(qv.astype(np.int64), ents[j].astype(np.int64))) % t for j in range(2)]
+    import itertools
+    fails = 0
+    for s in itertools.product((-1, 0, 1), repeat=n):
+        s = np.array(s, dtype=np.int8)
+        ct = capi.encrypt(qs, t, msg, s, a, e)
+        dec = capi.decrypt_q0(qs[0], t, capi.server_pair(qs, ct, p), s)
+        fails += [int(dec[j * d + d - 1]) for j in range(2)] != want
+    assert fails == 0
+
+
+def test_server_pairs_batch_matches_single():
+    n, L, d = 256, 3, 16
+    qs = capi.find_primes(n, L)
+    rng = np.random.default_rng(11)
+    cts = np.stack([np.stack([np.stack([rng.integers(0, q, size=n) for q in qs]) for _ in range(2)])
+                    for _ in range(3)]).astype(np.uint32)
+    ents = rng.integers(-15, 16, size=(40, d)).astype(np.int8)
+    pcs = capi.encode_cluster(ents, d, n)
+    pq = np.array([0, 1, 2, 2, 0], dtype=np.uint32)
+    pp = np.array([0, 1, 2, 0, 2], dtype=np.uint32)
+    out, used = capi.server_pairs(qs, cts, pcs, pq, pp, threads=2)
+    assert used >= 1
+    for k in range(pq.size):
+        assert np.array_equal(out[k], capi.server_pair(qs, cts[pq[k]], pcs[pp[k]]))
