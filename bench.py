@@ -1,0 +1,438 @@
+#!/usr/bin/env python
+"""Benchmark: encrypted query x entry dot products per second (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl wally|reference]
+
+One step = one pass of the whole hot path over one batch (SURVEY.md §8(a)
+rows a1-a6): the batcher, the forward NTT of every query ciphertext and the
+fused pointwise-modmul / inverse-NTT / modulus-switch kernel that writes
+every single-limb response ciphertext, for the configuration's full query
+batch (default: configs[2] "c3", the paper-scale 3.2M-entry workload the
+north star names; all inputs resident in HBM when the timed region starts).
+
+Multi-GPU (torchrun, one process per GPU): clusters are owned by ranks
+(cluster c -> rank c mod N); every rank evaluates the queries of the clusters
+it owns; value = all ranks' dot products / max-over-ranks device time.
+
+`--impl reference` times the CPU oracle (oracle/, plain C) on this host's
+cores on a bounded sample of the same workload (the reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "encrypted query x entry dot products/sec"
+UNIT = "dot products/s"
+SM_COUNT = 148
+IMAD_PER_CLK_PER_SM = 64   # 4 SMSPs x 16 lanes (FMA-heavy pipe, rt=2 cycles/warp-instr; B300_MICROARCH.md)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(synth.WORKLOADS))
+    ap.add_argument("--impl", default="wally", choices=["wally", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-sub-batch", type=int, default=1024)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--quiet", action="store_true")
+    return ap.parse_args()
+
+
+def log(*a):
+    print("[bench]", *a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+# workload arithmetic (counts only)
+# ---------------------------------------------------------------------------
+
+def modmul_per_pair(n: int, L: int) -> int:
+    """Algorithmic modular multiplications per (query, plaintext) pair in the
+    fused kernel: 2 components x [pointwise L n +
+    inverse NTT L (n/2) log2 n + modulus switch n L(L-1)/2]."""
+    lg = n.bit_length() - 1
+    return 2 * (L * n + L * (n // 2) * lg + n * L * (L - 1) // 2)
+
+
+def hbm_bytes_per_batch(w, nq, pairs, clusters_touched_pts):
+    """Algorithmic HBM bytes of the fused kernel for one batch: every needed
+    plaintext (values + Shoup companions) read once, every query's NTT form
+    read once, every response written once."""
+    pt = clusters_touched_pts * w.num_limbs * 2 * w.n * 4
+    q = nq * 2 * w.num_limbs * w.n * 4
+    r = pairs * 2 * w.n * 4
+    return pt + q + r
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, nm in enumerate(names):
+                if len(r) > 4 + i and r[4 + i].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def ncu_traffic(config: str):
+    """dram read+write bytes per launch of the fused kernel from a committed
+    `ncu --set full` summary (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_fused_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(config)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle baseline (rank 0, N=1 only; also the --impl reference arm)
+# ---------------------------------------------------------------------------
+
+def oracle_sample(w, moduli, ents, ids, cts_host_fn, seconds: float, seed: int = 7):
+    """Time the oracle (as it stands) on a bounded sample of (query, plaintext)
+    pairs of this workload using every host core.  Returns a dict."""
+    from oracle import capi
+    E = w.n // w.d
+    P = -(-w.cluster_size // E)
+    rng = np.random.default_rng(seed)
+    cores = len(os.sched_getaffinity(0))
+
+    def run(npairs):
+        qsel = rng.integers(0, ids.size, size=npairs)
+        ksel = rng.integers(0, P, size=npairs)
+        uq, inv = np.unique(qsel, return_inverse=True)
+        cts = cts_host_fn(uq)
+        keys = sorted(set((int(ids[q]), int(k)) for q, k in zip(qsel, ksel)))
+        pidx = {ck: i for i, ck in enumerate(keys)}
+        pcs = np.stack([capi.encode_plaintext(ents[c][k * E:(k + 1) * E], w.d, w.n) for c, k in keys])
+        pp = np.array([pidx[(int(ids[q]), int(k))] for q, k in zip(qsel, ksel)], dtype=np.uint32)
+        dots = int(sum(min(E, w.cluster_size - int(k) * E) for k in ksel))
+        t0 = time.perf_counter()
+        _, used = capi.server_pairs(moduli, cts, pcs, inv.astype(np.uint32), pp, threads=cores)
+        dt = time.perf_counter() - t0
+        return npairs, dots, dt, used
+
+    n0, d0, t0, used = run(max(cores, 8))
+    rate = n0 / t0
+    npairs = max(cores, int(rate * seconds))
+    n1, d1, t1, used = run(npairs)
+    return {"value": d1 / t1, "unit": UNIT, "cores": int(used), "kind": "oracle",
+            "sample": f"{n1} random (query, plaintext) pairs of {w.name} ({d1} dot products) in {t1:.1f} s "
+                      f"with {used} OpenMP threads; plain C oracle, uint64 % arithmetic"}
+
+
+# ---------------------------------------------------------------------------
+# the product arm
+# ---------------------------------------------------------------------------
+
+def run_wally(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2406_06761_b200.wally import WallyServer
+
+    torch.cuda.set_device(local_rank)
+    dev = f"cuda:{local_rank}"
+    w = synth.WORKLOADS[args.config]
+    t_setup = time.time()
+    ents = synth.cluster_entries(w)
+    ids_all = synth.query_clusters(w)
+    C = w.num_clusters
+    owner = (np.arange(C) % world).astype(np.int32)
+    srv = WallyServer(w.n, w.num_limbs, w.d, w.t, device=local_rank)
+    moduli = srv.moduli
+    srv.load_clusters(np.full(C, w.cluster_size, np.uint32), owner if world > 1 else None, rank)
+    local = srv.local_cluster_ids()
+    ent_dev = torch.from_numpy(np.ascontiguousarray(ents[local]).reshape(-1, w.d)).to(dev)
+    torch.cuda.synchronize()
+    te = time.time()
+    srv.encode(ent_dev)
+    torch.cuda.synchronize()
+    encode_s = time.time() - te
+    del ent_dev
+    mine = np.nonzero(owner[ids_all] == rank)[0] if world > 1 else np.arange(ids_all.size)
+    ids = np.ascontiguousarray(ids_all[mine])
+    cts_all = synth.uniform_ciphertexts_torch(w, moduli, device=dev)
+    cts = cts_all[torch.from_numpy(mine).to(dev)] if world > 1 else cts_all
+    if world > 1:
+        del cts_all
+    E = w.n // w.d
+    P = -(-w.cluster_size // E)
+    nq = int(ids.size)
+    pairs = nq * P
+    dots = nq * w.cluster_size
+    off = srv.response_layout(ids)
+    resp = torch.empty(int(off[-1]), dtype=torch.int32, device=dev)
+    ws = srv.alloc_workspace(nq)
+    torch.cuda.synchronize()
+    setup_s = time.time() - t_setup
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        srv.eval_batch(ids, cts, resp, ws)
+    srv.check_batch(ws)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    srv.enable_stage_timing(True)
+    srv.stage_times()
+    launches0 = srv.kernel_launches()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        start.record(stream)
+        for _ in range(args.steps):
+            srv.eval_batch(ids, cts, resp, ws)
+        end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(end)
+    launches = srv.kernel_launches() - launches0
+    st_batcher, st_fwd, st_fused, nb = srv.stage_times()
+    srv.enable_stage_timing(False)
+    srv.check_batch(ws)
+
+    # max over ranks (time) and sums (work)
+    t = torch.tensor([ms, st_fused / max(nb, 1)], dtype=torch.float64, device=dev)
+    wk = torch.tensor([dots, pairs, nq], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(wk, op=dist.ReduceOp.SUM)
+    ms_max, fused_ms_max = float(t[0]), float(t[1])
+    tot_dots, tot_pairs, tot_nq = (int(x) for x in wk.tolist())
+    ms_per_step = ms_max / args.steps
+    value = tot_dots / (ms_per_step / 1e3)
+
+    # roofline of the dominant (fused) kernel: integer multiply pipe
+    peaks = measured_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    clocks = clk.summary()
+    mm = modmul_per_pair(w.n, w.num_limbs)
+    imad_per_launch = 3.0 * mm * pairs          # this rank's launch
+    fused_ms = st_fused / max(nb, 1)
+    achieved = imad_per_launch / (fused_ms / 1e3) / 1e12
+    peak = SM_COUNT * IMAD_PER_CLK_PER_SM * sm_max * 1e6 / 1e12
+    sm_now = clocks.get("sm_mhz") or sm_max
+    roofline = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TIMAD/s",
+                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.config),
+                "frac_at_measured_clock": round(achieved / (peak * sm_now / sm_max), 4),
+                "kernel": "eval_kernel (fused pointwise Shoup modmul + inverse NTT + RNS mod-switch)",
+                "per_launch": f"{pairs} pairs x {mm} modmul x 3 IMAD",
+                "peak_basis": f"{SM_COUNT} SMs x {IMAD_PER_CLK_PER_SM} IMAD/clk x {sm_max:.0f} MHz (sm_max_mhz "
+                              "of MEASURED_PEAKS.json); IMAD rate from the guide's pipe model, not measured",
+                "fused_ms_per_launch": round(fused_ms, 4),
+                "hbm_algorithmic_GBps": round(hbm_bytes_per_batch(w, nq, pairs, len(np.unique(ids)) * P)
+                                              / (fused_ms / 1e3) / 1e9, 1),
+                "hbm_peak_GBps": peaks.get("hbm_gbs")}
+
+    out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+           "data": "synthetic (seeded numpy/torch; entries per BASELINE config; query ciphertexts are uniform "
+                   "RNS residues, which RLWE makes indistinguishable from fresh encryptions)",
+           "config": {"workload": w.name, "description": w.description, "n": w.n, "limbs": w.num_limbs,
+                      "d": w.d, "t": w.t, "clusters": w.num_clusters, "cluster_size": w.cluster_size,
+                      "queries": int(tot_nq), "pairs_per_step": int(tot_pairs), "dots_per_step": int(tot_dots),
+                      "ownership": "cluster c -> rank c mod N" if world > 1 else "single rank",
+                      "l2": "inputs larger than L2 (plaintext store, query NTTs and responses >> 126 MB)"},
+           "roofline": roofline,
+           "stages_ms_per_step": {"batcher": round(st_batcher / max(nb, 1), 4),
+                                  "forward_ntt": round(st_fwd / max(nb, 1), 4),
+                                  "fused": round(fused_ms, 4)},
+           "gpu_launches": int(launches),
+           "clocks": clocks,
+           "setup_s": round(setup_s, 1), "encode_s": round(encode_s, 3)}
+
+    # end-to-end through the host-buffer C-ABI call (pinned host memory)
+    if not args.no_e2e and args.e2e_steps > 0:
+        try:
+            out["e2e"] = run_e2e(args, srv, ids, cts, off, world, rank, local_rank, dots)
+        except Exception as e:  # report, never hide
+            out["e2e"] = {"value": None, "unit": UNIT, "error": repr(e)[:300]}
+    del resp, ws
+    torch.cuda.empty_cache()
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        def cts_host(qidx):
+            return cts[torch.from_numpy(qidx).to(dev)].cpu().numpy().view(np.uint32)
+        out["cpu_baseline"] = oracle_sample(w, moduli, ents, ids, cts_host, args.cpu_seconds)
+    srv.close()
+    return out
+
+
+def run_e2e(args, srv, ids, cts, off, world, rank, local_rank, dots_local):
+    import torch
+    import torch.distributed as dist
+    dev = f"cuda:{local_rank}"
+    words = int(off[-1])
+    qh = torch.empty(cts.shape, dtype=torch.int32, pin_memory=True)
+    qh.copy_(cts)
+    rh = torch.empty(words, dtype=torch.int32, pin_memory=True)
+    sub = args.e2e_sub_batch
+    ws = torch.empty(srv.host_workspace_bytes(sub) // 4 + 64, dtype=torch.int32, device=dev)
+    srv.eval_batch_host(ids, qh, rh, sub, ws)  # warm-up
+    stream = torch.cuda.current_stream()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    start.record(stream)
+    for _ in range(args.e2e_steps):
+        srv.eval_batch_host(ids, qh, rh, sub, ws)
+    end.record(stream)
+    torch.cuda.synchronize()
+    ms = start.elapsed_time(end) / args.e2e_steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    d = torch.tensor([dots_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(d, op=dist.ReduceOp.SUM)
+    h2d = int(cts.numel() * 4)
+    d2h = int(words * 4)
+    del ws, qh, rh
+    return {"value": round(float(d[0]) / (float(t[0]) / 1e3), 1), "unit": UNIT,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(float(t[0]), 3),
+            "api": "wally_eval_batch_host (pinned host query ciphertexts -> device -> pinned host responses, "
+                   f"sub-batches of {sub} queries overlapped on two streams)", "steps": args.e2e_steps}
+
+
+# ---------------------------------------------------------------------------
+# the reference arm: the CPU oracle as it stands
+# ---------------------------------------------------------------------------
+
+def run_reference(args):
+    from oracle import capi
+    w = synth.WORKLOADS[args.config]
+    moduli = capi.find_primes(w.n, w.num_limbs)
+    ents = synth.cluster_entries(w)
+    ids = synth.query_clusters(w)
+    E = w.n // w.d
+    P = -(-w.cluster_size // E)
+    cores = len(os.sched_getaffinity(0))
+    rng = np.random.default_rng(11)
+    # one fixed sample of pairs per step, sized for ~ a few seconds of oracle work
+    npairs = max(cores, 2 * cores)
+    qsel = rng.integers(0, ids.size, size=npairs)
+    ksel = rng.integers(0, P, size=npairs)
+    uq, inv = np.unique(qsel, return_inverse=True)
+    cts = synth.uniform_ciphertexts(synth.scaled(w, num_queries=len(uq)), moduli)
+    keys = sorted(set((int(ids[q]), int(k)) for q, k in zip(qsel, ksel)))
+    pidx = {ck: i for i, ck in enumerate(keys)}
+    pcs = np.stack([capi.encode_plaintext(ents[c][k * E:(k + 1) * E], w.d, w.n) for c, k in keys])
+    pp = np.array([pidx[(int(ids[q]), int(k))] for q, k in zip(qsel, ksel)], dtype=np.uint32)
+    dots = int(sum(min(E, w.cluster_size - int(k) * E) for k in ksel))
+    used = cores
+    for _ in range(args.warmup):
+        _, used = capi.server_pairs(moduli, cts, pcs, inv.astype(np.uint32), pp, threads=cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        _, used = capi.server_pairs(moduli, cts, pcs, inv.astype(np.uint32), pp, threads=cores)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = dots / dt
+    sample = (f"{npairs} random (query, plaintext) pairs of {w.name} per step ({dots} dot products); "
+              f"plain C oracle with {used} OpenMP threads")
+    return {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64 (oracle % arithmetic)",
+            "data": "synthetic (seeded)", "impl": "reference",
+            "config": {"workload": w.name, "description": w.description},
+            "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": int(used), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    out = run_wally(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,204 @@
+/*
+ * wally.h -- C ABI of the B200-native Wally server hot path.
+ *
+ * The operation (arXiv 2406.06761, PAPER.md; citation "P:Lnnn" = PAPER.md line):
+ *   The server holds a public database of d-dimensional integer embeddings
+ *   split into clusters (Alg 1 "ServerInit" P:L664-687).
+ *   Each query is an RLWE/BFV ciphertext (c0, c1) over R_Q = Z_Q[X]/(X^n+1),
+ *   Q = q_0 q_1 ... q_{L-1} in RNS form, tagged with
+ *   a cluster id.  For every query the server computes, under encryption,
+ *   the dot product of the query with every entry of its cluster and returns
+ *   the encrypted scores (Alg 4 "ServerComputation" P:L794-808).
+ *
+ *   This library computes that result with coefficient packing (BASELINE.json
+ *   north_star; DESIGN.md "Readings" S1): plaintext k of cluster c is
+ *     p_k(X) = sum_{j<E} sum_{i<d} e_{kE+j}[i] X^{j d + d - 1 - i},  E = floor(n/d),
+ *   and for every (query, plaintext) pair the response is
+ *     c'_b = round( (c_b * p_k mod (X^n+1, Q)) * q_0 / Q ) mod q_0,   b in {0, 1},
+ *   the modulus switch to the smallest limb q_0.
+ *   Decrypting c'_0 + c'_1 s mod q_0 and scaling by t/q_0 gives, at coefficient
+ *   j*d + d - 1, the dot product <query, e_{kE+j}> mod t.
+ *
+ * Conventions shared by every call:
+ *   - All integers little-endian.  Residues are uint32, canonical in [0, q_i).
+ *   - A polynomial with L limbs is stored limb-major: [L][n].
+ *   - Query ciphertexts: uint32 [nq][2][L][n] in coefficient form, component 0
+ *     is c0, component 1 is c1 (input-query order).
+ *   - Responses: for query q (input order), P(c_q) ciphertexts in plaintext
+ *     order, each uint32 [2][n] mod q_0.  Query q's first word is at
+ *     offsets[q] as returned by wally_response_layout (reading S12).
+ *   - "dev" pointers are CUDA device pointers on the context's device; "host"
+ *     pointers are CPU memory.  The caller owns every buffer it passes; the
+ *     library never frees them.  Device buffers the library needs beyond its
+ *     small internal tables (the plaintext store, the per-batch workspace and
+ *     the response buffer) are allocated by the caller (from PyTorch in the
+ *     Python binding) with the sizes the *_bytes queries return.
+ *   - "stream" is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Calls taking a stream are stream-ordered and return before the device
+ *     work finishes; inputs must stay valid until it has.
+ *   - Every call validates all of its arguments before launching anything and
+ *     does nothing on error.  Errors are returned as a negative wally_status;
+ *     wally_last_error() gives a detail string.  Nothing aborts.
+ *   - A context is bound to one device and is not thread-safe.
+ */
+#ifndef WALLY_H
+#define WALLY_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WALLY_MAX_LIMBS 4
+
+typedef enum {
+    WALLY_OK = 0,
+    WALLY_E_ARG = -1,             /* null pointer, size mismatch, bad range */
+    WALLY_E_PARAMS = -2,          /* unsupported n / L / d, moduli not NTT-friendly primes */
+    WALLY_E_UNKNOWN_CLUSTER = -3, /* cluster id >= total clusters or not owned by this context */
+    WALLY_E_RESIDUE = -4,         /* an input residue >= q_i (reported by wally_check_batch) */
+    WALLY_E_STATE = -5,           /* call order: e.g. eval before encode */
+    WALLY_E_CUDA = -6,            /* a CUDA runtime call failed */
+    WALLY_E_OOM = -8              /* internal table allocation failed */
+} wally_status;
+
+typedef struct wally_ctx wally_ctx;
+
+/* Scheme parameters.
+ *   n          ring degree, a power of two in {1024, 2048, 4096, 8192}
+ *   num_limbs  L in [1, 4]
+ *   t          plaintext modulus (only used for documentation / validation: t >= 2)
+ *   d          embedding dimension, 1 <= d <= n  (d need not divide n)
+ *   moduli     q_0 < q_1 < ... < q_{L-1}: distinct primes < 2^30, each = 1 mod 2n,
+ *              with q_{L-1} < 2 q_0 ("q_i = 1 mod 2n"; readings S5, S6). */
+typedef struct {
+    uint32_t n;
+    uint32_t num_limbs;
+    uint32_t t;
+    uint32_t d;
+    uint32_t moduli[WALLY_MAX_LIMBS];
+} wally_params;
+
+/* The L largest primes q < 2^30 with q = 1 (mod 2n), written ascending into
+ * moduli_out[0..L-1] (reading S5).  Pure host computation. */
+int wally_find_moduli(uint32_t n, uint32_t num_limbs, uint32_t *moduli_out);
+
+/* Create a context on CUDA device `device`: validates params, builds the
+ * NTT twiddle tables and modulus-switch constants and uploads them. */
+int wally_create(const wally_params *params, int device, wally_ctx **ctx_out);
+void wally_destroy(wally_ctx *ctx);
+/* Detail of the last error on ctx (or of the last failed wally_create when ctx is NULL). */
+const char *wally_last_error(const wally_ctx *ctx);
+
+/* ServerInit, part 1 (Alg 1): the cluster layout.
+ *   total_clusters      number of clusters in the whole database (all ranks)
+ *   cluster_sizes_host  uint32 [total_clusters]: entries in each cluster (>= 1)
+ *   owner_host          int32 [total_clusters]: owning rank of each cluster, or NULL
+ *                       meaning "every cluster is local" (reading: cluster-sharded
+ *                       data parallelism)
+ *   rank                this context's rank (ignored when owner_host is NULL)
+ * Local clusters are the ones with owner == rank, taken in ascending id order.
+ * Plaintexts per cluster: P_c = ceil(size_c / E), E = floor(n/d). */
+int wally_load_clusters(wally_ctx *ctx, uint32_t total_clusters, const uint32_t *cluster_sizes_host,
+                        const int32_t *owner_host, int32_t rank);
+
+/* Bytes of the device plaintext store for the local clusters:
+ * sum_c P_c * L * 2 * n * 4 (NTT-domain values plus Shoup companions). */
+int wally_plaintext_store_bytes(const wally_ctx *ctx, size_t *bytes_out);
+/* Number of local entries (rows of the entries array wally_encode_plaintexts_ntt reads). */
+int wally_local_entry_count(const wally_ctx *ctx, uint64_t *count_out);
+
+/* ServerInit, part 2: pack every local plaintext (entries reversed at offsets
+ * j*d, reading S1), lift each signed entry x to x mod q_i (S8), forward-NTT
+ * per limb and keep the result, with its Shoup companion, in store_dev.
+ *   entries_dev  int8 [local_entry_count][d] row-major, local clusters in
+ *                ascending cluster-id order, each cluster's entries contiguous
+ *   store_dev    device buffer of wally_plaintext_store_bytes bytes; the
+ *                context keeps using it until the next encode or destroy. */
+int wally_encode_plaintexts_ntt(wally_ctx *ctx, const int8_t *entries_dev, void *store_dev, size_t store_bytes,
+                                void *stream);
+
+/* Response layout of a batch (reading S12).
+ *   cluster_of_query_host  uint32 [nq]
+ *   offsets_host           uint64 [nq + 1] out: word offset of query q's responses;
+ *                          offsets[nq] = total words.  May be NULL.
+ *   total_words_out        total response words (may be NULL).
+ * Fails with WALLY_E_UNKNOWN_CLUSTER if a query names a cluster that is not local. */
+int wally_response_layout(const wally_ctx *ctx, uint32_t nq, const uint32_t *cluster_of_query_host,
+                          uint64_t *offsets_host, uint64_t *total_words_out);
+
+/* Bytes of device workspace wally_eval_batch needs for nq queries. */
+int wally_workspace_bytes(const wally_ctx *ctx, uint32_t nq, size_t *bytes_out);
+
+/* ServerComputation for a batch (Alg 4 P:L794-808 analog):
+ *   1. batcher kernels group the queries by cluster id (histogram, scan,
+ *      scatter) and build the (cluster, plaintext, query-chunk) work list;
+ *   2. forward negacyclic NTT of all 2*L*nq query polynomials;
+ *   3. one fused kernel per work item: pointwise Shoup modmul with each
+ *      NTT-domain plaintext, inverse NTT, RNS modulus switch to q_0, and the
+ *      write of the single-limb response ciphertext.
+ *   cluster_of_query_host  uint32 [nq] (host; validated before any launch)
+ *   query_ct_dev           uint32 [nq][2][L][n] canonical residues (device)
+ *   responses_dev          uint32 [responses_words] (device), layout of wally_response_layout
+ *   workspace_dev          wally_workspace_bytes(nq) bytes (device)
+ * Residues >= q_i are detected on the device and reported by wally_check_batch. */
+int wally_eval_batch(wally_ctx *ctx, uint32_t nq, const uint32_t *cluster_of_query_host,
+                     const uint32_t *query_ct_dev, uint32_t *responses_dev, uint64_t responses_words,
+                     void *workspace_dev, size_t workspace_bytes, void *stream);
+
+/* Synchronizes `stream` and reports device-side errors of the last batch run on
+ * this workspace: WALLY_E_RESIDUE if any query residue was >= its modulus. */
+int wally_check_batch(wally_ctx *ctx, const void *workspace_dev, void *stream);
+
+/* Copy responses device -> host (stream-ordered, then synchronizes the stream).
+ *   responses_dev  uint32 [words] (device);  out_host  uint32 [words] (host, pinned or pageable) */
+int wally_fetch_responses(wally_ctx *ctx, const uint32_t *responses_dev, uint64_t words, uint32_t *out_host,
+                          void *stream);
+
+/* End-to-end call with HOST buffers (the serving path): the batch is split
+ * into sub-batches of at most sub_batch queries; each sub-batch's query
+ * ciphertexts are copied host->device, evaluated, and its responses copied
+ * device->host into responses_host, with copies and compute of consecutive
+ * sub-batches overlapped on two streams.  Synchronizes before returning.
+ *   query_ct_host   uint32 [nq][2][L][n] (pinned for full copy bandwidth)
+ *   responses_host  uint32 [responses_words], layout of wally_response_layout
+ *   workspace_dev   wally_host_workspace_bytes(sub_batch, max_words) bytes */
+int wally_host_workspace_bytes(const wally_ctx *ctx, uint32_t sub_batch, size_t *bytes_out);
+int wally_eval_batch_host(wally_ctx *ctx, uint32_t nq, const uint32_t *cluster_of_query_host,
+                          const uint32_t *query_ct_host, uint32_t *responses_host, uint64_t responses_words,
+                          uint32_t sub_batch, void *workspace_dev, size_t workspace_bytes, void *stream);
+
+/* Multi-GPU routing: destination rank of every query
+ * from the owner map given to wally_load_clusters (rank of the owning
+ * context).  dest_rank_host int32 [nq] out. */
+int wally_route_queries(const wally_ctx *ctx, uint32_t nq, const uint32_t *cluster_of_query_host,
+                        int32_t *dest_rank_host);
+
+/* Test hooks on the same device code as the hot path.
+ * Forward NTT (the kernel of step 2): in_dev uint32 [count][L][n] canonical
+ * coefficient form -> out_dev uint32 [count][L][n] NTT domain (internal,
+ * bit-reversed order, residues in [0, 4 q_i)).
+ * Inverse NTT: out = n^{-1} * INTT(in), canonical coefficient form; in may be
+ * any residues < 2^32 congruent to the NTT values. */
+int wally_ntt_forward(wally_ctx *ctx, const uint32_t *in_dev, uint32_t *out_dev, uint32_t count, void *stream);
+int wally_ntt_inverse(wally_ctx *ctx, const uint32_t *in_dev, uint32_t *out_dev, uint32_t count, void *stream);
+
+/* Count of this library's kernel launches since create (for bench evidence). */
+uint64_t wally_kernel_launches(const wally_ctx *ctx);
+
+/* Per-stage device timing of wally_eval_batch (CUDA events recorded on the
+ * batch's stream around each stage when enabled; off by default).
+ * wally_stage_times synchronizes the recorded events and returns the summed
+ * milliseconds since the last call: ms_out[0] batcher kernels, ms_out[1]
+ * forward NTT, ms_out[2] fused modmul/iNTT/mod-switch kernel; batches_out =
+ * number of batches summed.  Clears the record. */
+int wally_enable_stage_timing(wally_ctx *ctx, int enable);
+int wally_stage_times(wally_ctx *ctx, double *ms_out, uint64_t *batches_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WALLY_H */

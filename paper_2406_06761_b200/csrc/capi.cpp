@@ -1,0 +1,640 @@
+// Host side of the C ABI declared in include/wally.h: parameter validation,
+// NTT tables, modulus-switch constants, cluster layout, batch workspace and
+// the host-buffer serving pipeline.  All device compute is in kernels.cu.
+//
+// Citations: PAPER.md P:L1310-1317 (RNS, NTT-friendly limbs), P:L1003 and
+// P:L1318-1324 (modulus switch to q_0), Alg 1 P:L664-687 (ServerInit),
+// Alg 4 P:L794-808 (ServerComputation), P:L63-64 (server groups received
+// queries by cluster).
+
+#include <algorithm>
+#include <array>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "wally_internal.h"
+
+using namespace wally;
+
+struct wally_ctx {
+    wally_params p{};
+    int device = 0;
+    int num_sms = 148;
+    uint32_t E = 0;
+    KParams kp{};
+    uint2 *d_tw_fwd = nullptr, *d_tw_inv = nullptr;
+    // cluster layout
+    bool loaded = false;
+    uint32_t total_clusters = 0, n_local = 0, npt = 0, max_pt = 0;
+    std::vector<int32_t> local_of_cluster;     // host copy
+    std::vector<int32_t> owner;                // [total_clusters] (empty: all local)
+    int32_t rank = 0;
+    std::vector<uint32_t> pt_of_local;         // P_c per local cluster
+    uint64_t local_entries = 0;
+    int32_t *d_local_of_cluster = nullptr;
+    uint32_t *d_pt_base = nullptr, *d_n_pt = nullptr, *d_pt_li = nullptr, *d_pt_k = nullptr, *d_size = nullptr;
+    uint64_t *d_entry_base = nullptr;
+    // encoded plaintexts (caller-owned)
+    const uint32_t *store = nullptr;
+    // pinned staging for per-batch metadata (ids + response offsets), 2 slots
+    struct Slot {
+        uint32_t *ids = nullptr;
+        uint64_t *off = nullptr;
+        size_t cap = 0;
+        cudaEvent_t done = nullptr;
+        bool pending = false;
+    } slot[2];
+    int next_slot = 0;
+    cudaStream_t side = nullptr;  // second stream of the host pipeline
+    uint64_t launches = 0;
+    // optional per-stage timing: 4 events per recorded batch
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::array<cudaEvent_t, 4>> ev_rec;
+    std::string err;
+};
+
+static thread_local std::string g_create_err;
+
+static int fail(wally_ctx *c, int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf; else g_create_err = buf;
+    return code;
+}
+
+#define CUDA_OK(ctx, call)                                                                              \
+    do {                                                                                                \
+        cudaError_t _e = (call);                                                                        \
+        if (_e != cudaSuccess) return fail(ctx, WALLY_E_CUDA, "%s: %s", #call, cudaGetErrorString(_e)); \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// Number theory (host).  Own implementation: deterministic Miller-Rabin for
+// 32-bit integers, primitive root by the first-found power, Shoup companions.
+// ---------------------------------------------------------------------------
+static uint64_t mulm(uint64_t a, uint64_t b, uint64_t m) { return (uint64_t)((unsigned __int128)a * b % m); }
+static uint64_t powm(uint64_t b, uint64_t e, uint64_t m) {
+    uint64_t r = 1 % m;
+    for (b %= m; e; e >>= 1, b = mulm(b, b, m))
+        if (e & 1) r = mulm(r, b, m);
+    return r;
+}
+static uint64_t invm(uint64_t a, uint64_t m) { return powm(a, m - 2, m); }  // m prime
+
+static bool is_prime32(uint64_t n) {
+    if (n < 2) return false;
+    for (uint64_t p : {2ull, 3ull, 5ull, 7ull, 11ull, 13ull})
+        if (n % p == 0) return n == p;
+    uint64_t d = n - 1;
+    int s = 0;
+    while (!(d & 1)) { d >>= 1; s++; }
+    for (uint64_t a : {2ull, 7ull, 61ull}) {  // deterministic for n < 4,759,123,141
+        uint64_t x = powm(a, d, n);
+        if (x == 1 || x == n - 1) continue;
+        bool comp = true;
+        for (int r = 1; r < s; r++) {
+            x = mulm(x, x, n);
+            if (x == n - 1) { comp = false; break; }
+        }
+        if (comp) return false;
+    }
+    return true;
+}
+
+static uint32_t shoup_companion(uint32_t w, uint32_t q) { return (uint32_t)(((uint64_t)w << 32) / q); }
+
+static uint32_t bitrev(uint32_t x, int bits) {
+    uint32_t r = 0;
+    for (int i = 0; i < bits; i++) r |= ((x >> i) & 1u) << (bits - 1 - i);
+    return r;
+}
+
+// A primitive 2n-th root of unity mod q: x^((q-1)/2n) for the first x that
+// gives psi^n = -1.
+static uint64_t primitive_2n_root(uint64_t q, uint32_t n) {
+    for (uint64_t x = 2; x < q; x++) {
+        uint64_t psi = powm(x, (q - 1) / (2ull * n), q);
+        if (powm(psi, n, q) == q - 1) return psi;
+    }
+    return 0;
+}
+
+extern "C" int wally_find_moduli(uint32_t n, uint32_t num_limbs, uint32_t *moduli_out) {
+    if (!moduli_out || num_limbs == 0 || num_limbs > WALLY_MAX_LIMBS || n < 2 || (n & (n - 1)))
+        return fail(nullptr, WALLY_E_ARG, "wally_find_moduli: bad arguments");
+    const uint64_t step = 2ull * n;
+    std::vector<uint32_t> found;
+    for (uint64_t q = ((1ull << 30) - 2) / step * step + 1; q > step && found.size() < num_limbs; q -= step)
+        if (q < (1ull << 30) && is_prime32(q)) found.push_back((uint32_t)q);
+    if (found.size() < num_limbs) return fail(nullptr, WALLY_E_PARAMS, "not enough NTT-friendly primes");
+    for (uint32_t i = 0; i < num_limbs; i++) moduli_out[i] = found[num_limbs - 1 - i];
+    return WALLY_OK;
+}
+
+// ---------------------------------------------------------------------------
+// create / destroy
+// ---------------------------------------------------------------------------
+extern "C" const char *wally_last_error(const wally_ctx *ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+
+extern "C" uint64_t wally_kernel_launches(const wally_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+extern "C" void wally_destroy(wally_ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    cudaFree(c->d_tw_fwd);
+    cudaFree(c->d_tw_inv);
+    cudaFree(c->d_local_of_cluster);
+    cudaFree(c->d_pt_base);
+    cudaFree(c->d_n_pt);
+    cudaFree(c->d_pt_li);
+    cudaFree(c->d_pt_k);
+    cudaFree(c->d_size);
+    cudaFree(c->d_entry_base);
+    for (auto &s : c->slot) {
+        if (s.ids) cudaFreeHost(s.ids);
+        if (s.off) cudaFreeHost(s.off);
+        if (s.done) cudaEventDestroy(s.done);
+    }
+    if (c->side) cudaStreamDestroy(c->side);
+    for (auto &r : c->ev_rec) for (auto e : r) c->ev_pool.push_back(e);
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    delete c;
+}
+
+extern "C" int wally_create(const wally_params *pp, int device, wally_ctx **out) {
+    if (!pp || !out) return fail(nullptr, WALLY_E_ARG, "wally_create: null argument");
+    *out = nullptr;
+    const wally_params &p = *pp;
+    if (p.n != 1024 && p.n != 2048 && p.n != 4096 && p.n != 8192)
+        return fail(nullptr, WALLY_E_PARAMS, "n=%u unsupported (1024, 2048, 4096, 8192)", p.n);
+    if (p.num_limbs < 1 || p.num_limbs > WALLY_MAX_LIMBS)
+        return fail(nullptr, WALLY_E_PARAMS, "num_limbs=%u unsupported (1..%d)", p.num_limbs, WALLY_MAX_LIMBS);
+    if (p.d < 1 || p.d > p.n) return fail(nullptr, WALLY_E_PARAMS, "d=%u must be in [1, n]", p.d);
+    if (p.t < 2) return fail(nullptr, WALLY_E_PARAMS, "t=%u must be >= 2", p.t);
+    for (uint32_t i = 0; i < p.num_limbs; i++) {
+        uint32_t q = p.moduli[i];
+        if (q >= (1u << 30) || q % (2 * p.n) != 1 || !is_prime32(q))
+            return fail(nullptr, WALLY_E_PARAMS, "modulus q_%u=%u is not a prime < 2^30 with q = 1 mod 2n", i, q);
+        if (i && q <= p.moduli[i - 1]) return fail(nullptr, WALLY_E_PARAMS, "moduli must be strictly ascending");
+    }
+    if (p.moduli[p.num_limbs - 1] >= 2ull * p.moduli[0])
+        return fail(nullptr, WALLY_E_PARAMS, "need q_{L-1} < 2 q_0 (single-subtract reduction of r mod q_i)");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+        return fail(nullptr, WALLY_E_CUDA, "no CUDA device %d", device);
+
+    wally_ctx *c = new wally_ctx();
+    c->p = p;
+    c->device = device;
+    c->E = p.n / p.d;
+    if (cudaSetDevice(device) != cudaSuccess) { delete c; return fail(nullptr, WALLY_E_CUDA, "cudaSetDevice"); }
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+
+    const uint32_t n = p.n, L = p.num_limbs;
+    int logn = 0;
+    while ((1u << logn) < n) logn++;
+    KParams &kp = c->kp;
+    std::vector<uint2> twf((size_t)L * n), twi((size_t)L * n);
+    for (uint32_t l = 0; l < L; l++) {
+        const uint64_t q = p.moduli[l];
+        kp.q[l] = (uint32_t)q;
+        kp.q2[l] = (uint32_t)(2 * q);
+        kp.h[l] = (uint32_t)(q / 2);
+        kp.ninv[l] = (uint32_t)invm(n, q);
+        kp.ninvp[l] = shoup_companion(kp.ninv[l], (uint32_t)q);
+        // fold F_l = n^{-1} prod_{k>l} q_k^{-1} mod q_l
+        uint64_t f = invm(n, q);
+        for (uint32_t k = l + 1; k < L; k++) f = mulm(f, invm(p.moduli[k] % q, q), q);
+        kp.fold[l] = (uint32_t)f;
+        kp.foldp[l] = shoup_companion((uint32_t)f, (uint32_t)q);
+        // C[l][m] = prod_{k=l+1..m} q_k^{-1} mod q_l
+        uint64_t cm = 1;
+        for (uint32_t m = l + 1; m < L; m++) {
+            cm = mulm(cm, invm(p.moduli[m] % q, q), q);
+            kp.C[l][m] = (uint32_t)cm;
+            kp.Cp[l][m] = shoup_companion((uint32_t)cm, (uint32_t)q);
+        }
+        const uint64_t psi = primitive_2n_root(q, n);
+        const uint64_t psi_inv = invm(psi, q);
+        for (uint32_t i = 0; i < n; i++) {
+            const uint32_t e = bitrev(i, logn);
+            const uint32_t w = (uint32_t)powm(psi, e, q), wi = (uint32_t)powm(psi_inv, e, q);
+            twf[(size_t)l * n + i] = make_uint2(w, shoup_companion(w, (uint32_t)q));
+            twi[(size_t)l * n + i] = make_uint2(wi, shoup_companion(wi, (uint32_t)q));
+        }
+    }
+    const size_t tb = sizeof(uint2) * twf.size();
+    if (cudaMalloc(&c->d_tw_fwd, tb) != cudaSuccess || cudaMalloc(&c->d_tw_inv, tb) != cudaSuccess) {
+        wally_destroy(c);
+        return fail(nullptr, WALLY_E_OOM, "twiddle table allocation failed");
+    }
+    cudaMemcpy(c->d_tw_fwd, twf.data(), tb, cudaMemcpyHostToDevice);
+    cudaMemcpy(c->d_tw_inv, twi.data(), tb, cudaMemcpyHostToDevice);
+    for (auto &s : c->slot) cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming);
+    cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+    if (cudaGetLastError() != cudaSuccess) {
+        wally_destroy(c);
+        return fail(nullptr, WALLY_E_CUDA, "context setup failed");
+    }
+    *out = c;
+    return WALLY_OK;
+}
+
+// ---------------------------------------------------------------------------
+// ServerInit
+// ---------------------------------------------------------------------------
+template <typename T>
+static int upload(wally_ctx *c, T **dst, const std::vector<T> &v) {
+    cudaFree(*dst);
+    *dst = nullptr;
+    size_t bytes = std::max<size_t>(1, v.size()) * sizeof(T);
+    if (cudaMalloc(dst, bytes) != cudaSuccess) return fail(c, WALLY_E_OOM, "device table allocation failed");
+    if (!v.empty()) CUDA_OK(c, cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return WALLY_OK;
+}
+
+extern "C" int wally_load_clusters(wally_ctx *c, uint32_t total_clusters, const uint32_t *sizes,
+                                   const int32_t *owner, int32_t rank) {
+    if (!c) return WALLY_E_ARG;
+    if (!sizes || total_clusters == 0) return fail(c, WALLY_E_ARG, "load_clusters: need >= 1 cluster and sizes");
+    std::vector<int32_t> local(total_clusters, -1);
+    std::vector<uint32_t> pt_base, n_pt, pt_li, pt_k, size;
+    std::vector<uint64_t> entry_base;
+    uint64_t entries = 0;
+    uint32_t npt = 0, max_pt = 0;
+    for (uint32_t cl = 0; cl < total_clusters; cl++) {
+        if (sizes[cl] == 0) return fail(c, WALLY_E_ARG, "cluster %u is empty", cl);
+        if (owner && owner[cl] != rank) continue;
+        const uint32_t li = (uint32_t)pt_base.size();
+        const uint32_t P = (sizes[cl] + c->E - 1) / c->E;
+        local[cl] = (int32_t)li;
+        pt_base.push_back(npt);
+        n_pt.push_back(P);
+        size.push_back(sizes[cl]);
+        entry_base.push_back(entries);
+        for (uint32_t k = 0; k < P; k++) { pt_li.push_back(li); pt_k.push_back(k); }
+        npt += P;
+        max_pt = std::max(max_pt, P);
+        entries += sizes[cl];
+    }
+    if (pt_base.empty()) return fail(c, WALLY_E_ARG, "rank %d owns no cluster", rank);
+    cudaSetDevice(c->device);
+    int rc;
+    if ((rc = upload(c, &c->d_local_of_cluster, local)) || (rc = upload(c, &c->d_pt_base, pt_base)) ||
+        (rc = upload(c, &c->d_n_pt, n_pt)) || (rc = upload(c, &c->d_pt_li, pt_li)) ||
+        (rc = upload(c, &c->d_pt_k, pt_k)) || (rc = upload(c, &c->d_size, size)) ||
+        (rc = upload(c, &c->d_entry_base, entry_base)))
+        return rc;
+    c->total_clusters = total_clusters;
+    c->n_local = (uint32_t)pt_base.size();
+    c->npt = npt;
+    c->max_pt = max_pt;
+    c->local_of_cluster = std::move(local);
+    c->owner = owner ? std::vector<int32_t>(owner, owner + total_clusters) : std::vector<int32_t>();
+    c->rank = rank;
+    c->pt_of_local = std::move(n_pt);
+    c->local_entries = entries;
+    c->store = nullptr;
+    c->loaded = true;
+    return WALLY_OK;
+}
+
+extern "C" int wally_plaintext_store_bytes(const wally_ctx *c, size_t *bytes) {
+    if (!c || !bytes) return WALLY_E_ARG;
+    if (!c->loaded) return fail(const_cast<wally_ctx *>(c), WALLY_E_STATE, "load_clusters first");
+    *bytes = (size_t)c->npt * c->p.num_limbs * 2 * c->p.n * sizeof(uint32_t);
+    return WALLY_OK;
+}
+
+extern "C" int wally_local_entry_count(const wally_ctx *c, uint64_t *count) {
+    if (!c || !count) return WALLY_E_ARG;
+    if (!c->loaded) return fail(const_cast<wally_ctx *>(c), WALLY_E_STATE, "load_clusters first");
+    *count = c->local_entries;
+    return WALLY_OK;
+}
+
+extern "C" int wally_encode_plaintexts_ntt(wally_ctx *c, const int8_t *entries_dev, void *store_dev,
+                                           size_t store_bytes, void *stream) {
+    if (!c) return WALLY_E_ARG;
+    if (!c->loaded) return fail(c, WALLY_E_STATE, "load_clusters first");
+    size_t need = 0;
+    wally_plaintext_store_bytes(c, &need);
+    if (!entries_dev || !store_dev) return fail(c, WALLY_E_ARG, "encode: null device pointer");
+    if (store_bytes < need) return fail(c, WALLY_E_ARG, "encode: store has %zu bytes, need %zu", store_bytes, need);
+    if ((uintptr_t)store_dev % 16) return fail(c, WALLY_E_ARG, "encode: store must be 16-byte aligned");
+    cudaSetDevice(c->device);
+    EncodeArgs a{};
+    a.kp = c->kp;
+    a.n = c->p.n;
+    a.L = c->p.num_limbs;
+    a.d = c->p.d;
+    a.E = c->E;
+    a.npt = c->npt;
+    a.tw_fwd = c->d_tw_fwd;
+    a.entries = entries_dev;
+    a.pt_li = c->d_pt_li;
+    a.pt_k = c->d_pt_k;
+    a.entry_base = c->d_entry_base;
+    a.size = c->d_size;
+    a.store = (uint32_t *)store_dev;
+    CUDA_OK(c, launch_encode(a, (cudaStream_t)stream, &c->launches));
+    c->store = (const uint32_t *)store_dev;
+    return WALLY_OK;
+}
+
+// ---------------------------------------------------------------------------
+// batches
+// ---------------------------------------------------------------------------
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+WsLayout wally::ws_layout(uint32_t nq, uint32_t n_local, uint32_t n, uint32_t L) {
+    // misc first: its offset (0) does not depend on nq, so wally_check_batch
+    // can find the error word of any batch's workspace.
+    WsLayout w{};
+    size_t o = 0;
+    w.zero_begin = o;
+    w.misc = o; o += sizeof(uint32_t) * kMiscWords;
+    w.counts = o; o += sizeof(uint32_t) * n_local;
+    w.fill = o; o += sizeof(uint32_t) * n_local;
+    w.zero_bytes = o - w.zero_begin;
+    o = align256(o);
+    w.ids = o; o = align256(o + sizeof(uint32_t) * nq);
+    w.resp_off = o; o = align256(o + sizeof(uint64_t) * nq);
+    w.perm = o; o = align256(o + sizeof(uint32_t) * nq);
+    w.seg = o; o = align256(o + sizeof(uint32_t) * n_local);
+    w.item_start = o; o = align256(o + sizeof(uint32_t) * (n_local + 1));
+    w.chat = o; o = align256(o + sizeof(uint32_t) * (size_t)nq * 2 * L * n);
+    w.total = o;
+    return w;
+}
+
+extern "C" int wally_workspace_bytes(const wally_ctx *c, uint32_t nq, size_t *bytes) {
+    if (!c || !bytes) return WALLY_E_ARG;
+    if (!c->loaded) return fail(const_cast<wally_ctx *>(c), WALLY_E_STATE, "load_clusters first");
+    *bytes = ws_layout(nq, c->n_local, c->p.n, c->p.num_limbs).total;
+    return WALLY_OK;
+}
+
+static int layout_impl(const wally_ctx *c, uint32_t nq, const uint32_t *ids, uint64_t *off, uint64_t *total) {
+    uint64_t o = 0;
+    const uint64_t per = 2ull * c->p.n;
+    for (uint32_t q = 0; q < nq; q++) {
+        const uint32_t cl = ids[q];
+        if (cl >= c->total_clusters || c->local_of_cluster[cl] < 0)
+            return fail(const_cast<wally_ctx *>(c), WALLY_E_UNKNOWN_CLUSTER,
+                        "query %u names cluster %u, which is not local (total %u)", q, cl, c->total_clusters);
+        if (off) off[q] = o;
+        o += per * c->pt_of_local[c->local_of_cluster[cl]];
+    }
+    if (off) off[nq] = o;
+    if (total) *total = o;
+    return WALLY_OK;
+}
+
+extern "C" int wally_response_layout(const wally_ctx *c, uint32_t nq, const uint32_t *ids, uint64_t *off,
+                                     uint64_t *total) {
+    if (!c || (nq && !ids)) return WALLY_E_ARG;
+    if (!c->loaded) return fail(const_cast<wally_ctx *>(c), WALLY_E_STATE, "load_clusters first");
+    return layout_impl(c, nq, ids, off, total);
+}
+
+// Evaluate one batch whose query ciphertexts are already on the device.
+static int eval_impl(wally_ctx *c, uint32_t nq, const uint32_t *ids, const uint32_t *query_dev, uint32_t *resp_dev,
+                     uint64_t resp_words, void *ws_dev, size_t ws_bytes, cudaStream_t s) {
+    if (!c->loaded) return fail(c, WALLY_E_STATE, "load_clusters first");
+    if (!c->store) return fail(c, WALLY_E_STATE, "encode_plaintexts_ntt first");
+    if (nq == 0) return WALLY_OK;
+    if (!ids || !query_dev || !resp_dev || !ws_dev) return fail(c, WALLY_E_ARG, "eval: null pointer");
+    if ((uintptr_t)query_dev % 16 || (uintptr_t)ws_dev % 256)
+        return fail(c, WALLY_E_ARG, "eval: query_ct must be 16-byte and workspace 256-byte aligned");
+    const WsLayout w = ws_layout(nq, c->n_local, c->p.n, c->p.num_limbs);
+    if (ws_bytes < w.total) return fail(c, WALLY_E_ARG, "eval: workspace %zu bytes, need %zu", ws_bytes, w.total);
+    // metadata staging slot (pinned); wait until its previous copy finished
+    wally_ctx::Slot &sl = c->slot[c->next_slot];
+    c->next_slot ^= 1;
+    if (sl.pending) { cudaEventSynchronize(sl.done); sl.pending = false; }
+    if (sl.cap < nq) {
+        if (sl.ids) cudaFreeHost(sl.ids);
+        if (sl.off) cudaFreeHost(sl.off);
+        sl.ids = nullptr; sl.off = nullptr; sl.cap = 0;
+        if (cudaMallocHost(&sl.ids, sizeof(uint32_t) * nq) != cudaSuccess ||
+            cudaMallocHost(&sl.off, sizeof(uint64_t) * (nq + 1)) != cudaSuccess)
+            return fail(c, WALLY_E_OOM, "pinned staging allocation failed");
+        sl.cap = nq;
+    }
+    uint64_t total = 0;
+    int rc = layout_impl(c, nq, ids, sl.off, &total);
+    if (rc) return rc;
+    if (resp_words < total) return fail(c, WALLY_E_ARG, "eval: response buffer has %llu words, need %llu",
+                                        (unsigned long long)resp_words, (unsigned long long)total);
+    memcpy(sl.ids, ids, sizeof(uint32_t) * nq);
+    char *ws = (char *)ws_dev;
+    CUDA_OK(c, cudaMemcpyAsync(ws + w.ids, sl.ids, sizeof(uint32_t) * nq, cudaMemcpyHostToDevice, s));
+    CUDA_OK(c, cudaMemcpyAsync(ws + w.resp_off, sl.off, sizeof(uint64_t) * nq, cudaMemcpyHostToDevice, s));
+    CUDA_OK(c, cudaEventRecord(sl.done, s));
+    sl.pending = true;
+    CUDA_OK(c, cudaMemsetAsync(ws + w.zero_begin, 0, w.zero_bytes, s));
+    BatchArgs a{};
+    a.kp = c->kp;
+    a.n = c->p.n;
+    a.L = c->p.num_limbs;
+    a.nq = nq;
+    a.n_local = c->n_local;
+    a.total_clusters = c->total_clusters;
+    a.tw_fwd = c->d_tw_fwd;
+    a.tw_inv = c->d_tw_inv;
+    a.local_of_cluster = c->d_local_of_cluster;
+    a.pt_base = c->d_pt_base;
+    a.n_pt = c->d_n_pt;
+    a.store = c->store;
+    a.query_ct = query_dev;
+    a.resp = resp_dev;
+    a.ids = (uint32_t *)(ws + w.ids);
+    a.resp_off = (uint64_t *)(ws + w.resp_off);
+    a.perm = (uint32_t *)(ws + w.perm);
+    a.counts = (uint32_t *)(ws + w.counts);
+    a.fill = (uint32_t *)(ws + w.fill);
+    a.misc = (uint32_t *)(ws + w.misc);
+    a.seg = (uint32_t *)(ws + w.seg);
+    a.item_start = (uint32_t *)(ws + w.item_start);
+    a.chat = (uint32_t *)(ws + w.chat);
+    std::array<cudaEvent_t, 4> ev{};
+    if (c->timing) {
+        for (auto &e : ev) {
+            if (c->ev_pool.empty()) {
+                CUDA_OK(c, cudaEventCreate(&e));
+            } else {
+                e = c->ev_pool.back();
+                c->ev_pool.pop_back();
+            }
+        }
+        c->ev_rec.push_back(ev);
+        CUDA_OK(c, cudaEventRecord(ev[0], s));
+    }
+    CUDA_OK(c, launch_batcher(a, s, &c->launches));
+    if (c->timing) CUDA_OK(c, cudaEventRecord(ev[1], s));
+    CUDA_OK(c, launch_query_ntt(a, s, &c->launches));
+    if (c->timing) CUDA_OK(c, cudaEventRecord(ev[2], s));
+    CUDA_OK(c, launch_eval(a, s, c->num_sms, &c->launches));
+    if (c->timing) CUDA_OK(c, cudaEventRecord(ev[3], s));
+    return WALLY_OK;
+}
+
+extern "C" int wally_enable_stage_timing(wally_ctx *c, int enable) {
+    if (!c) return WALLY_E_ARG;
+    c->timing = enable != 0;
+    return WALLY_OK;
+}
+
+extern "C" int wally_stage_times(wally_ctx *c, double *ms, uint64_t *batches) {
+    if (!c || !ms) return WALLY_E_ARG;
+    cudaSetDevice(c->device);
+    ms[0] = ms[1] = ms[2] = 0.0;
+    for (auto &r : c->ev_rec) {
+        CUDA_OK(c, cudaEventSynchronize(r[3]));
+        for (int i = 0; i < 3; i++) {
+            float t = 0.f;
+            CUDA_OK(c, cudaEventElapsedTime(&t, r[i], r[i + 1]));
+            ms[i] += t;
+        }
+    }
+    if (batches) *batches = c->ev_rec.size();
+    for (auto &r : c->ev_rec) for (auto e : r) c->ev_pool.push_back(e);
+    c->ev_rec.clear();
+    return WALLY_OK;
+}
+
+extern "C" int wally_eval_batch(wally_ctx *c, uint32_t nq, const uint32_t *ids, const uint32_t *query_dev,
+                                uint32_t *resp_dev, uint64_t resp_words, void *ws_dev, size_t ws_bytes, void *stream) {
+    if (!c) return WALLY_E_ARG;
+    cudaSetDevice(c->device);
+    return eval_impl(c, nq, ids, query_dev, resp_dev, resp_words, ws_dev, ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int wally_check_batch(wally_ctx *c, const void *ws_dev, void *stream) {
+    if (!c || !ws_dev) return WALLY_E_ARG;
+    cudaSetDevice(c->device);
+    CUDA_OK(c, cudaStreamSynchronize((cudaStream_t)stream));
+    uint32_t misc[kMiscWords];
+    CUDA_OK(c, cudaMemcpy(misc, ws_dev, sizeof misc, cudaMemcpyDeviceToHost));
+    if (misc[kMiscErr] & kErrResidue)
+        return fail(c, WALLY_E_RESIDUE, "a query ciphertext residue was >= its modulus");
+    return WALLY_OK;
+}
+
+extern "C" int wally_fetch_responses(wally_ctx *c, const uint32_t *resp_dev, uint64_t words, uint32_t *out_host,
+                                     void *stream) {
+    if (!c || (words && (!resp_dev || !out_host))) return WALLY_E_ARG;
+    cudaSetDevice(c->device);
+    CUDA_OK(c, cudaMemcpyAsync(out_host, resp_dev, words * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                               (cudaStream_t)stream));
+    CUDA_OK(c, cudaStreamSynchronize((cudaStream_t)stream));
+    return WALLY_OK;
+}
+
+extern "C" int wally_route_queries(const wally_ctx *c, uint32_t nq, const uint32_t *ids, int32_t *dest) {
+    if (!c || (nq && (!ids || !dest))) return WALLY_E_ARG;
+    if (!c->loaded) return fail(const_cast<wally_ctx *>(c), WALLY_E_STATE, "load_clusters first");
+    for (uint32_t q = 0; q < nq; q++) {
+        if (ids[q] >= c->total_clusters)
+            return fail(const_cast<wally_ctx *>(c), WALLY_E_UNKNOWN_CLUSTER, "query %u: cluster %u >= %u", q, ids[q],
+                        c->total_clusters);
+        dest[q] = c->owner.empty() ? c->rank : c->owner[ids[q]];
+    }
+    return WALLY_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host-buffer serving pipeline
+// ---------------------------------------------------------------------------
+struct HostWs {
+    size_t ws, qstage, rstage, per_slot, total;
+};
+static HostWs host_ws(const wally_ctx *c, uint32_t sub) {
+    HostWs h{};
+    h.ws = align256(ws_layout(sub, c->n_local, c->p.n, c->p.num_limbs).total);
+    h.qstage = align256((size_t)sub * 2 * c->p.num_limbs * c->p.n * sizeof(uint32_t));
+    h.rstage = align256((size_t)sub * c->max_pt * 2 * c->p.n * sizeof(uint32_t));
+    h.per_slot = h.ws + h.qstage + h.rstage;
+    h.total = 2 * h.per_slot;
+    return h;
+}
+
+extern "C" int wally_host_workspace_bytes(const wally_ctx *c, uint32_t sub, size_t *bytes) {
+    if (!c || !bytes || sub == 0) return WALLY_E_ARG;
+    if (!c->loaded) return fail(const_cast<wally_ctx *>(c), WALLY_E_STATE, "load_clusters first");
+    *bytes = host_ws(c, sub).total;
+    return WALLY_OK;
+}
+
+extern "C" int wally_eval_batch_host(wally_ctx *c, uint32_t nq, const uint32_t *ids, const uint32_t *query_host,
+                                     uint32_t *resp_host, uint64_t resp_words, uint32_t sub, void *ws_dev,
+                                     size_t ws_bytes, void *stream) {
+    if (!c) return WALLY_E_ARG;
+    if (!c->loaded) return fail(c, WALLY_E_STATE, "load_clusters first");
+    if (!c->store) return fail(c, WALLY_E_STATE, "encode_plaintexts_ntt first");
+    if (nq == 0) return WALLY_OK;
+    if (!ids || !query_host || !resp_host || !ws_dev || sub == 0) return fail(c, WALLY_E_ARG, "eval_host: bad args");
+    cudaSetDevice(c->device);
+    const HostWs h = host_ws(c, sub);
+    if (ws_bytes < h.total) return fail(c, WALLY_E_ARG, "eval_host: workspace %zu bytes, need %zu", ws_bytes, h.total);
+    std::vector<uint64_t> off(nq + 1);
+    uint64_t total = 0;
+    int rc = layout_impl(c, nq, ids, off.data(), &total);
+    if (rc) return rc;
+    if (resp_words < total) return fail(c, WALLY_E_ARG, "eval_host: response buffer too small");
+    cudaStream_t st[2] = {(cudaStream_t)stream, c->side};
+    cudaEvent_t start;
+    CUDA_OK(c, cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    CUDA_OK(c, cudaEventRecord(start, st[0]));
+    CUDA_OK(c, cudaStreamWaitEvent(st[1], start, 0));
+    const size_t qwords = 2ull * c->p.num_limbs * c->p.n;
+    uint32_t b = 0;
+    for (uint32_t q0 = 0; q0 < nq; q0 += sub, b++) {
+        const uint32_t cnt = std::min(sub, nq - q0);
+        const int k = b & 1;
+        cudaStream_t s = st[k];
+        char *base = (char *)ws_dev + k * h.per_slot;
+        uint32_t *qdev = (uint32_t *)(base + h.ws);
+        uint32_t *rdev = (uint32_t *)(base + h.ws + h.qstage);
+        CUDA_OK(c, cudaMemcpyAsync(qdev, query_host + q0 * qwords, cnt * qwords * sizeof(uint32_t),
+                                   cudaMemcpyHostToDevice, s));
+        const uint64_t words = off[q0 + cnt] - off[q0];
+        rc = eval_impl(c, cnt, ids + q0, qdev, rdev, words, base, h.ws, s);
+        if (rc) { cudaEventDestroy(start); return rc; }
+        CUDA_OK(c, cudaMemcpyAsync(resp_host + off[q0], rdev, words * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    }
+    cudaEventDestroy(start);
+    CUDA_OK(c, cudaStreamSynchronize(st[1]));
+    CUDA_OK(c, cudaStreamSynchronize(st[0]));
+    return WALLY_OK;
+}
+
+// ---------------------------------------------------------------------------
+// test hooks
+// ---------------------------------------------------------------------------
+extern "C" int wally_ntt_forward(wally_ctx *c, const uint32_t *in, uint32_t *out, uint32_t count, void *stream) {
+    if (!c || (count && (!in || !out))) return WALLY_E_ARG;
+    if ((uintptr_t)out % 16) return fail(c, WALLY_E_ARG, "ntt_forward: out must be 16-byte aligned");
+    cudaSetDevice(c->device);
+    CUDA_OK(c, launch_ntt_forward(c->kp, c->p.n, c->p.num_limbs, c->d_tw_fwd, in, out, count, nullptr,
+                                  (cudaStream_t)stream, &c->launches));
+    return WALLY_OK;
+}
+
+extern "C" int wally_ntt_inverse(wally_ctx *c, const uint32_t *in, uint32_t *out, uint32_t count, void *stream) {
+    if (!c || (count && (!in || !out))) return WALLY_E_ARG;
+    if ((uintptr_t)in % 16) return fail(c, WALLY_E_ARG, "ntt_inverse: in must be 16-byte aligned");
+    cudaSetDevice(c->device);
+    CUDA_OK(c, launch_ntt_inverse(c->kp, c->p.n, c->p.num_limbs, c->d_tw_inv, in, out, count, (cudaStream_t)stream,
+                                  &c->launches));
+    return WALLY_OK;
+}

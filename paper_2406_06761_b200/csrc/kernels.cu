@@ -1,0 +1,481 @@
+// sm_100a kernels of the Wally server hot path.
+//
+//   encode_kernel        a0  ServerInit: pack entries (reversed, offsets j*d),
+//                            lift mod q_i, forward NTT, fold constants, Shoup companion
+//   batch_count/scan/    a1  group the batch by cluster id, build the work list
+//   scatter kernels
+//   ntt_forward_kernel   a2  forward negacyclic NTT of every query polynomial
+//   eval_kernel          a3-a6 fused: pointwise Shoup modmul, inverse NTT,
+//                            RNS modulus switch to q_0, response write
+//
+// Citations: PAPER.md P:L1000 / P:L1467-1472 (Harvey NTT, lazy reduction),
+// P:L1003 / P:L1318-1324 (modulus switch to q_0), Alg 1 P:L664-687 and
+// Alg 4 P:L794-808 (ServerInit / ServerComputation).
+
+#include <cstdint>
+
+#include "ntt_device.cuh"
+#include "wally_internal.h"
+
+namespace wally {
+
+// ---------------------------------------------------------------------------
+// a2: forward NTT of query polynomials (and of any [count][L][n] array)
+// ---------------------------------------------------------------------------
+template <int N>
+__global__ void __launch_bounds__(NttGeom<N>::T) ntt_forward_kernel(KParams kp, uint32_t L, const uint2 *__restrict__ tw,
+                                                                    const uint32_t *__restrict__ in,
+                                                                    uint32_t *__restrict__ out, uint32_t *err) {
+    using Gm = NttGeom<N>;
+    constexpr int V = Gm::V;
+    extern __shared__ uint32_t smem[];
+    uint32_t *bufA = smem, *bufB = smem + Gm::SMEM_WORDS;
+    const int g = threadIdx.x;
+    const size_t poly = blockIdx.x;
+    const uint32_t limb = (uint32_t)(poly % L);
+    const uint32_t q = kp.q[limb], q2 = kp.q2[limb];
+    const uint32_t *src = in + poly * N;
+    uint32_t a[V];
+    bool bad = false;
+    // pass-2 groups: element idx = hi*TB2*R2 + k*TB2 + lo  (coalesced across threads)
+#pragma unroll
+    for (int j = 0; j < V / Gm::R2; j++)
+#pragma unroll
+        for (int k = 0; k < Gm::R2; k++) {
+            uint32_t x = __ldg(src + pass_index<N, Gm::TB2, Gm::R2>(g, j, k));
+            bad |= (x >= q);
+            a[j * Gm::R2 + k] = x;
+        }
+    if (bad && err) atomicOr(err, (uint32_t)kErrResidue);
+    ntt_chain<N>(a, tw + (size_t)limb * N, g, q, q2, bufA, bufB);
+    uint4 *dst = reinterpret_cast<uint4 *>(out + poly * N + (size_t)g * V);
+#pragma unroll
+    for (int v = 0; v < V / 4; v++) dst[v] = make_uint4(a[4 * v], a[4 * v + 1], a[4 * v + 2], a[4 * v + 3]);
+}
+
+// Debug/test inverse NTT: out = n^{-1} INTT(in), canonical.
+template <int N>
+__global__ void __launch_bounds__(NttGeom<N>::T) ntt_inverse_kernel(KParams kp, uint32_t L, const uint2 *__restrict__ tw,
+                                                                    const uint32_t *__restrict__ in,
+                                                                    uint32_t *__restrict__ out) {
+    using Gm = NttGeom<N>;
+    constexpr int V = Gm::V;
+    extern __shared__ uint32_t smem[];
+    uint32_t *bufA = smem, *bufB = smem + Gm::SMEM_WORDS;
+    const int g = threadIdx.x;
+    const size_t poly = blockIdx.x;
+    const uint32_t limb = (uint32_t)(poly % L);
+    const uint32_t q = kp.q[limb], q2 = kp.q2[limb];
+    uint32_t a[V];
+    const uint4 *src = reinterpret_cast<const uint4 *>(in + poly * N + (size_t)g * V);
+#pragma unroll
+    for (int v = 0; v < V / 4; v++) {
+        uint4 x = __ldg(src + v);
+        // any 32-bit residue -> [0, 2q): x mod q via one Shoup multiply by 1
+        a[4 * v] = x.x;
+        a[4 * v + 1] = x.y;
+        a[4 * v + 2] = x.z;
+        a[4 * v + 3] = x.w;
+    }
+#pragma unroll
+    for (int v = 0; v < V; v++) a[v] = shoup_mul(a[v], kp.ninv[limb], kp.ninvp[limb], q);  // scale first (linear)
+    intt_chain<N>(a, tw + (size_t)limb * N, g, q, q2, bufA, bufB);
+    uint32_t *dst = out + poly * N;
+#pragma unroll
+    for (int j = 0; j < V / Gm::R2; j++)
+#pragma unroll
+        for (int k = 0; k < Gm::R2; k++)
+            dst[pass_index<N, Gm::TB2, Gm::R2>(g, j, k)] = csub(a[j * Gm::R2 + k], q);
+}
+
+// ---------------------------------------------------------------------------
+// a0: plaintext encoding (ServerInit)
+// ---------------------------------------------------------------------------
+template <int N>
+__global__ void __launch_bounds__(NttGeom<N>::T) encode_kernel(EncodeArgs ea) {
+    using Gm = NttGeom<N>;
+    constexpr int V = Gm::V;
+    extern __shared__ uint32_t smem[];
+    uint32_t *bufA = smem, *bufB = smem + Gm::SMEM_WORDS;
+    const int g = threadIdx.x;
+    const uint32_t pt = blockIdx.x, limb = blockIdx.y;
+    const uint32_t q = ea.kp.q[limb], q2 = ea.kp.q2[limb];
+    const uint32_t li = ea.pt_li[pt], k = ea.pt_k[pt];
+    const uint32_t first = k * ea.E;  // first entry of this plaintext inside the cluster
+    const uint32_t size = ea.size[li];
+    const uint32_t count = min(ea.E, size - first);
+    const int8_t *ent = ea.entries + (ea.entry_base[li] + first) * (uint64_t)ea.d;
+    uint32_t a[V];
+#pragma unroll
+    for (int j = 0; j < V / Gm::R2; j++)
+#pragma unroll
+        for (int kk = 0; kk < Gm::R2; kk++) {
+            // coefficient position pos = j'*d + d - 1 - i holds entry j', component i
+            const uint32_t pos = pass_index<N, Gm::TB2, Gm::R2>(g, j, kk);
+            const uint32_t jj = pos / ea.d, i = ea.d - 1 - pos % ea.d;
+            int32_t x = 0;
+            if (jj < count) x = ent[(size_t)jj * ea.d + i];
+            a[j * Gm::R2 + kk] = (x < 0) ? (uint32_t)((int64_t)q + x) : (uint32_t)x;  // x mod q (reading S8)
+        }
+    ntt_chain<N>(a, ea.tw_fwd + (size_t)limb * N, g, q, q2, bufA, bufB);
+    uint32_t *dst = ea.store + ((size_t)pt * ea.L + limb) * 2 * N + (size_t)g * V;
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+        uint32_t y = csub(shoup_mul(a[v], ea.kp.fold[limb], ea.kp.foldp[limb], q), q);  // canonical
+        dst[v] = y;
+        dst[N + v] = (uint32_t)(((uint64_t)y << 32) / q);                               // Shoup companion
+    }
+}
+
+// ---------------------------------------------------------------------------
+// a1: batcher
+// ---------------------------------------------------------------------------
+__global__ void batch_count_kernel(const uint32_t *__restrict__ ids, uint32_t nq,
+                                   const int32_t *__restrict__ local_of_cluster, uint32_t total_clusters,
+                                   uint32_t *__restrict__ counts) {
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
+        uint32_t c = ids[q];
+        int32_t li = c < total_clusters ? local_of_cluster[c] : -1;
+        if (li >= 0) atomicAdd(&counts[li], 1u);
+    }
+}
+
+// One CTA of 1024 threads: exclusive scans of query counts (segment starts)
+// and of work items  P_c * ceil(count_c / chunk)  (item starts).
+__global__ void __launch_bounds__(1024) batch_scan_kernel(const uint32_t *__restrict__ counts, uint32_t n_local,
+                                                          const uint32_t *__restrict__ n_pt, uint32_t chunk,
+                                                          uint32_t *__restrict__ seg, uint32_t *__restrict__ item_start,
+                                                          uint32_t *__restrict__ misc) {
+    __shared__ uint32_t wsum_q[32], wsum_i[32];
+    const uint32_t tid = threadIdx.x, per = (n_local + 1023) / 1024;
+    const uint32_t b = tid * per, e = min(n_local, b + per);
+    uint32_t sq = 0, si = 0;
+    for (uint32_t i = b; i < e; i++) {
+        uint32_t c = counts[i];
+        sq += c;
+        si += n_pt[i] * ((c + chunk - 1) / chunk);
+    }
+    // block exclusive scan of (sq, si)
+    uint32_t iq = sq, ii = si;
+    const int lane = tid & 31, w = tid >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t xq = __shfl_up_sync(0xffffffffu, iq, o), xi = __shfl_up_sync(0xffffffffu, ii, o);
+        if (lane >= o) { iq += xq; ii += xi; }
+    }
+    if (lane == 31) { wsum_q[w] = iq; wsum_i[w] = ii; }
+    __syncthreads();
+    if (w == 0) {
+        uint32_t vq = wsum_q[lane], vi = wsum_i[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t xq = __shfl_up_sync(0xffffffffu, vq, o), xi = __shfl_up_sync(0xffffffffu, vi, o);
+            if (lane >= o) { vq += xq; vi += xi; }
+        }
+        wsum_q[lane] = vq;
+        wsum_i[lane] = vi;
+    }
+    __syncthreads();
+    uint32_t oq = iq - sq + (w ? wsum_q[w - 1] : 0), oi = ii - si + (w ? wsum_i[w - 1] : 0);
+    for (uint32_t i = b; i < e; i++) {
+        uint32_t c = counts[i];
+        seg[i] = oq;
+        item_start[i] = oi;
+        oq += c;
+        oi += n_pt[i] * ((c + chunk - 1) / chunk);
+    }
+    if (tid == 1023) {
+        item_start[n_local] = oi;
+        misc[kMiscTotalItems] = oi;
+    }
+}
+
+__global__ void batch_scatter_kernel(const uint32_t *__restrict__ ids, uint32_t nq,
+                                     const int32_t *__restrict__ local_of_cluster, uint32_t total_clusters,
+                                     const uint32_t *__restrict__ seg, uint32_t *__restrict__ fill,
+                                     uint32_t *__restrict__ perm) {
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
+        uint32_t c = ids[q];
+        int32_t li = c < total_clusters ? local_of_cluster[c] : -1;
+        if (li >= 0) perm[seg[li] + atomicAdd(&fill[li], 1u)] = q;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// a3-a6: fused pointwise modmul + inverse NTT + modulus switch + write
+// ---------------------------------------------------------------------------
+
+// ((h_m - (r mod q_l)) * C[l][m]) mod q_l, canonical; r < q_m < 2 q_l.
+__device__ __forceinline__ uint32_t ms_term(uint32_t r, uint32_t h_m, uint32_t q_l, uint32_t C, uint32_t Cp) {
+    uint32_t rl = csub(r, q_l);
+    return csub(shoup_mul(h_m + q_l - rl, C, Cp, q_l), q_l);
+}
+
+// Modulus-switch bookkeeping after the inverse NTT of limb J (limbs are
+// processed L-1, ..., 0).  y = a[] holds c_J * F_J in [0, 2q_J) where the fold
+// F_J = prod_{k>J} q_k^{-1} was applied through the plaintext.  Implements
+// the sequential drop-last rounding (reading S7):
+//   r_m = (c_m + h_m) mod q_m,  c_l <- (c_l + h_m - r_m) q_m^{-1}  for l < m,
+// accumulating  A_l = sum_{m>l} (h_m - r_m) prod_{k=l+1..m} q_k^{-1}  so that
+// c_l(final) = c_l F_l + A_l.  Limb 0's final value is the response word.
+template <int L, int J, int V, int NA>
+__device__ __forceinline__ void ms_step(uint32_t (&a)[V], uint32_t (&rtop)[V], uint32_t (&acc)[NA][V],
+                                        const KParams &kp) {
+    const uint32_t qj = kp.q[J];
+#pragma unroll
+    for (int v = 0; v < V; v++) a[v] = csub(a[v], qj);
+    if constexpr (L == 1) {
+        return;
+    } else if constexpr (J == L - 1) {
+#pragma unroll
+        for (int v = 0; v < V; v++) rtop[v] = csub(a[v] + kp.h[J], qj);
+    } else {
+#pragma unroll
+        for (int v = 0; v < V; v++) {
+            uint32_t A;
+            if constexpr (J == L - 2)
+                A = ms_term(rtop[v], kp.h[L - 1], qj, kp.C[J][L - 1], kp.Cp[J][L - 1]);
+            else
+                A = acc[J][v];
+            a[v] = csub(a[v] + A, qj);
+        }
+        if constexpr (J > 0) {
+#pragma unroll
+            for (int v = 0; v < V; v++) {
+                const uint32_t r = csub(a[v] + kp.h[J], qj);
+#pragma unroll
+                for (int l = 0; l < J; l++) {
+                    const uint32_t ql = kp.q[l];
+                    const uint32_t term = ms_term(r, kp.h[J], ql, kp.C[l][J], kp.Cp[l][J]);
+                    if constexpr (J == L - 2)
+                        acc[l][v] = csub(ms_term(rtop[v], kp.h[L - 1], ql, kp.C[l][L - 1], kp.Cp[l][L - 1]) + term, ql);
+                    else
+                        acc[l][v] = csub(acc[l][v] + term, ql);
+                }
+            }
+        }
+    }
+}
+
+template <int N, int L, int J>
+__device__ __forceinline__ void eval_limb(uint32_t (&a)[NttGeom<N>::V], uint32_t (&rtop)[NttGeom<N>::V],
+                                          uint32_t (&acc)[(L > 2) ? (L - 2) : 1][NttGeom<N>::V], const BatchArgs &ba,
+                                          const uint32_t *chat_q, const uint32_t *phat, int g, uint32_t *bufA,
+                                          uint32_t *bufB) {
+    using Gm = NttGeom<N>;
+    constexpr int V = Gm::V;
+    const uint32_t q = ba.kp.q[J], q2 = ba.kp.q2[J];
+    const uint4 *cs = reinterpret_cast<const uint4 *>(chat_q + (size_t)J * N + (size_t)g * V);
+    const uint4 *ps = reinterpret_cast<const uint4 *>(phat + (size_t)J * 2 * N + (size_t)g * V);
+    const uint4 *pps = reinterpret_cast<const uint4 *>(phat + (size_t)J * 2 * N + N + (size_t)g * V);
+#pragma unroll
+    for (int v = 0; v < V / 4; v++) {
+        const uint4 c = __ldg(cs + v), p = __ldg(ps + v), pp = __ldg(pps + v);
+        a[4 * v + 0] = shoup_mul(c.x, p.x, pp.x, q);
+        a[4 * v + 1] = shoup_mul(c.y, p.y, pp.y, q);
+        a[4 * v + 2] = shoup_mul(c.z, p.z, pp.z, q);
+        a[4 * v + 3] = shoup_mul(c.w, p.w, pp.w, q);
+    }
+    intt_chain<N>(a, ba.tw_inv + (size_t)J * N, g, q, q2, bufA, bufB);
+    ms_step<L, J, V>(a, rtop, acc, ba.kp);
+}
+
+template <int N, int L, int J>
+struct LimbLoop {
+    static __device__ __forceinline__ void run(uint32_t (&a)[NttGeom<N>::V], uint32_t (&rtop)[NttGeom<N>::V],
+                                               uint32_t (&acc)[(L > 2) ? (L - 2) : 1][NttGeom<N>::V],
+                                               const BatchArgs &ba, const uint32_t *chat_q, const uint32_t *phat, int g,
+                                               uint32_t *bufA, uint32_t *bufB) {
+        eval_limb<N, L, J>(a, rtop, acc, ba, chat_q, phat, g, bufA, bufB);
+        LimbLoop<N, L, J - 1>::run(a, rtop, acc, ba, chat_q, phat, g, bufA, bufB);
+    }
+};
+template <int N, int L>
+struct LimbLoop<N, L, -1> {
+    static __device__ __forceinline__ void run(uint32_t (&)[NttGeom<N>::V], uint32_t (&)[NttGeom<N>::V],
+                                               uint32_t (&)[(L > 2) ? (L - 2) : 1][NttGeom<N>::V], const BatchArgs &,
+                                               const uint32_t *, const uint32_t *, int, uint32_t *, uint32_t *) {}
+};
+
+template <int N, int L>
+__global__ void __launch_bounds__(NttGeom<N>::T, (N <= 4096) ? 2 : 1) eval_kernel(BatchArgs ba) {
+    using Gm = NttGeom<N>;
+    constexpr int V = Gm::V;
+    constexpr int NA = (L > 2) ? (L - 2) : 1;
+    extern __shared__ uint32_t smem[];
+    uint32_t *bufA = smem, *bufB = smem + Gm::SMEM_WORDS;
+    __shared__ uint32_t s_item[2];
+    const int g = threadIdx.x;
+    const uint32_t total = ba.misc[kMiscTotalItems];
+    for (uint32_t it = 0;; it++) {
+        if (g == 0) s_item[it & 1] = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
+        __syncthreads();
+        const uint32_t item = s_item[it & 1];
+        if (item >= total) break;
+        // local cluster: last li with item_start[li] <= item
+        uint32_t lo = 0, hi = ba.n_local;  // item_start[lo] <= item < item_start[hi]
+        while (hi - lo > 1) {
+            uint32_t mid = (lo + hi) >> 1;
+            if (ba.item_start[mid] <= item) lo = mid; else hi = mid;
+        }
+        const uint32_t li = lo;
+        const uint32_t cnt = ba.counts[li];
+        const uint32_t nch = (cnt + kQueryChunk - 1) / kQueryChunk;
+        const uint32_t local = item - ba.item_start[li];
+        const uint32_t k = local / nch, ch = local % nch;
+        const uint32_t qb = ba.seg[li] + ch * kQueryChunk;
+        const uint32_t qe = min(qb + kQueryChunk, ba.seg[li] + cnt);
+        const uint32_t *phat = ba.store + (size_t)(ba.pt_base[li] + k) * L * 2 * N;
+        for (uint32_t qi = qb; qi < qe; qi++) {
+            const uint32_t qo = ba.perm[qi];
+            uint32_t *out_q = ba.resp + ba.resp_off[qo] + (size_t)k * 2 * N;
+#pragma unroll 1
+            for (int comp = 0; comp < 2; comp++) {
+                uint32_t a[V], rtop[V], acc[NA][V];
+                const uint32_t *chat_q = ba.chat + ((size_t)qo * 2 + comp) * L * N;
+                LimbLoop<N, L, L - 1>::run(a, rtop, acc, ba, chat_q, phat, g, bufA, bufB);
+                uint32_t *dst = out_q + (size_t)comp * N;
+#pragma unroll
+                for (int j = 0; j < V / Gm::R2; j++)
+#pragma unroll
+                    for (int kk = 0; kk < Gm::R2; kk++)
+                        __stcs(dst + pass_index<N, Gm::TB2, Gm::R2>(g, j, kk), a[j * Gm::R2 + kk]);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+template <int N>
+static constexpr size_t chain_smem() { return 2 * NttGeom<N>::SMEM_WORDS * sizeof(uint32_t); }
+
+template <typename K>
+static cudaError_t allow_smem(K kernel, size_t bytes) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+template <int N>
+static cudaError_t launch_encode_n(const EncodeArgs &a, cudaStream_t s) {
+    dim3 grid(a.npt, a.L);
+    cudaError_t e = allow_smem(encode_kernel<N>, chain_smem<N>());
+    if (e != cudaSuccess) return e;
+    encode_kernel<N><<<grid, NttGeom<N>::T, chain_smem<N>(), s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_encode(const EncodeArgs &a, cudaStream_t s, uint64_t *launches) {
+    if (a.npt == 0) return cudaSuccess;
+    *launches += 1;
+    switch (a.n) {
+        case 1024: return launch_encode_n<1024>(a, s);
+        case 2048: return launch_encode_n<2048>(a, s);
+        case 4096: return launch_encode_n<4096>(a, s);
+        case 8192: return launch_encode_n<8192>(a, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <int N>
+static cudaError_t launch_fwd_n(const KParams &kp, uint32_t L, const uint2 *tw, const uint32_t *in, uint32_t *out,
+                                uint32_t count, uint32_t *err, cudaStream_t s) {
+    cudaError_t e = allow_smem(ntt_forward_kernel<N>, chain_smem<N>());
+    if (e != cudaSuccess) return e;
+    ntt_forward_kernel<N><<<(unsigned)(count * L), NttGeom<N>::T, chain_smem<N>(), s>>>(kp, L, tw, in, out, err);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ntt_forward(const KParams &kp, uint32_t n, uint32_t L, const uint2 *tw_fwd, const uint32_t *in,
+                               uint32_t *out, uint32_t count, uint32_t *err, cudaStream_t s, uint64_t *launches) {
+    if (count == 0) return cudaSuccess;
+    *launches += 1;
+    switch (n) {
+        case 1024: return launch_fwd_n<1024>(kp, L, tw_fwd, in, out, count, err, s);
+        case 2048: return launch_fwd_n<2048>(kp, L, tw_fwd, in, out, count, err, s);
+        case 4096: return launch_fwd_n<4096>(kp, L, tw_fwd, in, out, count, err, s);
+        case 8192: return launch_fwd_n<8192>(kp, L, tw_fwd, in, out, count, err, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <int N>
+static cudaError_t launch_inv_n(const KParams &kp, uint32_t L, const uint2 *tw, const uint32_t *in, uint32_t *out,
+                                uint32_t count, cudaStream_t s) {
+    cudaError_t e = allow_smem(ntt_inverse_kernel<N>, chain_smem<N>());
+    if (e != cudaSuccess) return e;
+    ntt_inverse_kernel<N><<<(unsigned)(count * L), NttGeom<N>::T, chain_smem<N>(), s>>>(kp, L, tw, in, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ntt_inverse(const KParams &kp, uint32_t n, uint32_t L, const uint2 *tw_inv, const uint32_t *in,
+                               uint32_t *out, uint32_t count, cudaStream_t s, uint64_t *launches) {
+    if (count == 0) return cudaSuccess;
+    *launches += 1;
+    switch (n) {
+        case 1024: return launch_inv_n<1024>(kp, L, tw_inv, in, out, count, s);
+        case 2048: return launch_inv_n<2048>(kp, L, tw_inv, in, out, count, s);
+        case 4096: return launch_inv_n<4096>(kp, L, tw_inv, in, out, count, s);
+        case 8192: return launch_inv_n<8192>(kp, L, tw_inv, in, out, count, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <int N, int L>
+static cudaError_t launch_eval_nl(const BatchArgs &a, cudaStream_t s, int num_sms) {
+    using Gm = NttGeom<N>;
+    const size_t smem = 2 * Gm::SMEM_WORDS * sizeof(uint32_t);
+    static bool configured = false;
+    static int blocks_per_sm = 1;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(eval_kernel<N, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, eval_kernel<N, L>, Gm::T, smem);
+        if (e != cudaSuccess) return e;
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+        configured = true;
+    }
+    eval_kernel<N, L><<<num_sms * blocks_per_sm, Gm::T, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int N>
+static cudaError_t launch_eval_n(const BatchArgs &a, cudaStream_t s, int num_sms) {
+    switch (a.L) {
+        case 1: return launch_eval_nl<N, 1>(a, s, num_sms);
+        case 2: return launch_eval_nl<N, 2>(a, s, num_sms);
+        case 3: return launch_eval_nl<N, 3>(a, s, num_sms);
+        case 4: return launch_eval_nl<N, 4>(a, s, num_sms);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_batcher(const BatchArgs &a, cudaStream_t s, uint64_t *launches) {
+    if (a.nq == 0) return cudaSuccess;
+    const unsigned threads = 256;
+    const unsigned blocks = (a.nq + threads - 1) / threads;
+    batch_count_kernel<<<blocks, threads, 0, s>>>(a.ids, a.nq, a.local_of_cluster, a.total_clusters, a.counts);
+    batch_scan_kernel<<<1, 1024, 0, s>>>(a.counts, a.n_local, a.n_pt, kQueryChunk, a.seg, a.item_start, a.misc);
+    batch_scatter_kernel<<<blocks, threads, 0, s>>>(a.ids, a.nq, a.local_of_cluster, a.total_clusters, a.seg, a.fill,
+                                                    a.perm);
+    *launches += 3;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_query_ntt(const BatchArgs &a, cudaStream_t s, uint64_t *launches) {
+    return launch_ntt_forward(a.kp, a.n, a.L, a.tw_fwd, a.query_ct, a.chat, 2 * a.nq, a.misc + kMiscErr, s, launches);
+}
+
+cudaError_t launch_eval(const BatchArgs &a, cudaStream_t s, int num_sms, uint64_t *launches) {
+    if (a.nq == 0) return cudaSuccess;
+    *launches += 1;
+    switch (a.n) {
+        case 1024: return launch_eval_n<1024>(a, s, num_sms);
+        case 2048: return launch_eval_n<2048>(a, s, num_sms);
+        case 4096: return launch_eval_n<4096>(a, s, num_sms);
+        case 8192: return launch_eval_n<8192>(a, s, num_sms);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace wally

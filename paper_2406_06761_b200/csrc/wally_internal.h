@@ -1,0 +1,96 @@
+// Internal declarations shared by the host C-ABI (capi.cpp) and the kernels
+// (kernels.cu).  Not part of the public ABI (include/wally.h).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "wally.h"
+
+namespace wally {
+
+constexpr int kMaxLimbs = WALLY_MAX_LIMBS;
+// Queries per work item of the fused kernel (a query chunk of one cluster
+// shares every staged plaintext).
+constexpr uint32_t kQueryChunk = 8;
+
+// Per-limb constants, passed by value to every kernel (kernel parameter
+// space -> constant bank, uniform across the grid).
+struct KParams {
+    uint32_t q[kMaxLimbs];        // moduli, ascending
+    uint32_t q2[kMaxLimbs];       // 2 q
+    uint32_t h[kMaxLimbs];        // floor(q/2): rounding offset of the drop-last step
+    uint32_t ninv[kMaxLimbs];     // n^{-1} mod q       (debug inverse NTT)
+    uint32_t ninvp[kMaxLimbs];    //   Shoup companion
+    uint32_t fold[kMaxLimbs];     // F_l = n^{-1} prod_{k>l} q_k^{-1} mod q_l (folded into plaintexts)
+    uint32_t foldp[kMaxLimbs];    //   Shoup companion
+    uint32_t C[kMaxLimbs][kMaxLimbs];   // C[l][m] = prod_{k=l+1..m} q_k^{-1} mod q_l, l < m
+    uint32_t Cp[kMaxLimbs][kMaxLimbs];  //   Shoup companions
+};
+
+// Workspace layout of one batch (device), offsets in bytes.
+struct WsLayout {
+    size_t ids, resp_off, perm, counts, fill, misc, seg, item_start, chat, total;
+    size_t zero_begin, zero_bytes;  // region cleared at the start of every batch
+};
+WsLayout ws_layout(uint32_t nq, uint32_t n_local, uint32_t n, uint32_t L);
+
+// misc[] words in the workspace
+enum { kMiscTotalItems = 0, kMiscWorkCounter = 1, kMiscErr = 2, kMiscWords = 4 };
+enum { kErrResidue = 1u };
+
+struct BatchArgs {
+    KParams kp;
+    uint32_t n, L;
+    uint32_t nq;
+    uint32_t n_local;
+    uint32_t total_clusters;
+    const uint2 *tw_fwd;          // [L][n] (w, w') psi^{brev(i)}
+    const uint2 *tw_inv;          // [L][n] (w, w') psi^{-brev(i)}
+    const int32_t *local_of_cluster;  // [total_clusters]
+    const uint32_t *pt_base;      // [n_local]
+    const uint32_t *n_pt;         // [n_local]
+    const uint32_t *store;        // [npt][L][2][n]
+    const uint32_t *query_ct;     // [nq][2][L][n]
+    uint32_t *resp;
+    // workspace pieces
+    uint32_t *ids;
+    uint64_t *resp_off;
+    uint32_t *perm;
+    uint32_t *counts;
+    uint32_t *fill;
+    uint32_t *misc;
+    uint32_t *seg;
+    uint32_t *item_start;
+    uint32_t *chat;               // [nq][2][L][n]
+};
+
+struct EncodeArgs {
+    KParams kp;
+    uint32_t n, L, d, E;
+    uint32_t npt;
+    const uint2 *tw_fwd;
+    const int8_t *entries;        // [local entries][d]
+    const uint32_t *pt_li;        // [npt] local cluster of each plaintext
+    const uint32_t *pt_k;         // [npt] index of the plaintext in its cluster
+    const uint64_t *entry_base;   // [n_local] first entry row of each local cluster
+    const uint32_t *size;         // [n_local] entries of each local cluster
+    uint32_t *store;              // [npt][L][2][n]
+};
+
+// Kernel launchers (kernels.cu).  Each returns the cudaError_t of the launch
+// and adds the number of kernels launched to *launches.
+cudaError_t launch_encode(const EncodeArgs &a, cudaStream_t s, uint64_t *launches);
+cudaError_t launch_batcher(const BatchArgs &a, cudaStream_t s, uint64_t *launches);
+cudaError_t launch_query_ntt(const BatchArgs &a, cudaStream_t s, uint64_t *launches);
+cudaError_t launch_eval(const BatchArgs &a, cudaStream_t s, int num_sms, uint64_t *launches);
+cudaError_t launch_ntt_forward(const KParams &kp, uint32_t n, uint32_t L, const uint2 *tw_fwd, const uint32_t *in,
+                               uint32_t *out, uint32_t count, uint32_t *err, cudaStream_t s, uint64_t *launches);
+cudaError_t launch_ntt_inverse(const KParams &kp, uint32_t n, uint32_t L, const uint2 *tw_inv, const uint32_t *in,
+                               uint32_t *out, uint32_t count, cudaStream_t s, uint64_t *launches);
+
+}  // namespace wally

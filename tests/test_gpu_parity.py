@@ -1,0 +1,239 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar: bit-exact on every response word (integer path).  Inputs are seeded
+(synth/); expected values come only from oracle/.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import capi
+from tests import helpers as H
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2406_06761_b200.wally import WallyError, WallyServer  # noqa: E402
+
+
+# --------------------------------------------------------------------------
+# NTT kernels (step a2 and the inverse used inside the fused kernel)
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n,L", [(1024, 1), (2048, 2), (4096, 2), (4096, 3), (8192, 4)])
+def test_ntt_roundtrip_and_product(n, L):
+    srv = WallyServer(n, L, d=n // 32)
+    qs = srv.moduli
+    rng = np.random.default_rng(n + L)
+    count = 3
+    a = np.stack([np.stack([rng.integers(0, q, size=n) for q in qs]) for _ in range(count)]).astype(np.uint32)
+    b = np.stack([np.stack([rng.integers(0, q, size=n) for q in qs]) for _ in range(count)]).astype(np.uint32)
+    da = torch.from_numpy(a.view(np.int32)).cuda()
+    db = torch.from_numpy(b.view(np.int32)).cuda()
+    fa, fb, back = torch.empty_like(da), torch.empty_like(db), torch.empty_like(da)
+    srv.ntt_forward(da, fa, count)
+    srv.ntt_inverse(fa, back, count)
+    assert np.array_equal(back.cpu().numpy().view(np.uint32), a)
+    # forward values are in [0, 4q)
+    fa_h = fa.cpu().numpy().view(np.uint32).astype(np.uint64)
+    srv.ntt_forward(db, fb, count)
+    fb_h = fb.cpu().numpy().view(np.uint32).astype(np.uint64)
+    qv = np.array(qs, dtype=np.uint64)[None, :, None]
+    assert (fa_h < 4 * qv).all()
+    prod = (fa_h % qv) * (fb_h % qv) % qv
+    dp = torch.from_numpy(prod.astype(np.uint32).view(np.int32)).cuda()
+    out = torch.empty_like(dp)
+    srv.ntt_inverse(dp, out, count)
+    got = out.cpu().numpy().view(np.uint32)
+    for c in range(count):
+        for l, q in enumerate(qs):
+            want = capi.polymul_ntt(a[c, l], b[c, l], q)
+            assert np.array_equal(got[c, l], want), (c, l)
+    srv.close()
+
+
+# --------------------------------------------------------------------------
+# Whole path on configs[0] (c1): every pair, real encryptions, decrypt check
+# --------------------------------------------------------------------------
+
+def test_c1_all_pairs_bit_exact_and_decrypts():
+    w = synth.WORKLOADS["c1"]
+    ents = synth.cluster_entries(w)
+    ids = synth.query_clusters(w)
+    qv = synth.query_vectors(w, ids)
+    srv = H.make_server(w, ents)
+    qs = srv.moduli
+    cts, keys = H.encrypt_queries(w, qs, qv)
+    resp, off = H.run_batch(srv, ids, cts)
+    pcs = capi.encode_cluster(ents[0], w.d, w.n)
+    P = pcs.shape[0]
+    assert P == 32
+    pq = np.repeat(np.arange(w.num_queries), P)
+    pp = np.tile(np.arange(P), w.num_queries)
+    want = H.oracle_pairs(qs, cts, pcs, pq, pp)
+    E = w.n // w.d
+    for i, (q, k) in enumerate(zip(pq, pp)):
+        got = H.response_of(resp, off, q, k, w.n)
+        assert np.array_equal(got, want[i]), (q, k)
+        dec = capi.decrypt_q0(qs[0], w.t, got, keys[q].s)
+        for j in range(E):
+            assert int(dec[j * w.d + w.d - 1]) == int(np.dot(qv[q].astype(np.int64),
+                                                             ents[0][k * E + j].astype(np.int64))) % w.t
+    assert srv.kernel_launches() > 0
+    srv.close()
+
+
+# --------------------------------------------------------------------------
+# Edge cases: ragged clusters, d not dividing n, d = 1, d = n, tiny clusters,
+# chunks of queries (> 8 per cluster), clusters without queries, L = 1..4
+# --------------------------------------------------------------------------
+
+EDGE = [
+    dict(n=1024, L=1, d=100, sizes=[1, 10, 11, 37], nq=30),
+    dict(n=2048, L=2, d=2048, sizes=[1, 3], nq=19),
+    dict(n=2048, L=3, d=1, sizes=[2048, 2049, 5], nq=21),
+    dict(n=4096, L=2, d=192, sizes=[2000, 21, 22, 1], nq=40),
+    dict(n=4096, L=4, d=128, sizes=[65, 1024], nq=17),
+    dict(n=8192, L=4, d=512, sizes=[17, 33], nq=12),
+    dict(n=8192, L=2, d=300, sizes=[100], nq=9),
+]
+
+
+@pytest.mark.parametrize("cfg", EDGE, ids=[f"n{c['n']}_L{c['L']}_d{c['d']}" for c in EDGE])
+def test_edge_cases_bit_exact(cfg):
+    n, L, d = cfg["n"], cfg["L"], cfg["d"]
+    rng = np.random.default_rng(n + 7 * L + d)
+    clusters = [rng.integers(-15, 16, size=(s, d)).astype(np.int8) for s in cfg["sizes"]]
+    srv = H.make_server_ragged(n, L, d, clusters)
+    qs = srv.moduli
+    C = len(clusters)
+    # skewed ids: cluster 0 gets most queries (> one chunk), the last cluster none
+    ids = np.where(rng.random(cfg["nq"]) < 0.6, 0, rng.integers(0, max(1, C - 1), size=cfg["nq"])).astype(np.uint32)
+    cts = np.stack([np.stack([np.stack([rng.integers(0, q, size=n) for q in qs]) for _ in range(2)])
+                    for _ in range(cfg["nq"])]).astype(np.uint32)
+    resp, off = H.run_batch(srv, ids, cts)
+    E = n // d
+    pcs_by_c = [capi.encode_cluster(c, d, n) for c in clusters]
+    for q in range(cfg["nq"]):
+        c = int(ids[q])
+        P = pcs_by_c[c].shape[0]
+        assert int(off[q + 1] - off[q]) == P * 2 * n
+        want = H.oracle_pairs(qs, cts[q:q + 1], pcs_by_c[c], np.zeros(P), np.arange(P))
+        for k in range(P):
+            assert np.array_equal(H.response_of(resp, off, q, k, n), want[k]), (q, k)
+    assert E >= 1
+    srv.close()
+
+
+def test_empty_batch_and_errors():
+    w = synth.scaled(synth.WORKLOADS["c1"], cluster_size=64, num_queries=3)
+    ents = synth.cluster_entries(w)
+    srv = H.make_server(w, ents)
+    qs = srv.moduli
+    # empty batch is a no-op
+    ws = srv.alloc_workspace(0)
+    resp = torch.empty(1, dtype=torch.int32, device="cuda")
+    srv.eval_batch(np.zeros(0, np.uint32), torch.empty(0, dtype=torch.int32, device="cuda"), resp, ws)
+    # unknown cluster id -> error before any launch
+    cts = torch.zeros((1, 2, w.num_limbs, w.n), dtype=torch.int32, device="cuda")
+    with pytest.raises(WallyError) as ei:
+        srv.response_layout(np.array([5], np.uint32))
+    assert ei.value.code == -3
+    before = srv.kernel_launches()
+    with pytest.raises(WallyError):
+        srv.eval_batch(np.array([1], np.uint32), cts, resp, srv.alloc_workspace(1))
+    assert srv.kernel_launches() == before
+    # a residue >= q is reported
+    bad = cts.clone()
+    bad[0, 0, 0, 5] = qs[0]
+    off = srv.response_layout(np.array([0], np.uint32))
+    resp = torch.empty(int(off[-1]), dtype=torch.int32, device="cuda")
+    ws = srv.alloc_workspace(1)
+    srv.eval_batch(np.array([0], np.uint32), bad, resp, ws)
+    with pytest.raises(WallyError) as ei:
+        srv.check_batch(ws)
+    assert ei.value.code == -4
+    srv.close()
+
+
+def test_host_buffer_path_matches_device_path():
+    w = synth.scaled(synth.WORKLOADS["c2"], num_clusters=6, cluster_size=300, num_queries=37)
+    ents = synth.cluster_entries(w)
+    srv = H.make_server(w, ents)
+    ids = synth.query_clusters(w)
+    cts = synth.uniform_ciphertexts(w, srv.moduli)
+    resp_dev, off = H.run_batch(srv, ids, cts)
+    host_resp = torch.empty(int(off[-1]), dtype=torch.int32).pin_memory()
+    qh = torch.from_numpy(cts.view(np.int32)).pin_memory()
+    sub = 8
+    ws = torch.empty(srv.host_workspace_bytes(sub) // 4 + 1, dtype=torch.int32, device="cuda")
+    srv.eval_batch_host(ids, qh, host_resp, sub, ws)
+    assert np.array_equal(host_resp.numpy().view(np.uint32), resp_dev)
+    srv.close()
+
+
+# --------------------------------------------------------------------------
+# Full BASELINE configs, in the bench's launch configuration, sampled pairs
+# --------------------------------------------------------------------------
+
+def _sampled_full_config(name, n_pairs=384, real_queries=4):
+    w = synth.WORKLOADS[name]
+    ents = synth.cluster_entries(w)
+    ids = synth.query_clusters(w)
+    srv = H.make_server(w, ents)
+    qs = srv.moduli
+    cts_dev = synth.uniform_ciphertexts_torch(w, qs)
+    # a few real encryptions (decrypt check) replace uniform stand-ins
+    qv = synth.query_vectors(w, ids)
+    real = np.linspace(0, w.num_queries - 1, real_queries).astype(np.int64)
+    rcts, keys = H.encrypt_queries(w, qs, qv[real], index_base=0)
+    cts_dev[torch.from_numpy(real).cuda()] = torch.from_numpy(rcts.view(np.int32)).cuda()
+    off = srv.response_layout(ids)
+    resp = torch.empty(int(off[-1]), dtype=torch.int32, device="cuda")
+    ws = srv.alloc_workspace(w.num_queries)
+    srv.eval_batch(ids, cts_dev, resp, ws)
+    srv.check_batch(ws)
+    rng = np.random.default_rng(99)
+    E = w.n // w.d
+    P = -(-w.cluster_size // E)
+    qsel = np.concatenate([real, rng.integers(0, w.num_queries, size=n_pairs // 2)])
+    pq = np.repeat(qsel, 2)
+    pp = np.empty_like(pq)
+    pp[0::2] = 0
+    pp[1::2] = P - 1                      # first and last (partial) plaintext
+    extra_q = rng.integers(0, w.num_queries, size=n_pairs // 4)
+    pq = np.concatenate([pq, extra_q])
+    pp = np.concatenate([pp, rng.integers(0, P, size=extra_q.size)])
+    uq, inv = np.unique(pq, return_inverse=True)
+    cts_h = cts_dev[torch.from_numpy(uq).cuda()].cpu().numpy().view(np.uint32)
+    # plaintext coefficients of every (cluster, k) needed
+    need = sorted(set((int(ids[q]), int(k)) for q, k in zip(pq, pp)))
+    pidx = {ck: i for i, ck in enumerate(need)}
+    pcs = np.stack([capi.encode_plaintext(ents[c][k * E:(k + 1) * E], w.d, w.n) for c, k in need])
+    want = H.oracle_pairs(qs, cts_h, pcs, inv, [pidx[(int(ids[q]), int(k))] for q, k in zip(pq, pp)])
+    # only the sampled responses are copied back
+    for i, (q, k) in enumerate(zip(pq, pp)):
+        b = int(off[q]) + int(k) * 2 * w.n
+        got = resp[b:b + 2 * w.n].cpu().numpy().view(np.uint32).reshape(2, w.n)
+        assert np.array_equal(got, want[i]), (name, q, k)
+    for i, q in enumerate(real):
+        c = int(ids[q])
+        for k in (0, P - 1):
+            b = int(off[q]) + k * 2 * w.n
+            got = resp[b:b + 2 * w.n].cpu().numpy().view(np.uint32)
+            dec = capi.decrypt_q0(qs[0], w.t, got, keys[i].s)
+            cnt = min(E, w.cluster_size - k * E)
+            for j in range(cnt):
+                assert int(dec[j * w.d + w.d - 1]) == int(np.dot(qv[q].astype(np.int64),
+                                                                 ents[c][k * E + j].astype(np.int64))) % w.t
+    srv.close()
+    del resp, ws, cts_dev
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
+def test_full_config_sampled_bit_exact(name):
+    _sampled_full_config(name)
