@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--quiet", action="store_true")
+    ap.add_argument("--queries", type=int, default=0,
+                    help="profiling only: evaluate just the first Q queries of the batch (not a bench line)")
     return ap.parse_args()
 
 
@@ -107,7 +109,15 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append([x.strip() for x in line.split(",")] + [time.time()])
+
+    def wait_first(self, timeout=5.0):
+        t0 = time.time()
+        while self.proc and not self.rows and time.time() - t0 < timeout:
+            time.sleep(0.05)
+
+    def mark(self):
+        return time.time()
 
     def __exit__(self, *a):
         if self.proc:
@@ -117,7 +127,12 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
+    def summary(self, t0=None, t1=None):
+        rows = self.rows
+        if t0 is not None:
+            win = [r for r in rows if t0 - 0.25 <= r[-1] <= t1 + 0.25]
+            rows = win if win else rows[-1:]
+        self.rows = rows
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
@@ -217,11 +232,12 @@ def run_wally(args, rank, world, local_rank):
     torch.cuda.synchronize()
     encode_s = time.time() - te
     del ent_dev
-    mine = np.nonzero(owner[ids_all] == rank)[0] if world > 1 else np.arange(ids_all.size)
+    nsel = args.queries if args.queries > 0 else ids_all.size
+    mine = np.nonzero(owner[ids_all[:nsel]] == rank)[0] if world > 1 else np.arange(nsel)
     ids = np.ascontiguousarray(ids_all[mine])
     cts_all = synth.uniform_ciphertexts_torch(w, moduli, device=dev)
-    cts = cts_all[torch.from_numpy(mine).to(dev)] if world > 1 else cts_all
-    if world > 1:
+    cts = cts_all[torch.from_numpy(mine).to(dev)] if (world > 1 or nsel < ids_all.size) else cts_all
+    if cts is not cts_all:
         del cts_all
     E = w.n // w.d
     P = -(-w.cluster_size // E)
@@ -246,14 +262,17 @@ def run_wally(args, rank, world, local_rank):
     launches0 = srv.kernel_launches()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
+        clk.wait_first()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        t_clk0 = clk.mark()
         start.record(stream)
         for _ in range(args.steps):
             srv.eval_batch(ids, cts, resp, ws)
         end.record(stream)
         torch.cuda.synchronize()
+        t_clk1 = clk.mark()
     if world > 1:
         dist.barrier()
     ms = start.elapsed_time(end)
@@ -276,7 +295,7 @@ def run_wally(args, rank, world, local_rank):
     # roofline of the dominant (fused) kernel: integer multiply pipe
     peaks = measured_peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    clocks = clk.summary()
+    clocks = clk.summary(t_clk0, t_clk1)
     mm = modmul_per_pair(w.n, w.num_limbs)
     imad_per_launch = 3.0 * mm * pairs          # this rank's launch
     fused_ms = st_fused / max(nb, 1)
@@ -312,6 +331,8 @@ def run_wally(args, rank, world, local_rank):
            "gpu_launches": int(launches),
            "clocks": clocks,
            "setup_s": round(setup_s, 1), "encode_s": round(encode_s, 3)}
+    if args.queries > 0:
+        out["profiling_subset"] = f"first {args.queries} queries only -- not a bench line"
 
     # end-to-end through the host-buffer C-ABI call (pinned host memory)
     if not args.no_e2e and args.e2e_steps > 0:

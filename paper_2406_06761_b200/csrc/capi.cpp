@@ -15,6 +15,7 @@
 #include <string>
 #include <vector>
 
+#include "ntt_device.cuh"
 #include "wally_internal.h"
 
 using namespace wally;
@@ -126,6 +127,56 @@ static uint64_t primitive_2n_root(uint64_t q, uint32_t n) {
     return 0;
 }
 
+// Pass-major twiddle tables (layout documented in ntt_device.cuh): per pass
+// (TB, R), one block of R entries per hi, holding in execution order the
+// entries m + hi*NB + b (m = n / (2 TB 2^s), NB = R >> (s+1)) of the merged
+// table; GS (inverse) slot R - (R >> s) + b, CT (forward) slot (R >> (s+1)) + b.
+template <int N>
+static void build_pass_tables_n(const uint2 *pf, const uint2 *pi, uint2 *fwd, uint2 *inv) {
+    using Gm = NttGeom<N>;
+    const int TB[3] = {Gm::TB0, Gm::TB1, Gm::TB2}, R[3] = {Gm::R0, Gm::R1, Gm::R2};
+    const int OFF[3] = {Gm::TW0, Gm::TW1, Gm::TW2};
+    for (int p = 0; p < 3; p++) {
+        const int H = N / (TB[p] * R[p]);
+        int logr = 0;
+        while ((1 << logr) < R[p]) logr++;
+        // pass 0 (hi = thread g): slot-pair-major, uint2 index ((slot/2) T + g) 2 + slot%2
+        auto at = [&](int hi, int slot) -> size_t {
+            if (p == 0) return (size_t)OFF[0] + ((size_t)(slot / 2) * Gm::T + hi) * 2 + (slot % 2);
+            return (size_t)OFF[p] + (size_t)hi * R[p] + slot;
+        };
+        for (int hi = 0; hi < H; hi++) {
+            for (int k = 0; k < R[p]; k++) inv[at(hi, k)] = fwd[at(hi, k)] = make_uint2(0, 0);
+            for (int s = 0; s < logr; s++) {
+                const int nb = R[p] >> (s + 1), m = N / (2 * TB[p] * (1 << s));
+                for (int b = 0; b < nb; b++) {
+                    inv[at(hi, R[p] - (R[p] >> s) + b)] = pi[m + hi * nb + b];
+                    fwd[at(hi, (R[p] >> (s + 1)) + b)] = pf[m + hi * nb + b];
+                }
+            }
+        }
+    }
+}
+
+static size_t tw_limb_entries(uint32_t n) {
+    switch (n) {
+        case 1024: return NttGeom<1024>::TW_LIMB;
+        case 2048: return NttGeom<2048>::TW_LIMB;
+        case 4096: return NttGeom<4096>::TW_LIMB;
+        case 8192: return NttGeom<8192>::TW_LIMB;
+    }
+    return 0;
+}
+
+static void build_pass_tables(uint32_t n, const uint2 *pf, const uint2 *pi, uint2 *fwd, uint2 *inv) {
+    switch (n) {
+        case 1024: build_pass_tables_n<1024>(pf, pi, fwd, inv); break;
+        case 2048: build_pass_tables_n<2048>(pf, pi, fwd, inv); break;
+        case 4096: build_pass_tables_n<4096>(pf, pi, fwd, inv); break;
+        case 8192: build_pass_tables_n<8192>(pf, pi, fwd, inv); break;
+    }
+}
+
 extern "C" int wally_find_moduli(uint32_t n, uint32_t num_limbs, uint32_t *moduli_out) {
     if (!moduli_out || num_limbs == 0 || num_limbs > WALLY_MAX_LIMBS || n < 2 || (n & (n - 1)))
         return fail(nullptr, WALLY_E_ARG, "wally_find_moduli: bad arguments");
@@ -202,7 +253,8 @@ extern "C" int wally_create(const wally_params *pp, int device, wally_ctx **out)
     int logn = 0;
     while ((1u << logn) < n) logn++;
     KParams &kp = c->kp;
-    std::vector<uint2> twf((size_t)L * n), twi((size_t)L * n);
+    const size_t tw_limb = tw_limb_entries(n);
+    std::vector<uint2> twf((size_t)L * tw_limb), twi((size_t)L * tw_limb);
     for (uint32_t l = 0; l < L; l++) {
         const uint64_t q = p.moduli[l];
         kp.q[l] = (uint32_t)q;
@@ -224,12 +276,14 @@ extern "C" int wally_create(const wally_params *pp, int device, wally_ctx **out)
         }
         const uint64_t psi = primitive_2n_root(q, n);
         const uint64_t psi_inv = invm(psi, q);
+        std::vector<uint2> pf(n), pi(n);   // standard merged tables psi^{brev(i)}, psi^{-brev(i)}
         for (uint32_t i = 0; i < n; i++) {
             const uint32_t e = bitrev(i, logn);
             const uint32_t w = (uint32_t)powm(psi, e, q), wi = (uint32_t)powm(psi_inv, e, q);
-            twf[(size_t)l * n + i] = make_uint2(w, shoup_companion(w, (uint32_t)q));
-            twi[(size_t)l * n + i] = make_uint2(wi, shoup_companion(wi, (uint32_t)q));
+            pf[i] = make_uint2(w, shoup_companion(w, (uint32_t)q));
+            pi[i] = make_uint2(wi, shoup_companion(wi, (uint32_t)q));
         }
+        build_pass_tables(n, pf.data(), pi.data(), twf.data() + l * tw_limb, twi.data() + l * tw_limb);
     }
     const size_t tb = sizeof(uint2) * twf.size();
     if (cudaMalloc(&c->d_tw_fwd, tb) != cudaSuccess || cudaMalloc(&c->d_tw_inv, tb) != cudaSuccess) {

@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(NttGeom<N>::T) ntt_forward_kernel(KParams kp, 
     const uint32_t limb = (uint32_t)(poly % L);
     const uint32_t q = kp.q[limb], q2 = kp.q2[limb];
     const uint32_t *src = in + poly * N;
-    uint32_t a[V];
+    uint32_t a[1][V];
     bool bad = false;
     // pass-2 groups: element idx = hi*TB2*R2 + k*TB2 + lo  (coalesced across threads)
 #pragma unroll
@@ -44,13 +44,13 @@ __global__ void __launch_bounds__(NttGeom<N>::T) ntt_forward_kernel(KParams kp, 
         for (int k = 0; k < Gm::R2; k++) {
             uint32_t x = __ldg(src + pass_index<N, Gm::TB2, Gm::R2>(g, j, k));
             bad |= (x >= q);
-            a[j * Gm::R2 + k] = x;
+            a[0][j * Gm::R2 + k] = x;
         }
     if (bad && err) atomicOr(err, (uint32_t)kErrResidue);
-    ntt_chain<N>(a, tw + (size_t)limb * N, g, q, q2, bufA, bufB);
+    ntt_chain<N, 1>(a, tw + (size_t)limb * Gm::TW_LIMB, g, q, q2, bufA, bufB);
     uint4 *dst = reinterpret_cast<uint4 *>(out + poly * N + (size_t)g * V);
 #pragma unroll
-    for (int v = 0; v < V / 4; v++) dst[v] = make_uint4(a[4 * v], a[4 * v + 1], a[4 * v + 2], a[4 * v + 3]);
+    for (int v = 0; v < V / 4; v++) dst[v] = make_uint4(a[0][4 * v], a[0][4 * v + 1], a[0][4 * v + 2], a[0][4 * v + 3]);
 }
 
 // Debug/test inverse NTT: out = n^{-1} INTT(in), canonical.
@@ -66,26 +66,24 @@ __global__ void __launch_bounds__(NttGeom<N>::T) ntt_inverse_kernel(KParams kp, 
     const size_t poly = blockIdx.x;
     const uint32_t limb = (uint32_t)(poly % L);
     const uint32_t q = kp.q[limb], q2 = kp.q2[limb];
-    uint32_t a[V];
+    uint32_t a[1][V];
     const uint4 *src = reinterpret_cast<const uint4 *>(in + poly * N + (size_t)g * V);
 #pragma unroll
     for (int v = 0; v < V / 4; v++) {
-        uint4 x = __ldg(src + v);
-        // any 32-bit residue -> [0, 2q): x mod q via one Shoup multiply by 1
-        a[4 * v] = x.x;
-        a[4 * v + 1] = x.y;
-        a[4 * v + 2] = x.z;
-        a[4 * v + 3] = x.w;
+        const uint4 x = __ldg(src + v);
+        // scale first (the transform is linear); Shoup accepts any 32-bit input -> [0, 2q)
+        a[0][4 * v + 0] = shoup_mul(x.x, kp.ninv[limb], kp.ninvp[limb], q);
+        a[0][4 * v + 1] = shoup_mul(x.y, kp.ninv[limb], kp.ninvp[limb], q);
+        a[0][4 * v + 2] = shoup_mul(x.z, kp.ninv[limb], kp.ninvp[limb], q);
+        a[0][4 * v + 3] = shoup_mul(x.w, kp.ninv[limb], kp.ninvp[limb], q);
     }
-#pragma unroll
-    for (int v = 0; v < V; v++) a[v] = shoup_mul(a[v], kp.ninv[limb], kp.ninvp[limb], q);  // scale first (linear)
-    intt_chain<N>(a, tw + (size_t)limb * N, g, q, q2, bufA, bufB);
+    intt_chain<N, 1>(a, tw + (size_t)limb * Gm::TW_LIMB, g, q, q2, bufA, bufB);
     uint32_t *dst = out + poly * N;
 #pragma unroll
     for (int j = 0; j < V / Gm::R2; j++)
 #pragma unroll
         for (int k = 0; k < Gm::R2; k++)
-            dst[pass_index<N, Gm::TB2, Gm::R2>(g, j, k)] = csub(a[j * Gm::R2 + k], q);
+            dst[pass_index<N, Gm::TB2, Gm::R2>(g, j, k)] = csub(a[0][j * Gm::R2 + k], q);
 }
 
 // ---------------------------------------------------------------------------
@@ -105,7 +103,7 @@ __global__ void __launch_bounds__(NttGeom<N>::T) encode_kernel(EncodeArgs ea) {
     const uint32_t size = ea.size[li];
     const uint32_t count = min(ea.E, size - first);
     const int8_t *ent = ea.entries + (ea.entry_base[li] + first) * (uint64_t)ea.d;
-    uint32_t a[V];
+    uint32_t a[1][V];
 #pragma unroll
     for (int j = 0; j < V / Gm::R2; j++)
 #pragma unroll
@@ -115,15 +113,15 @@ __global__ void __launch_bounds__(NttGeom<N>::T) encode_kernel(EncodeArgs ea) {
             const uint32_t jj = pos / ea.d, i = ea.d - 1 - pos % ea.d;
             int32_t x = 0;
             if (jj < count) x = ent[(size_t)jj * ea.d + i];
-            a[j * Gm::R2 + kk] = (x < 0) ? (uint32_t)((int64_t)q + x) : (uint32_t)x;  // x mod q (reading S8)
+            a[0][j * Gm::R2 + kk] = (x < 0) ? (uint32_t)((int64_t)q + x) : (uint32_t)x;  // x mod q (reading S8)
         }
-    ntt_chain<N>(a, ea.tw_fwd + (size_t)limb * N, g, q, q2, bufA, bufB);
+    ntt_chain<N, 1>(a, ea.tw_fwd + (size_t)limb * Gm::TW_LIMB, g, q, q2, bufA, bufB);
     uint32_t *dst = ea.store + ((size_t)pt * ea.L + limb) * 2 * N + (size_t)g * V;
 #pragma unroll
     for (int v = 0; v < V; v++) {
-        uint32_t y = csub(shoup_mul(a[v], ea.kp.fold[limb], ea.kp.foldp[limb], q), q);  // canonical
+        uint32_t y = csub(shoup_mul(a[0][v], ea.kp.fold[limb], ea.kp.foldp[limb], q), q);  // canonical
         dst[v] = y;
-        dst[N + v] = (uint32_t)(((uint64_t)y << 32) / q);                               // Shoup companion
+        dst[N + v] = (uint32_t)(((uint64_t)y << 32) / q);                                  // Shoup companion
     }
 }
 
@@ -257,91 +255,189 @@ __device__ __forceinline__ void ms_step(uint32_t (&a)[V], uint32_t (&rtop)[V], u
     }
 }
 
-template <int N, int L, int J>
-__device__ __forceinline__ void eval_limb(uint32_t (&a)[NttGeom<N>::V], uint32_t (&rtop)[NttGeom<N>::V],
-                                          uint32_t (&acc)[(L > 2) ? (L - 2) : 1][NttGeom<N>::V], const BatchArgs &ba,
-                                          const uint32_t *chat_q, const uint32_t *phat, int g, uint32_t *bufA,
-                                          uint32_t *bufB) {
+// Per-thread state of NC polynomials (the NC ciphertext components a thread
+// carries through all limbs).
+template <int N, int L, int NC>
+struct EvalState {
+    static constexpr int V = NttGeom<N>::V;
+    static constexpr int NA = (L > 2) ? (L - 2) : 1;
+    uint32_t a[NC][V];
+    uint32_t rtop[NC][V];
+    uint32_t acc[NC][NA][V];
+};
+
+// Where the inverse transform of one limb gets its twiddles and exchange
+// buffers: GRP = false -> whole-CTA chain, global twiddles, double buffers;
+// GRP = true -> one thread group of a multi-group CTA, twiddles in shared
+// memory, one buffer per polynomial, named barrier `bar`.
+struct ChainCtx {
+    const uint2 *tw;      // inverse twiddles of limb 0 (global or shared)
+    uint32_t *bufA, *bufB;
+    int bar;
+};
+
+// One limb of the fused computation for NC components of one query:
+// pointwise product with the NTT-domain plaintext, inverse NTT (shared
+// twiddles), modulus-switch step.
+template <int N, int L, int NC, int J, bool GRP>
+__device__ __forceinline__ void eval_limb(EvalState<N, L, NC> &st, const BatchArgs &ba, const uint32_t *chat_q,
+                                          int comp0, const uint32_t *phat, int g, const ChainCtx &cx) {
     using Gm = NttGeom<N>;
     constexpr int V = Gm::V;
     const uint32_t q = ba.kp.q[J], q2 = ba.kp.q2[J];
-    const uint4 *cs = reinterpret_cast<const uint4 *>(chat_q + (size_t)J * N + (size_t)g * V);
-    const uint4 *ps = reinterpret_cast<const uint4 *>(phat + (size_t)J * 2 * N + (size_t)g * V);
-    const uint4 *pps = reinterpret_cast<const uint4 *>(phat + (size_t)J * 2 * N + N + (size_t)g * V);
+    const uint32_t *pv = phat + (size_t)J * 2 * N + (size_t)g * V;
 #pragma unroll
     for (int v = 0; v < V / 4; v++) {
-        const uint4 c = __ldg(cs + v), p = __ldg(ps + v), pp = __ldg(pps + v);
-        a[4 * v + 0] = shoup_mul(c.x, p.x, pp.x, q);
-        a[4 * v + 1] = shoup_mul(c.y, p.y, pp.y, q);
-        a[4 * v + 2] = shoup_mul(c.z, p.z, pp.z, q);
-        a[4 * v + 3] = shoup_mul(c.w, p.w, pp.w, q);
+        const uint4 p = ldg_stream(pv + 4 * v), pp = ldg_stream(pv + N + 4 * v);
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+            const uint4 x = ldg_stream(chat_q + ((size_t)(comp0 + c) * L + J) * N + (size_t)g * V + 4 * v);
+            st.a[c][4 * v + 0] = shoup_mul(x.x, p.x, pp.x, q);
+            st.a[c][4 * v + 1] = shoup_mul(x.y, p.y, pp.y, q);
+            st.a[c][4 * v + 2] = shoup_mul(x.z, p.z, pp.z, q);
+            st.a[c][4 * v + 3] = shoup_mul(x.w, p.w, pp.w, q);
+        }
     }
-    intt_chain<N>(a, ba.tw_inv + (size_t)J * N, g, q, q2, bufA, bufB);
-    ms_step<L, J, V>(a, rtop, acc, ba.kp);
+    if constexpr (GRP)
+        intt_chain_group<N, NC>(st.a, cx.tw + (size_t)J * Gm::TW_LIMB, g, q, q2, cx.bufA, cx.bar);
+    else
+        intt_chain<N, NC>(st.a, cx.tw + (size_t)J * Gm::TW_LIMB, g, q, q2, cx.bufA, cx.bufB);
+#pragma unroll
+    for (int c = 0; c < NC; c++) ms_step<L, J, V>(st.a[c], st.rtop[c], st.acc[c], ba.kp);
 }
 
-template <int N, int L, int J>
+template <int N, int L, int NC, int J, bool GRP>
 struct LimbLoop {
-    static __device__ __forceinline__ void run(uint32_t (&a)[NttGeom<N>::V], uint32_t (&rtop)[NttGeom<N>::V],
-                                               uint32_t (&acc)[(L > 2) ? (L - 2) : 1][NttGeom<N>::V],
-                                               const BatchArgs &ba, const uint32_t *chat_q, const uint32_t *phat, int g,
-                                               uint32_t *bufA, uint32_t *bufB) {
-        eval_limb<N, L, J>(a, rtop, acc, ba, chat_q, phat, g, bufA, bufB);
-        LimbLoop<N, L, J - 1>::run(a, rtop, acc, ba, chat_q, phat, g, bufA, bufB);
+    static __device__ __forceinline__ void run(EvalState<N, L, NC> &st, const BatchArgs &ba, const uint32_t *chat_q,
+                                               int comp0, const uint32_t *phat, int g, const ChainCtx &cx) {
+        eval_limb<N, L, NC, J, GRP>(st, ba, chat_q, comp0, phat, g, cx);
+        if constexpr (J > 0) LimbLoop<N, L, NC, J - 1, GRP>::run(st, ba, chat_q, comp0, phat, g, cx);
     }
 };
-template <int N, int L>
-struct LimbLoop<N, L, -1> {
-    static __device__ __forceinline__ void run(uint32_t (&)[NttGeom<N>::V], uint32_t (&)[NttGeom<N>::V],
-                                               uint32_t (&)[(L > 2) ? (L - 2) : 1][NttGeom<N>::V], const BatchArgs &,
-                                               const uint32_t *, const uint32_t *, int, uint32_t *, uint32_t *) {}
+
+// Components per thread: both (c0, c1) share twiddle and plaintext loads and
+// double the independent butterflies per stage; at n = 8192 (32 values per
+// thread per component) one component per thread keeps registers in budget.
+template <int N>
+struct EvalCfg {
+    static constexpr int NC = (N <= 4096) ? 2 : 1;
+#ifdef WALLY_EVAL_MINB
+    static constexpr int MINB = WALLY_EVAL_MINB;
+#else
+    static constexpr int MINB = (N <= 4096) ? 2 : 1;
+#endif
 };
 
-template <int N, int L>
-__global__ void __launch_bounds__(NttGeom<N>::T, (N <= 4096) ? 2 : 1) eval_kernel(BatchArgs ba) {
+// Work item -> (local cluster, plaintext, query range).  Items of one
+// cluster are consecutive, so the cluster found for the previous item is
+// checked before falling back to a binary search over item_start.
+struct ItemCursor {
+    uint32_t li = 0, b = 1, e = 0;  // item range [b, e) of cluster li (empty at start)
+    __device__ __forceinline__ void seek(const BatchArgs &ba, uint32_t item) {
+        if (item >= b && item < e) return;
+        uint32_t lo = 0, hi = ba.n_local;  // item_start[lo] <= item < item_start[hi]
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (ba.item_start[mid] <= item) lo = mid; else hi = mid;
+        }
+        li = lo;
+        b = ba.item_start[lo];
+        e = ba.item_start[lo + 1];
+    }
+};
+
+// Evaluate work item `item` (cursor already positioned) for one thread group.
+template <int N, int L, bool GRP>
+__device__ __forceinline__ void eval_item(const BatchArgs &ba, const ItemCursor &cur, uint32_t item, int g,
+                                          const ChainCtx &cx) {
     using Gm = NttGeom<N>;
     constexpr int V = Gm::V;
-    constexpr int NA = (L > 2) ? (L - 2) : 1;
+    constexpr int NC = EvalCfg<N>::NC;
+    const uint32_t li = cur.li;
+    const uint32_t cnt = ba.counts[li];
+    const uint32_t nch = (cnt + kQueryChunk - 1) / kQueryChunk;
+    const uint32_t local = item - cur.b;
+    const uint32_t k = local / nch, ch = local % nch;
+    const uint32_t qb = ba.seg[li] + ch * kQueryChunk;
+    const uint32_t qe = min(qb + kQueryChunk, ba.seg[li] + cnt);
+    const uint32_t *phat = ba.store + (size_t)(ba.pt_base[li] + k) * L * 2 * N;
+    for (uint32_t qi = qb; qi < qe; qi++) {
+        const uint32_t qo = ba.perm[qi];
+        uint32_t *out_q = ba.resp + ba.resp_off[qo] + (size_t)k * 2 * N;
+        const uint32_t *chat_q = ba.chat + (size_t)qo * 2 * L * N;
+#pragma unroll 1
+        for (int comp0 = 0; comp0 < 2; comp0 += NC) {
+            EvalState<N, L, NC> st;
+            LimbLoop<N, L, NC, L - 1, GRP>::run(st, ba, chat_q, comp0, phat, g, cx);
+#pragma unroll
+            for (int c = 0; c < NC; c++) {
+                uint32_t *dst = out_q + (size_t)(comp0 + c) * N;
+#pragma unroll
+                for (int j = 0; j < V / Gm::R2; j++)
+#pragma unroll
+                    for (int kk = 0; kk < Gm::R2; kk++)
+                        __stcs(dst + pass_index<N, Gm::TB2, Gm::R2>(g, j, kk), st.a[c][j * Gm::R2 + kk]);
+            }
+        }
+    }
+}
+
+// Fused kernel, whole-CTA form (used for n = 8192: twiddles from global
+// memory through L1, double-buffered exchange).
+template <int N, int L>
+__global__ void __launch_bounds__(NttGeom<N>::T, EvalCfg<N>::MINB) eval_kernel(BatchArgs ba) {
+    using Gm = NttGeom<N>;
+    constexpr int NC = EvalCfg<N>::NC;
     extern __shared__ uint32_t smem[];
-    uint32_t *bufA = smem, *bufB = smem + Gm::SMEM_WORDS;
+    ChainCtx cx{ba.tw_inv, smem, smem + NC * Gm::SMEM_WORDS, 0};
     __shared__ uint32_t s_item[2];
     const int g = threadIdx.x;
     const uint32_t total = ba.misc[kMiscTotalItems];
+    ItemCursor cur;
     for (uint32_t it = 0;; it++) {
         if (g == 0) s_item[it & 1] = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
         __syncthreads();
         const uint32_t item = s_item[it & 1];
         if (item >= total) break;
-        // local cluster: last li with item_start[li] <= item
-        uint32_t lo = 0, hi = ba.n_local;  // item_start[lo] <= item < item_start[hi]
-        while (hi - lo > 1) {
-            uint32_t mid = (lo + hi) >> 1;
-            if (ba.item_start[mid] <= item) lo = mid; else hi = mid;
-        }
-        const uint32_t li = lo;
-        const uint32_t cnt = ba.counts[li];
-        const uint32_t nch = (cnt + kQueryChunk - 1) / kQueryChunk;
-        const uint32_t local = item - ba.item_start[li];
-        const uint32_t k = local / nch, ch = local % nch;
-        const uint32_t qb = ba.seg[li] + ch * kQueryChunk;
-        const uint32_t qe = min(qb + kQueryChunk, ba.seg[li] + cnt);
-        const uint32_t *phat = ba.store + (size_t)(ba.pt_base[li] + k) * L * 2 * N;
-        for (uint32_t qi = qb; qi < qe; qi++) {
-            const uint32_t qo = ba.perm[qi];
-            uint32_t *out_q = ba.resp + ba.resp_off[qo] + (size_t)k * 2 * N;
-#pragma unroll 1
-            for (int comp = 0; comp < 2; comp++) {
-                uint32_t a[V], rtop[V], acc[NA][V];
-                const uint32_t *chat_q = ba.chat + ((size_t)qo * 2 + comp) * L * N;
-                LimbLoop<N, L, L - 1>::run(a, rtop, acc, ba, chat_q, phat, g, bufA, bufB);
-                uint32_t *dst = out_q + (size_t)comp * N;
-#pragma unroll
-                for (int j = 0; j < V / Gm::R2; j++)
-#pragma unroll
-                    for (int kk = 0; kk < Gm::R2; kk++)
-                        __stcs(dst + pass_index<N, Gm::TB2, Gm::R2>(g, j, kk), a[j * Gm::R2 + kk]);
-            }
-        }
+        cur.seek(ba, item);
+        eval_item<N, L, false>(ba, cur, item, g, cx);
+    }
+}
+
+// Fused kernel, grouped form (n <= 4096): a CTA holds GROUPS independent
+// T-thread groups that share the limbs' inverse twiddle tables staged once
+// in shared memory; each group pulls its own work items (fetching the next
+// item index one item ahead) and synchronises with its own named barrier.
+constexpr int kEvalGroups = 2;
+
+template <int N, int L>
+__global__ void __launch_bounds__(kEvalGroups * NttGeom<N>::T, 1) eval_kernel_grp(BatchArgs ba) {
+    using Gm = NttGeom<N>;
+    constexpr int NC = EvalCfg<N>::NC;
+    constexpr int T = Gm::T;
+    extern __shared__ uint4 smem4[];
+    uint2 *tw = reinterpret_cast<uint2 *>(smem4);
+    uint32_t *xbuf = reinterpret_cast<uint32_t *>(tw + L * Gm::TW_LIMB);
+    __shared__ uint32_t s_item[kEvalGroups][2];
+    const int grp = threadIdx.x / T, g = threadIdx.x % T;
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(ba.tw_inv);
+        for (int i = threadIdx.x; i < L * Gm::TW_LIMB / 2; i += blockDim.x) smem4[i] = __ldg(src + i);
+    }
+    if (g == 0) s_item[grp][0] = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
+    __syncthreads();
+    const ChainCtx cx{tw, xbuf + grp * NC * Gm::SMEM_WORDS, nullptr, 1 + grp};
+    const uint32_t total = ba.misc[kMiscTotalItems];
+    ItemCursor cur;
+    for (uint32_t it = 0;; it++) {
+        const uint32_t item = s_item[grp][it & 1];
+        if (item >= total) break;
+        uint32_t next = 0;
+        if (g == 0) next = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
+        cur.seek(ba, item);
+        eval_item<N, L, true>(ba, cur, item, g, cx);
+        if (g == 0) s_item[grp][(it + 1) & 1] = next;
+        group_sync(1 + grp, T);
     }
 }
 
@@ -349,7 +445,7 @@ __global__ void __launch_bounds__(NttGeom<N>::T, (N <= 4096) ? 2 : 1) eval_kerne
 // launchers
 // ---------------------------------------------------------------------------
 template <int N>
-static constexpr size_t chain_smem() { return 2 * NttGeom<N>::SMEM_WORDS * sizeof(uint32_t); }
+static constexpr size_t chain_smem(int nc = 1) { return 2 * (size_t)nc * NttGeom<N>::SMEM_WORDS * sizeof(uint32_t); }
 
 template <typename K>
 static cudaError_t allow_smem(K kernel, size_t bytes) {
@@ -424,18 +520,33 @@ cudaError_t launch_ntt_inverse(const KParams &kp, uint32_t n, uint32_t L, const 
 template <int N, int L>
 static cudaError_t launch_eval_nl(const BatchArgs &a, cudaStream_t s, int num_sms) {
     using Gm = NttGeom<N>;
-    const size_t smem = 2 * Gm::SMEM_WORDS * sizeof(uint32_t);
     static bool configured = false;
     static int blocks_per_sm = 1;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(eval_kernel<N, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, eval_kernel<N, L>, Gm::T, smem);
-        if (e != cudaSuccess) return e;
-        if (blocks_per_sm < 1) blocks_per_sm = 1;
-        configured = true;
+    if constexpr (N <= 4096) {
+        const size_t smem = (size_t)L * Gm::TW_LIMB * sizeof(uint2) +
+                            (size_t)kEvalGroups * EvalCfg<N>::NC * Gm::SMEM_WORDS * sizeof(uint32_t);
+        if (!configured) {
+            cudaError_t e = allow_smem(eval_kernel_grp<N, L>, smem);
+            if (e != cudaSuccess) return e;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, eval_kernel_grp<N, L>,
+                                                              kEvalGroups * Gm::T, smem);
+            if (e != cudaSuccess) return e;
+            if (blocks_per_sm < 1) blocks_per_sm = 1;
+            configured = true;
+        }
+        eval_kernel_grp<N, L><<<num_sms * blocks_per_sm, kEvalGroups * Gm::T, smem, s>>>(a);
+    } else {
+        const size_t smem = chain_smem<N>(EvalCfg<N>::NC);
+        if (!configured) {
+            cudaError_t e = allow_smem(eval_kernel<N, L>, smem);
+            if (e != cudaSuccess) return e;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, eval_kernel<N, L>, Gm::T, smem);
+            if (e != cudaSuccess) return e;
+            if (blocks_per_sm < 1) blocks_per_sm = 1;
+            configured = true;
+        }
+        eval_kernel<N, L><<<num_sms * blocks_per_sm, Gm::T, smem, s>>>(a);
     }
-    eval_kernel<N, L><<<num_sms * blocks_per_sm, Gm::T, smem, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -44,6 +44,16 @@ __device__ __forceinline__ void ct_bfly(uint32_t &X, uint32_t &Y, uint32_t w, ui
     Y = x - t + q2;
 }
 
+// Streaming 128-bit load that does not allocate in L1 (keeps the L1 for the
+// twiddle tables, which every polynomial re-reads).
+__device__ __forceinline__ uint4 ldg_stream(const void *p) {
+    uint4 r;
+    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+        : "l"(p));
+    return r;
+}
+
 // ---------------------------------------------------------------------------
 // NTT pass geometry
 //
@@ -54,6 +64,18 @@ __device__ __forceinline__ void ct_bfly(uint32_t &X, uint32_t &Y, uint32_t w, ui
 // the R elements  idx(k) = hi*TB*R + k*TB + lo,  (hi, lo) = divmod(gamma, TB).
 // All S stages of the pass are butterflies inside a group, so they run in
 // registers; between passes the data goes through shared memory.
+//
+// Twiddle tables are "pass-major": per limb, pass p holds one block of R
+// (w, w') pairs per value of hi, with the stage twiddles the group needs in
+// execution order -- so a group reads its twiddles as contiguous 16-byte
+// vectors.  The stage with butterfly distance 2^s (stride t = TB 2^s) uses
+// psi-table entry m + hi*NB + b, m = n/(2t), NB = R >> (s+1), b < NB
+// (merged negacyclic tables: psi^{brev} forward, psi^{-brev} inverse).
+//   inverse (GS, s ascending):  slot of (s, b) = R - (R >> s) + b
+//   forward (CT, s descending): slot of (s, b) = (R >> (s+1)) + b
+// Pass 0 (TB = 1, hi = thread g, one unique block per thread) is stored
+// slot-pair-major, uint4 index (slot/2) * T + g, so the 16-byte loads of a
+// warp are contiguous (global) and bank-conflict free (shared memory).
 // ---------------------------------------------------------------------------
 
 template <int N>
@@ -79,7 +101,15 @@ struct NttGeom {
     static_assert(TB2 * R2 == N, "passes must cover log2(n) stages");
     static constexpr int PAD_SHIFT = (N >= 8192) ? 5 : 4;
     static constexpr int SMEM_WORDS = N + (N >> PAD_SHIFT) + 32;  // one exchange buffer
+    // pass-major twiddle table offsets (uint2 entries) inside one limb's table
+    static constexpr int TW0 = 0, TW1 = N / TB0, TW2 = N / TB0 + N / TB1;
+    static constexpr int TW_LIMB = N / TB0 + N / TB1 + N / TB2;
 };
+
+template <int R>
+struct Log2 { static constexpr int v = (R <= 1) ? 0 : 1 + Log2<R / 2>::v; };
+template <>
+struct Log2<1> { static constexpr int v = 0; };
 
 template <int N>
 __device__ __forceinline__ int smem_pad(int i) { return i + (i >> NttGeom<N>::PAD_SHIFT); }
@@ -92,93 +122,175 @@ __device__ __forceinline__ int pass_index(int g, int j, int k) {
     return hi * TB * R + k * TB + lo;
 }
 
-template <int N, int TB, int R>
-__device__ __forceinline__ void smem_store(uint32_t *buf, const uint32_t (&a)[NttGeom<N>::V], int g) {
+// NC polynomials per thread: a[c][V]; poly c exchanges through buf + c * SMEM_WORDS.
+template <int N, int TB, int R, int NC>
+__device__ __forceinline__ void smem_store(uint32_t *buf, const uint32_t (&a)[NC][NttGeom<N>::V], int g) {
     constexpr int V = NttGeom<N>::V, G = V / R;
 #pragma unroll
-    for (int j = 0; j < G; j++)
+    for (int c = 0; c < NC; c++)
 #pragma unroll
-        for (int k = 0; k < R; k++) buf[smem_pad<N>(pass_index<N, TB, R>(g, j, k))] = a[j * R + k];
+        for (int j = 0; j < G; j++)
+#pragma unroll
+            for (int k = 0; k < R; k++)
+                buf[c * NttGeom<N>::SMEM_WORDS + smem_pad<N>(pass_index<N, TB, R>(g, j, k))] = a[c][j * R + k];
 }
 
-template <int N, int TB, int R>
-__device__ __forceinline__ void smem_load(const uint32_t *buf, uint32_t (&a)[NttGeom<N>::V], int g) {
+template <int N, int TB, int R, int NC>
+__device__ __forceinline__ void smem_load(const uint32_t *buf, uint32_t (&a)[NC][NttGeom<N>::V], int g) {
     constexpr int V = NttGeom<N>::V, G = V / R;
 #pragma unroll
-    for (int j = 0; j < G; j++)
+    for (int c = 0; c < NC; c++)
 #pragma unroll
-        for (int k = 0; k < R; k++) a[j * R + k] = buf[smem_pad<N>(pass_index<N, TB, R>(g, j, k))];
+        for (int j = 0; j < G; j++)
+#pragma unroll
+            for (int k = 0; k < R; k++)
+                a[c][j * R + k] = buf[c * NttGeom<N>::SMEM_WORDS + smem_pad<N>(pass_index<N, TB, R>(g, j, k))];
 }
 
-// All stages of one pass.  INVERSE: GS stages with strides TB, 2TB, ...;
-// forward: CT stages with strides TB*R/2, ..., TB.  Stage with stride t uses
-// twiddle tw[m + i], m = n/(2t), i = idx / (2t) (the standard merged
-// negacyclic tables: psi^{brev} forward, psi^{-brev} inverse).
-template <int N, int TB, int R, bool INVERSE>
-__device__ __forceinline__ void ntt_pass(uint32_t (&a)[NttGeom<N>::V], const uint2 *__restrict__ tw, int g, uint32_t q,
-                                         uint32_t q2) {
+// Twiddle fetch: plain loads when the table lives in shared memory (TWS),
+// read-only-cache loads when it lives in global memory.
+template <bool TWS>
+__device__ __forceinline__ uint4 tw_ld4(const uint4 *p) {
+    if constexpr (TWS) return *p; else return __ldg(p);
+}
+template <bool TWS>
+__device__ __forceinline__ uint2 tw_ld2(const uint2 *p) {
+    if constexpr (TWS) return *p; else return __ldg(p);
+}
+
+// One stage (butterfly distance 2^S inside each group) of a pass, applied to
+// NC polynomials that share the twiddles.  All bounds are constant
+// expressions, so the stage unrolls into straight register code.
+template <int N, int TB, int R, int S, bool INVERSE, int NC, bool TWS>
+__device__ __forceinline__ void ntt_stage(uint32_t (&a)[NC][NttGeom<N>::V], const uint2 *__restrict__ twp, int g,
+                                          uint32_t q, uint32_t q2) {
     constexpr int V = NttGeom<N>::V, T = NttGeom<N>::T, G = V / R;
-    constexpr int LOGR = (R == 2) ? 1 : (R == 4) ? 2 : (R == 8) ? 3 : (R == 16) ? 4 : (R == 32) ? 5 : 6;
+    constexpr int HALF = 1 << S;
+    constexpr int NB = R >> (S + 1);
+    constexpr int OFF = INVERSE ? (R - (R >> S)) : (R >> (S + 1));
 #pragma unroll
     for (int j = 0; j < G; j++) {
-        const int hi = (g + j * T) / TB;
+        uint2 w[NB];
+        if constexpr (TB == 1) {
+            // pass 0: slot-pair-major, uint4 index (slot/2) * T + g   (G == 1)
+            const uint4 *t4 = reinterpret_cast<const uint4 *>(twp) + g;
+            if constexpr (NB >= 2) {
 #pragma unroll
-        for (int ss = 0; ss < LOGR; ss++) {
-            const int s = INVERSE ? ss : (LOGR - 1 - ss);
-            const int half = 1 << s;
-            const int m = N / (2 * TB * half);
-            const int nb = R >> (s + 1);
-            const uint2 *twp = tw + m + hi * nb;
-#pragma unroll
-            for (int b = 0; b < nb; b++) {
-                const uint2 w = __ldg(twp + b);
-#pragma unroll
-                for (int kk = 0; kk < half; kk++) {
-                    const int k0 = b * 2 * half + kk;
-                    if (INVERSE)
-                        gs_bfly(a[j * R + k0], a[j * R + k0 + half], w.x, w.y, q, q2);
-                    else
-                        ct_bfly(a[j * R + k0], a[j * R + k0 + half], w.x, w.y, q, q2);
+                for (int b = 0; b < NB / 2; b++) {
+                    const uint4 x = tw_ld4<TWS>(t4 + (OFF / 2 + b) * T);
+                    w[2 * b] = make_uint2(x.x, x.y);
+                    w[2 * b + 1] = make_uint2(x.z, x.w);
                 }
+            } else {
+                w[0] = tw_ld2<TWS>(reinterpret_cast<const uint2 *>(t4 + (OFF / 2) * T) + (OFF % 2));
+            }
+        } else {
+            const uint2 *t = twp + ((g + j * T) / TB) * R + OFF;
+            if constexpr (NB >= 2) {
+#pragma unroll
+                for (int b = 0; b < NB / 2; b++) {
+                    const uint4 x = tw_ld4<TWS>(reinterpret_cast<const uint4 *>(t) + b);
+                    w[2 * b] = make_uint2(x.x, x.y);
+                    w[2 * b + 1] = make_uint2(x.z, x.w);
+                }
+            } else {
+                w[0] = tw_ld2<TWS>(t);
             }
         }
+#pragma unroll
+        for (int b = 0; b < NB; b++)
+#pragma unroll
+            for (int kk = 0; kk < HALF; kk++)
+#pragma unroll
+                for (int c = 0; c < NC; c++) {
+                    if constexpr (INVERSE)
+                        gs_bfly(a[c][j * R + b * 2 * HALF + kk], a[c][j * R + b * 2 * HALF + kk + HALF], w[b].x,
+                                w[b].y, q, q2);
+                    else
+                        ct_bfly(a[c][j * R + b * 2 * HALF + kk], a[c][j * R + b * 2 * HALF + kk + HALF], w[b].x,
+                                w[b].y, q, q2);
+                }
     }
 }
 
-// Whole inverse transform (without the n^{-1} scale) for one polynomial
-// held as pass-0 groups (thread g owns elements g*V .. g*V+V-1) on entry;
-// on exit the thread owns the pass-2 groups.  Two barriers per call; two
-// exchange buffers alternate so no write-after-read barrier is needed.
-template <int N>
-__device__ __forceinline__ void intt_chain(uint32_t (&a)[NttGeom<N>::V], const uint2 *__restrict__ tw, int g,
+template <int N, int TB, int R, bool INVERSE, int NC, bool TWS, int SS>
+struct PassStages {
+    static constexpr int LOGR = Log2<R>::v;
+    static __device__ __forceinline__ void run(uint32_t (&a)[NC][NttGeom<N>::V], const uint2 *__restrict__ twp, int g,
+                                               uint32_t q, uint32_t q2) {
+        ntt_stage<N, TB, R, INVERSE ? SS : (LOGR - 1 - SS), INVERSE, NC, TWS>(a, twp, g, q, q2);
+        if constexpr (SS + 1 < LOGR) PassStages<N, TB, R, INVERSE, NC, TWS, SS + 1>::run(a, twp, g, q, q2);
+    }
+};
+
+// All stages of one pass (twp = this pass's table inside the limb's table).
+template <int N, int TB, int R, bool INVERSE, int NC, bool TWS = false>
+__device__ __forceinline__ void ntt_pass(uint32_t (&a)[NC][NttGeom<N>::V], const uint2 *__restrict__ twp, int g,
+                                         uint32_t q, uint32_t q2) {
+    PassStages<N, TB, R, INVERSE, NC, TWS, 0>::run(a, twp, g, q, q2);
+}
+
+// Whole inverse transform (without the n^{-1} scale) of NC polynomials held
+// as pass-0 groups (thread g owns elements g*V .. g*V+V-1) on entry; on exit
+// the thread owns the pass-2 groups.  tw = the limb's inverse table.  Two
+// barriers per call; bufA/bufB (NC exchange buffers each) alternate, so no
+// write-after-read barrier is needed between consecutive calls.
+template <int N, int NC>
+__device__ __forceinline__ void intt_chain(uint32_t (&a)[NC][NttGeom<N>::V], const uint2 *__restrict__ tw, int g,
                                            uint32_t q, uint32_t q2, uint32_t *bufA, uint32_t *bufB) {
     using Gm = NttGeom<N>;
-    ntt_pass<N, Gm::TB0, Gm::R0, true>(a, tw, g, q, q2);
-    smem_store<N, Gm::TB0, Gm::R0>(bufA, a, g);
+    ntt_pass<N, Gm::TB0, Gm::R0, true, NC>(a, tw + Gm::TW0, g, q, q2);
+    smem_store<N, Gm::TB0, Gm::R0, NC>(bufA, a, g);
     __syncthreads();
-    smem_load<N, Gm::TB1, Gm::R1>(bufA, a, g);
-    ntt_pass<N, Gm::TB1, Gm::R1, true>(a, tw, g, q, q2);
-    smem_store<N, Gm::TB1, Gm::R1>(bufB, a, g);
+    smem_load<N, Gm::TB1, Gm::R1, NC>(bufA, a, g);
+    ntt_pass<N, Gm::TB1, Gm::R1, true, NC>(a, tw + Gm::TW1, g, q, q2);
+    smem_store<N, Gm::TB1, Gm::R1, NC>(bufB, a, g);
     __syncthreads();
-    smem_load<N, Gm::TB2, Gm::R2>(bufB, a, g);
-    ntt_pass<N, Gm::TB2, Gm::R2, true>(a, tw, g, q, q2);
+    smem_load<N, Gm::TB2, Gm::R2, NC>(bufB, a, g);
+    ntt_pass<N, Gm::TB2, Gm::R2, true, NC>(a, tw + Gm::TW2, g, q, q2);
+}
+
+// Named barrier over the `nthreads` threads of one thread group.
+__device__ __forceinline__ void group_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Inverse transform for one T-thread group of a multi-group CTA, with the
+// twiddle table in shared memory and a single exchange buffer per
+// polynomial (four named barriers: the first protects the buffer against
+// the previous call's last reads).
+template <int N, int NC>
+__device__ __forceinline__ void intt_chain_group(uint32_t (&a)[NC][NttGeom<N>::V], const uint2 *tw_smem, int g,
+                                                 uint32_t q, uint32_t q2, uint32_t *buf, int bar_id) {
+    using Gm = NttGeom<N>;
+    ntt_pass<N, Gm::TB0, Gm::R0, true, NC, true>(a, tw_smem + Gm::TW0, g, q, q2);
+    group_sync(bar_id, Gm::T);
+    smem_store<N, Gm::TB0, Gm::R0, NC>(buf, a, g);
+    group_sync(bar_id, Gm::T);
+    smem_load<N, Gm::TB1, Gm::R1, NC>(buf, a, g);
+    ntt_pass<N, Gm::TB1, Gm::R1, true, NC, true>(a, tw_smem + Gm::TW1, g, q, q2);
+    group_sync(bar_id, Gm::T);
+    smem_store<N, Gm::TB1, Gm::R1, NC>(buf, a, g);
+    group_sync(bar_id, Gm::T);
+    smem_load<N, Gm::TB2, Gm::R2, NC>(buf, a, g);
+    ntt_pass<N, Gm::TB2, Gm::R2, true, NC, true>(a, tw_smem + Gm::TW2, g, q, q2);
 }
 
 // Whole forward transform: on entry the thread owns pass-2 groups, on exit
 // pass-0 groups (contiguous V elements, bit-reversed NTT order).
-template <int N>
-__device__ __forceinline__ void ntt_chain(uint32_t (&a)[NttGeom<N>::V], const uint2 *__restrict__ tw, int g,
+template <int N, int NC>
+__device__ __forceinline__ void ntt_chain(uint32_t (&a)[NC][NttGeom<N>::V], const uint2 *__restrict__ tw, int g,
                                           uint32_t q, uint32_t q2, uint32_t *bufA, uint32_t *bufB) {
     using Gm = NttGeom<N>;
-    ntt_pass<N, Gm::TB2, Gm::R2, false>(a, tw, g, q, q2);
-    smem_store<N, Gm::TB2, Gm::R2>(bufA, a, g);
+    ntt_pass<N, Gm::TB2, Gm::R2, false, NC>(a, tw + Gm::TW2, g, q, q2);
+    smem_store<N, Gm::TB2, Gm::R2, NC>(bufA, a, g);
     __syncthreads();
-    smem_load<N, Gm::TB1, Gm::R1>(bufA, a, g);
-    ntt_pass<N, Gm::TB1, Gm::R1, false>(a, tw, g, q, q2);
-    smem_store<N, Gm::TB1, Gm::R1>(bufB, a, g);
+    smem_load<N, Gm::TB1, Gm::R1, NC>(bufA, a, g);
+    ntt_pass<N, Gm::TB1, Gm::R1, false, NC>(a, tw + Gm::TW1, g, q, q2);
+    smem_store<N, Gm::TB1, Gm::R1, NC>(bufB, a, g);
     __syncthreads();
-    smem_load<N, Gm::TB0, Gm::R0>(bufB, a, g);
-    ntt_pass<N, Gm::TB0, Gm::R0, false>(a, tw, g, q, q2);
+    smem_load<N, Gm::TB0, Gm::R0, NC>(bufB, a, g);
+    ntt_pass<N, Gm::TB0, Gm::R0, false, NC>(a, tw + Gm::TW0, g, q, q2);
 }
 
 }  // namespace wally

@@ -17,7 +17,8 @@ import numpy as np
 
 from . import build as _build
 
-_LIB_PATH = _build.LIB
+# WALLY_LIB: load an alternative build of the same library (kernel-variant experiments).
+_LIB_PATH = os.environ.get("WALLY_LIB", _build.LIB)
 
 WALLY_MAX_LIMBS = 4
 STATUS = {0: "WALLY_OK", -1: "WALLY_E_ARG", -2: "WALLY_E_PARAMS", -3: "WALLY_E_UNKNOWN_CLUSTER",
