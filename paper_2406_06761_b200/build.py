@@ -39,16 +39,21 @@ def _stale(target: str) -> bool:
     return any(os.path.getmtime(p) > t for p in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale(LIB):
-        return LIB
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, lib: str = LIB, defines=()) -> str:
+    """Build `lib` (default: the product libwally.so).  `defines` (e.g.
+    ["WALLY_EVAL_V=2"]) build a kernel-variant library for A/B timing; the
+    binding loads it only when WALLY_LIB points at it."""
+    if not force and not _stale(lib):
+        return lib
+    bdir = BUILD if lib == LIB else os.path.join(BUILD, os.path.basename(lib) + ".d")
+    os.makedirs(bdir, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
 
     def compile_one(src):
-        obj = os.path.join(BUILD, src + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(bdir, src + ".o")
+        cmd = [NVCC, *ARCH, *FLAGS, *dflags, "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cpp"):
-            cmd = [NVCC, *FLAGS, "-x", "cu", "-c", os.path.join(CSRC, src), "-o", obj, *ARCH]
+            cmd = [NVCC, *FLAGS, *dflags, "-x", "cu", "-c", os.path.join(CSRC, src), "-o", obj, *ARCH]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)
@@ -56,11 +61,22 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
+
+
+def build_intpipe_bench(force: bool = False) -> str:
+    """The integer-pipe microbenchmark, a standalone binary."""
+    exe = os.path.join(PKG, "intpipe_bench")
+    src = os.path.join(CSRC, "intpipe_bench.cu")
+    if force or not os.path.exists(exe) or os.path.getmtime(src) > os.path.getmtime(exe) or \
+            os.path.getmtime(os.path.join(CSRC, "ntt_device.cuh")) > os.path.getmtime(exe):
+        subprocess.check_call([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-I" + CSRC, src, "-o", exe])
+    return exe
 
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+    print(build_intpipe_bench(force="--force" in sys.argv))

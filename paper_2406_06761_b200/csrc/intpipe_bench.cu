@@ -4,8 +4,8 @@
 // measured number rather than a datasheet guess.
 //
 //   imad      x = x * a + b            (IMAD, FMA-heavy pipe)
-//   imad_hi   x = umulhi(x, a) + x     (IMAD.HI + ...)
-//   iadd      x = x + a + b            (IADD3, ALU pipe)
+//   imad_hi   x = umulhi(x, a)         (IMAD.HI)
+//   iadd      x = x + b                (IADD3, ALU pipe)
 //   shoup     x = shoup_mul(x, w, wp)  (3 IMAD-pipe instructions: one modmul)
 //   gs_bfly   (X, Y) <- Harvey GS butterfly (3 IMAD + 3 ALU)
 //
@@ -40,9 +40,10 @@ __global__ void __launch_bounds__(1024) bench_kernel(uint32_t iters, uint32_t a,
     for (uint32_t i = 0; i < iters; i++) {
 #pragma unroll
         for (int c = 0; c < CHAINS; c++) {
-            if (OP == 0) x[c] = x[c] * a + b;
-            if (OP == 1) x[c] = __umulhi(x[c], a) + x[c];
-            if (OP == 2) x[c] = x[c] + a + b + i;
+            // volatile asm: one instruction per chain step, never folded across iterations
+            if (OP == 0) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[c]) : "r"(a), "r"(b));
+            if (OP == 1) asm volatile("mul.hi.u32 %0, %0, %1;" : "+r"(x[c]) : "r"(a));
+            if (OP == 2) asm volatile("add.u32 %0, %0, %1;" : "+r"(x[c]) : "r"(b));
             if (OP == 3) x[c] = shoup_mul(x[c], a, wp, q);
             if (OP == 4) gs_bfly(x[c], y[c], a, wp, q, 2 * q);
         }
@@ -96,7 +97,7 @@ int main() {
     int num_sms = 0;
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, 0);
     run<0>("imad", 1, num_sms);
-    run<1>("imad_hi_plus_add", 1, num_sms);
+    run<1>("imad_hi", 1, num_sms);
     run<2>("iadd3", 1, num_sms);
     run<3>("shoup_modmul", 1, num_sms);
     run<4>("gs_butterfly", 1, num_sms);

@@ -99,8 +99,9 @@ struct NttGeom {
     static constexpr int TB2 = 1 << (C::S0 + C::S1), R2 = 1 << C::S2;
     static_assert(R0 == V, "pass 0 must give each thread one contiguous group");
     static_assert(TB2 * R2 == N, "passes must cover log2(n) stages");
-    static constexpr int PAD_SHIFT = (N >= 8192) ? 5 : 4;
-    static constexpr int SMEM_WORDS = N + (N >> PAD_SHIFT) + 32;  // one exchange buffer
+    // one exchange buffer (largest of the two paddings of smem_pad)
+    static constexpr int PADW = (N >> C::S0) > (16 * (N >> (C::S0 + C::S1))) ? (N >> C::S0) : 16 * (N >> (C::S0 + C::S1));
+    static constexpr int SMEM_WORDS = N + PADW + 32;
     // pass-major twiddle table offsets (uint2 entries) inside one limb's table
     static constexpr int TW0 = 0, TW1 = N / TB0, TW2 = N / TB0 + N / TB1;
     static constexpr int TW_LIMB = N / TB0 + N / TB1 + N / TB2;
@@ -111,8 +112,19 @@ struct Log2 { static constexpr int v = (R <= 1) ? 0 : 1 + Log2<R / 2>::v; };
 template <>
 struct Log2<1> { static constexpr int v = 0; };
 
-template <int N>
-__device__ __forceinline__ int smem_pad(int i) { return i + (i >> NttGeom<N>::PAD_SHIFT); }
+// Exchange-buffer address of element i.  Each of the two exchanges of a
+// transform has its own padding, chosen so that both access patterns of
+// that exchange hit 32 distinct banks per warp instruction while every
+// per-thread offset stays a compile-time immediate (checked exhaustively for
+// n = 1024..8192):
+//   X = 0, between pass 0 (contiguous groups) and pass 1:  i + (i >> S0)
+//   X = 1, between pass 1 and pass 2 (stride n/R groups):  i + 16 (i >> (S0+S1))
+template <int N, int X>
+__device__ __forceinline__ int smem_pad(int i) {
+    using C = NttCfg<N>;
+    if constexpr (X == 0) return i + (i >> C::S0);
+    else return i + ((i >> (C::S0 + C::S1)) << 4);
+}
 
 template <int N, int TB, int R>
 __device__ __forceinline__ int pass_index(int g, int j, int k) {
@@ -123,7 +135,7 @@ __device__ __forceinline__ int pass_index(int g, int j, int k) {
 }
 
 // NC polynomials per thread: a[c][V]; poly c exchanges through buf + c * SMEM_WORDS.
-template <int N, int TB, int R, int NC>
+template <int N, int TB, int R, int NC, int X>
 __device__ __forceinline__ void smem_store(uint32_t *buf, const uint32_t (&a)[NC][NttGeom<N>::V], int g) {
     constexpr int V = NttGeom<N>::V, G = V / R;
 #pragma unroll
@@ -132,10 +144,10 @@ __device__ __forceinline__ void smem_store(uint32_t *buf, const uint32_t (&a)[NC
         for (int j = 0; j < G; j++)
 #pragma unroll
             for (int k = 0; k < R; k++)
-                buf[c * NttGeom<N>::SMEM_WORDS + smem_pad<N>(pass_index<N, TB, R>(g, j, k))] = a[c][j * R + k];
+                buf[c * NttGeom<N>::SMEM_WORDS + smem_pad<N, X>(pass_index<N, TB, R>(g, j, k))] = a[c][j * R + k];
 }
 
-template <int N, int TB, int R, int NC>
+template <int N, int TB, int R, int NC, int X>
 __device__ __forceinline__ void smem_load(const uint32_t *buf, uint32_t (&a)[NC][NttGeom<N>::V], int g) {
     constexpr int V = NttGeom<N>::V, G = V / R;
 #pragma unroll
@@ -144,7 +156,7 @@ __device__ __forceinline__ void smem_load(const uint32_t *buf, uint32_t (&a)[NC]
         for (int j = 0; j < G; j++)
 #pragma unroll
             for (int k = 0; k < R; k++)
-                a[c][j * R + k] = buf[c * NttGeom<N>::SMEM_WORDS + smem_pad<N>(pass_index<N, TB, R>(g, j, k))];
+                a[c][j * R + k] = buf[c * NttGeom<N>::SMEM_WORDS + smem_pad<N, X>(pass_index<N, TB, R>(g, j, k))];
 }
 
 // Twiddle fetch: plain loads when the table lives in shared memory (TWS),
@@ -240,13 +252,13 @@ __device__ __forceinline__ void intt_chain(uint32_t (&a)[NC][NttGeom<N>::V], con
                                            uint32_t q, uint32_t q2, uint32_t *bufA, uint32_t *bufB) {
     using Gm = NttGeom<N>;
     ntt_pass<N, Gm::TB0, Gm::R0, true, NC>(a, tw + Gm::TW0, g, q, q2);
-    smem_store<N, Gm::TB0, Gm::R0, NC>(bufA, a, g);
+    smem_store<N, Gm::TB0, Gm::R0, NC, 0>(bufA, a, g);
     __syncthreads();
-    smem_load<N, Gm::TB1, Gm::R1, NC>(bufA, a, g);
+    smem_load<N, Gm::TB1, Gm::R1, NC, 0>(bufA, a, g);
     ntt_pass<N, Gm::TB1, Gm::R1, true, NC>(a, tw + Gm::TW1, g, q, q2);
-    smem_store<N, Gm::TB1, Gm::R1, NC>(bufB, a, g);
+    smem_store<N, Gm::TB1, Gm::R1, NC, 1>(bufB, a, g);
     __syncthreads();
-    smem_load<N, Gm::TB2, Gm::R2, NC>(bufB, a, g);
+    smem_load<N, Gm::TB2, Gm::R2, NC, 1>(bufB, a, g);
     ntt_pass<N, Gm::TB2, Gm::R2, true, NC>(a, tw + Gm::TW2, g, q, q2);
 }
 
@@ -265,14 +277,14 @@ __device__ __forceinline__ void intt_chain_group(uint32_t (&a)[NC][NttGeom<N>::V
     using Gm = NttGeom<N>;
     ntt_pass<N, Gm::TB0, Gm::R0, true, NC, true>(a, tw_smem + Gm::TW0, g, q, q2);
     group_sync(bar_id, Gm::T);
-    smem_store<N, Gm::TB0, Gm::R0, NC>(buf, a, g);
+    smem_store<N, Gm::TB0, Gm::R0, NC, 0>(buf, a, g);
     group_sync(bar_id, Gm::T);
-    smem_load<N, Gm::TB1, Gm::R1, NC>(buf, a, g);
+    smem_load<N, Gm::TB1, Gm::R1, NC, 0>(buf, a, g);
     ntt_pass<N, Gm::TB1, Gm::R1, true, NC, true>(a, tw_smem + Gm::TW1, g, q, q2);
     group_sync(bar_id, Gm::T);
-    smem_store<N, Gm::TB1, Gm::R1, NC>(buf, a, g);
+    smem_store<N, Gm::TB1, Gm::R1, NC, 1>(buf, a, g);
     group_sync(bar_id, Gm::T);
-    smem_load<N, Gm::TB2, Gm::R2, NC>(buf, a, g);
+    smem_load<N, Gm::TB2, Gm::R2, NC, 1>(buf, a, g);
     ntt_pass<N, Gm::TB2, Gm::R2, true, NC, true>(a, tw_smem + Gm::TW2, g, q, q2);
 }
 
@@ -283,13 +295,13 @@ __device__ __forceinline__ void ntt_chain(uint32_t (&a)[NC][NttGeom<N>::V], cons
                                           uint32_t q, uint32_t q2, uint32_t *bufA, uint32_t *bufB) {
     using Gm = NttGeom<N>;
     ntt_pass<N, Gm::TB2, Gm::R2, false, NC>(a, tw + Gm::TW2, g, q, q2);
-    smem_store<N, Gm::TB2, Gm::R2, NC>(bufA, a, g);
+    smem_store<N, Gm::TB2, Gm::R2, NC, 1>(bufA, a, g);
     __syncthreads();
-    smem_load<N, Gm::TB1, Gm::R1, NC>(bufA, a, g);
+    smem_load<N, Gm::TB1, Gm::R1, NC, 1>(bufA, a, g);
     ntt_pass<N, Gm::TB1, Gm::R1, false, NC>(a, tw + Gm::TW1, g, q, q2);
-    smem_store<N, Gm::TB1, Gm::R1, NC>(bufB, a, g);
+    smem_store<N, Gm::TB1, Gm::R1, NC, 0>(bufB, a, g);
     __syncthreads();
-    smem_load<N, Gm::TB0, Gm::R0, NC>(bufB, a, g);
+    smem_load<N, Gm::TB0, Gm::R0, NC, 0>(bufB, a, g);
     ntt_pass<N, Gm::TB0, Gm::R0, false, NC>(a, tw + Gm::TW0, g, q, q2);
 }
 
