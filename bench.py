@@ -37,7 +37,16 @@ import synth  # noqa: E402
 METRIC = "encrypted query x entry dot products/sec"
 UNIT = "dot products/s"
 SM_COUNT = 148
-IMAD_PER_CLK_PER_SM = 64   # 4 SMSPs x 16 lanes (FMA-heavy pipe, rt=2 cycles/warp-instr; B300_MICROARCH.md)
+# Integer roofline: the FMA-heavy pipe issues 64 IMAD
+# per clock per SM (4 SMSPs x 16 lanes; B300_MICROARCH.md "Pipe rates",
+# rt_SMSP = 2), and IMAD.HI occupies it for two slots (measured on B200:
+# profiles/r01_intpipe_ncu.txt, 31.8 IMAD.HI vs 63.3 IMAD per clock per SM).
+# A Shoup modmul is IMAD.HI + 2 IMAD = 4 slots, so the pipe peaks at 16
+# modmuls per clock per SM (measured: 15.94).
+IMAD_SLOTS_PER_CLK_PER_SM = 64
+SLOTS_PER_MODMUL = 4
+MODMUL_PER_CLK_PER_SM = IMAD_SLOTS_PER_CLK_PER_SM / SLOTS_PER_MODMUL
+MEASURED_MODMUL_PER_CLK_PER_SM = 15.94   # intpipe_bench shoup_modmul under ncu
 
 
 def parse():
@@ -220,10 +229,15 @@ def run_wally(args, rank, world, local_rank):
     ents = synth.cluster_entries(w)
     ids_all = synth.query_clusters(w)
     C = w.num_clusters
-    owner = (np.arange(C) % world).astype(np.int32)
+    sizes = np.full(C, w.cluster_size, np.uint32)
+    E = w.n // w.d
+    P = -(-w.cluster_size // E)
+    from paper_2406_06761_b200 import wally as W
+    # cluster ownership (N > 1): greedy LPT on expected work = prior query share x P_c
+    owner = W.wally_assign_owners(synth.cluster_popularity(w) * P, world) if world > 1 else None
     srv = WallyServer(w.n, w.num_limbs, w.d, w.t, device=local_rank)
     moduli = srv.moduli
-    srv.load_clusters(np.full(C, w.cluster_size, np.uint32), owner if world > 1 else None, rank)
+    srv.load_clusters(sizes, owner, rank)
     local = srv.local_cluster_ids()
     ent_dev = torch.from_numpy(np.ascontiguousarray(ents[local]).reshape(-1, w.d)).to(dev)
     torch.cuda.synchronize()
@@ -233,26 +247,44 @@ def run_wally(args, rank, world, local_rank):
     encode_s = time.time() - te
     del ent_dev
     nsel = args.queries if args.queries > 0 else ids_all.size
-    mine = np.nonzero(owner[ids_all[:nsel]] == rank)[0] if world > 1 else np.arange(nsel)
-    ids = np.ascontiguousarray(ids_all[mine])
-    cts_all = synth.uniform_ciphertexts_torch(w, moduli, device=dev)
-    cts = cts_all[torch.from_numpy(mine).to(dev)] if (world > 1 or nsel < ids_all.size) else cts_all
-    if cts is not cts_all:
-        del cts_all
-    E = w.n // w.d
-    P = -(-w.cluster_size // E)
+    ids_in = np.ascontiguousarray(ids_all[:nsel])
+    router = None
+    if world > 1:
+        # queries arrive on the ingress rank 0 (resident in its HBM); every step
+        # broadcasts their cluster ids, routes (wally_route_plan, same on every
+        # rank) and scatters each owner's share with NCCL P2P (dist.Router)
+        from paper_2406_06761_b200.dist import Router
+        router = Router(sizes, owner, w.n, w.d, w.num_limbs, srv=srv, device=dev)
+        cts_in = synth.uniform_ciphertexts_torch(w, moduli, device=dev)[:nsel] if rank == 0 else None
+        plan = router.plan(ids_in)
+        ids = np.ascontiguousarray(ids_in[plan.share(rank)])
+    else:
+        cts_in = synth.uniform_ciphertexts_torch(w, moduli, device=dev)
+        if nsel < ids_all.size:
+            cts_in = cts_in[:nsel].contiguous()
+        ids = ids_in
     nq = int(ids.size)
     pairs = nq * P
     dots = nq * w.cluster_size
     off = srv.response_layout(ids)
-    resp = torch.empty(int(off[-1]), dtype=torch.int32, device=dev)
-    ws = srv.alloc_workspace(nq)
+    resp = torch.empty(max(1, int(off[-1])), dtype=torch.int32, device=dev)
+    ws = srv.alloc_workspace(max(nq, 1))
     torch.cuda.synchronize()
     setup_s = time.time() - t_setup
     stream = torch.cuda.current_stream()
 
+    def step():
+        if router is None:
+            srv.eval_batch(ids, cts_in, resp, ws)
+            return cts_in
+        ids_r = router.broadcast_ids(ids_in if rank == 0 else None, nsel)
+        pl = router.plan(ids_r)
+        mine = router.scatter(pl, cts_in)
+        srv.eval_batch(ids_r[pl.share(rank)], mine, resp, ws)
+        return mine
+
     for _ in range(args.warmup):
-        srv.eval_batch(ids, cts, resp, ws)
+        cts = step()
     srv.check_batch(ws)
     torch.cuda.synchronize()
     if world > 1:
@@ -269,7 +301,7 @@ def run_wally(args, rank, world, local_rank):
         t_clk0 = clk.mark()
         start.record(stream)
         for _ in range(args.steps):
-            srv.eval_batch(ids, cts, resp, ws)
+            cts = step()
         end.record(stream)
         torch.cuda.synchronize()
         t_clk1 = clk.mark()
@@ -280,35 +312,51 @@ def run_wally(args, rank, world, local_rank):
     st_batcher, st_fwd, st_fused, nb = srv.stage_times()
     srv.enable_stage_timing(False)
     srv.check_batch(ws)
+    gather_ms = None
+    if router is not None:
+        # optional response gather to the ingress, timed separately
+        ge0, ge1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        dist.barrier()
+        ge0.record(stream)
+        gathered = router.gather(router.plan(ids_in), resp)
+        ge1.record(stream)
+        torch.cuda.synchronize()
+        gather_ms = ge0.elapsed_time(ge1)
+        del gathered
 
     # max over ranks (time) and sums (work)
-    t = torch.tensor([ms, st_fused / max(nb, 1)], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms, st_fused / max(nb, 1), gather_ms or 0.0], dtype=torch.float64, device=dev)
     wk = torch.tensor([dots, pairs, nq], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(wk, op=dist.ReduceOp.SUM)
-    ms_max, fused_ms_max = float(t[0]), float(t[1])
+    ms_max, fused_ms_max, gather_ms_max = float(t[0]), float(t[1]), float(t[2])
     tot_dots, tot_pairs, tot_nq = (int(x) for x in wk.tolist())
     ms_per_step = ms_max / args.steps
     value = tot_dots / (ms_per_step / 1e3)
 
-    # roofline of the dominant (fused) kernel: integer multiply pipe
+    # roofline of the dominant (fused) kernel: the integer multiply (FMA-heavy) pipe
     peaks = measured_peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     clocks = clk.summary(t_clk0, t_clk1)
     mm = modmul_per_pair(w.n, w.num_limbs)
-    imad_per_launch = 3.0 * mm * pairs          # this rank's launch
+    modmul_per_launch = float(mm) * pairs          # this rank's launch
     fused_ms = st_fused / max(nb, 1)
-    achieved = imad_per_launch / (fused_ms / 1e3) / 1e12
-    peak = SM_COUNT * IMAD_PER_CLK_PER_SM * sm_max * 1e6 / 1e12
+    achieved = modmul_per_launch / (fused_ms / 1e3) / 1e12
+    peak = SM_COUNT * MODMUL_PER_CLK_PER_SM * sm_max * 1e6 / 1e12
     sm_now = clocks.get("sm_mhz") or sm_max
-    roofline = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TIMAD/s",
+    roofline = {"bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 4), "unit": "Tmodmul/s",
                 "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.config),
                 "frac_at_measured_clock": round(achieved / (peak * sm_now / sm_max), 4),
+                "frac_vs_microbench": round(achieved / (SM_COUNT * MEASURED_MODMUL_PER_CLK_PER_SM * sm_max * 1e6 / 1e12),
+                                            4),
+                "frac_vs_3imad_model": round(achieved * 3 / (SM_COUNT * 64 * sm_max * 1e6 / 1e12), 4),
                 "kernel": "eval_kernel (fused pointwise Shoup modmul + inverse NTT + RNS mod-switch)",
-                "per_launch": f"{pairs} pairs x {mm} modmul x 3 IMAD",
-                "peak_basis": f"{SM_COUNT} SMs x {IMAD_PER_CLK_PER_SM} IMAD/clk x {sm_max:.0f} MHz (sm_max_mhz "
-                              "of MEASURED_PEAKS.json); IMAD rate from the guide's pipe model, not measured",
+                "per_launch": f"{pairs} pairs x {mm} modmul (SURVEY.md 8(d) M_pair)",
+                "peak_basis": f"{SM_COUNT} SMs x {MODMUL_PER_CLK_PER_SM:.0f} Shoup modmul/clk/SM (64 FMA-heavy IMAD "
+                              f"slots/clk/SM, IMAD.HI = 2 slots, measured) x {sm_max:.0f} MHz (sm_max_mhz of "
+                              "MEASURED_PEAKS.json)",
                 "fused_ms_per_launch": round(fused_ms, 4),
                 "hbm_algorithmic_GBps": round(hbm_bytes_per_batch(w, nq, pairs, len(np.unique(ids)) * P)
                                               / (fused_ms / 1e3) / 1e9, 1),
@@ -322,13 +370,15 @@ def run_wally(args, rank, world, local_rank):
            "config": {"workload": w.name, "description": w.description, "n": w.n, "limbs": w.num_limbs,
                       "d": w.d, "t": w.t, "clusters": w.num_clusters, "cluster_size": w.cluster_size,
                       "queries": int(tot_nq), "pairs_per_step": int(tot_pairs), "dots_per_step": int(tot_dots),
-                      "ownership": "cluster c -> rank c mod N" if world > 1 else "single rank",
+                      "ownership": ("greedy LPT on expected work (wally_assign_owners); queries resident on "
+                                    "rank 0, scattered by NCCL P2P inside every step") if world > 1 else "single rank",
                       "l2": "inputs larger than L2 (plaintext store, query NTTs and responses >> 126 MB)"},
            "roofline": roofline,
            "stages_ms_per_step": {"batcher": round(st_batcher / max(nb, 1), 4),
                                   "forward_ntt": round(st_fwd / max(nb, 1), 4),
                                   "fused": round(fused_ms, 4)},
            "gpu_launches": int(launches),
+           "gather_ms_per_batch": round(gather_ms_max, 3) if world > 1 else None,
            "clocks": clocks,
            "setup_s": round(setup_s, 1), "encode_s": round(encode_s, 3)}
     if args.queries > 0:

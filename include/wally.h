@@ -176,6 +176,48 @@ int wally_eval_batch_host(wally_ctx *ctx, uint32_t nq, const uint32_t *cluster_o
 int wally_route_queries(const wally_ctx *ctx, uint32_t nq, const uint32_t *cluster_of_query_host,
                         int32_t *dest_rank_host);
 
+/* Cluster ownership for cluster-sharded data parallelism (DESIGN.md
+ * "Multi-GPU"): greedy longest-processing-time assignment.  Clusters are
+ * taken in descending weight_host order (ties: ascending id) and each goes
+ * to the rank with the least total weight so far (ties: lowest rank).  The
+ * weight of a cluster is the caller's expected work for it, e.g. expected
+ * queries x P_c.  Pure host computation.
+ *   weight_host  double [total_clusters], each >= 0
+ *   owner_out    int32 [total_clusters] out: rank in [0, world) */
+int wally_assign_owners(uint32_t total_clusters, const double *weight_host, uint32_t world, int32_t *owner_out);
+
+/* Routing plan of one batch arriving at an ingress rank (north_star: queries
+ * are routed to the rank owning their cluster; Alg 4's per-query work is
+ * independent, so a query's responses are produced entirely on its owner).
+ * Pure host computation, identical on every rank for the same inputs.
+ *   cluster_of_query_host  uint32 [nq]
+ *   cluster_sizes_host     uint32 [total_clusters] (entries per cluster, >= 1)
+ *   owner_host             int32 [total_clusters] (rank of each cluster; NULL = all on rank 0)
+ *   n, d                   ring degree and dimension (P_c = ceil(size_c / floor(n/d)))
+ * Outputs (caller-allocated):
+ *   counts_out        uint32 [world]: queries routed to each rank
+ *   order_out         uint32 [nq]: input indices grouped by destination rank
+ *                     (ascending rank, input order within a rank) -- the scatter's send
+ *                     order; rank r's share is order_out[sum_{s<r} counts .. +counts[r]]
+ *   resp_words_out    uint64 [world]: response words rank r produces for its share
+ *   gathered_off_out  uint64 [nq + 1] or NULL: word offset of query q's responses
+ *                     when the ranks' response buffers are concatenated in rank order
+ *                     (each rank's buffer in its local query order); [nq] = total words.
+ * Errors: WALLY_E_UNKNOWN_CLUSTER (id >= total_clusters), WALLY_E_ARG (owner not
+ * in [0, world), bad sizes); nothing is written on error. */
+int wally_route_plan(uint32_t nq, const uint32_t *cluster_of_query_host, uint32_t total_clusters,
+                     const uint32_t *cluster_sizes_host, const int32_t *owner_host, uint32_t n, uint32_t d,
+                     uint32_t world, uint32_t *counts_out, uint32_t *order_out, uint64_t *resp_words_out,
+                     uint64_t *gathered_off_out);
+
+/* Scatter-side packing on the ingress rank: out_dev[i] = query_ct_dev[index_dev[i]]
+ * for i < count, rows of 2*L*n uint32 (one query ciphertext).  Stream-ordered.
+ *   index_dev     uint32 [count] (device), each < nq
+ *   query_ct_dev  uint32 [nq][2][L][n] (device, 16-byte aligned)
+ *   out_dev       uint32 [count][2][L][n] (device, 16-byte aligned) */
+int wally_pack_queries(wally_ctx *ctx, uint32_t count, const uint32_t *index_dev, const uint32_t *query_ct_dev,
+                       uint32_t *out_dev, void *stream);
+
 /* Test hooks on the same device code as the hot path.
  * Forward NTT (the kernel of step 2): in_dev uint32 [count][L][n] canonical
  * coefficient form -> out_dev uint32 [count][L][n] NTT domain (internal,

@@ -692,3 +692,82 @@ extern "C" int wally_ntt_inverse(wally_ctx *c, const uint32_t *in, uint32_t *out
                                   &c->launches));
     return WALLY_OK;
 }
+
+// ---------------------------------------------------------------------------
+// multi-GPU routing (host logic)
+// ---------------------------------------------------------------------------
+extern "C" int wally_assign_owners(uint32_t total_clusters, const double *weight, uint32_t world, int32_t *owner) {
+    if (!weight || !owner || total_clusters == 0 || world == 0)
+        return fail(nullptr, WALLY_E_ARG, "assign_owners: bad arguments");
+    for (uint32_t c = 0; c < total_clusters; c++)
+        if (!(weight[c] >= 0.0)) return fail(nullptr, WALLY_E_ARG, "assign_owners: weight[%u] < 0 or NaN", c);
+    std::vector<uint32_t> ids(total_clusters);
+    for (uint32_t c = 0; c < total_clusters; c++) ids[c] = c;
+    std::stable_sort(ids.begin(), ids.end(), [&](uint32_t a, uint32_t b) { return weight[a] > weight[b]; });
+    std::vector<double> load(world, 0.0);
+    for (uint32_t c : ids) {
+        uint32_t best = 0;
+        for (uint32_t r = 1; r < world; r++)
+            if (load[r] < load[best]) best = r;
+        owner[c] = (int32_t)best;
+        load[best] += weight[c];
+    }
+    return WALLY_OK;
+}
+
+extern "C" int wally_route_plan(uint32_t nq, const uint32_t *ids, uint32_t total_clusters, const uint32_t *sizes,
+                                const int32_t *owner, uint32_t n, uint32_t d, uint32_t world, uint32_t *counts,
+                                uint32_t *order, uint64_t *resp_words, uint64_t *gathered_off) {
+    if ((nq && (!ids || !order)) || !sizes || !counts || !resp_words || total_clusters == 0 || world == 0 ||
+        n == 0 || d == 0 || d > n)
+        return fail(nullptr, WALLY_E_ARG, "route_plan: bad arguments");
+    for (uint32_t c = 0; c < total_clusters; c++) {
+        if (sizes[c] == 0) return fail(nullptr, WALLY_E_ARG, "route_plan: cluster %u is empty", c);
+        if (owner && (owner[c] < 0 || (uint32_t)owner[c] >= world))
+            return fail(nullptr, WALLY_E_ARG, "route_plan: owner[%u] = %d not in [0, %u)", c, owner[c], world);
+    }
+    for (uint32_t q = 0; q < nq; q++)
+        if (ids[q] >= total_clusters)
+            return fail(nullptr, WALLY_E_UNKNOWN_CLUSTER, "route_plan: query %u names cluster %u >= %u", q, ids[q],
+                        total_clusters);
+    const uint64_t E = n / d, per_pt = 2ull * n;
+    std::vector<uint32_t> cnt(world, 0), start(world, 0);
+    std::vector<uint64_t> words(world, 0);
+    for (uint32_t q = 0; q < nq; q++) {
+        const uint32_t r = owner ? (uint32_t)owner[ids[q]] : 0;
+        cnt[r]++;
+        words[r] += per_pt * ((sizes[ids[q]] + E - 1) / E);
+    }
+    for (uint32_t r = 1; r < world; r++) start[r] = start[r - 1] + cnt[r - 1];
+    std::vector<uint64_t> base(world, 0);
+    for (uint32_t r = 1; r < world; r++) base[r] = base[r - 1] + words[r - 1];
+    std::vector<uint32_t> fill(start);
+    std::vector<uint64_t> wfill(base);
+    for (uint32_t q = 0; q < nq; q++) {
+        const uint32_t r = owner ? (uint32_t)owner[ids[q]] : 0;
+        order[fill[r]++] = q;
+        if (gathered_off) {
+            gathered_off[q] = wfill[r];
+            wfill[r] += per_pt * ((sizes[ids[q]] + E - 1) / E);
+        }
+    }
+    if (gathered_off) gathered_off[nq] = world ? base[world - 1] + words[world - 1] : 0;
+    for (uint32_t r = 0; r < world; r++) {
+        counts[r] = cnt[r];
+        resp_words[r] = words[r];
+    }
+    return WALLY_OK;
+}
+
+extern "C" int wally_pack_queries(wally_ctx *c, uint32_t count, const uint32_t *index_dev, const uint32_t *query_dev,
+                                  uint32_t *out_dev, void *stream) {
+    if (!c) return WALLY_E_ARG;
+    if (count == 0) return WALLY_OK;
+    if (!index_dev || !query_dev || !out_dev) return fail(c, WALLY_E_ARG, "pack_queries: null pointer");
+    if ((uintptr_t)query_dev % 16 || (uintptr_t)out_dev % 16)
+        return fail(c, WALLY_E_ARG, "pack_queries: query and out must be 16-byte aligned");
+    cudaSetDevice(c->device);
+    const uint32_t row_words = 2u * c->p.num_limbs * c->p.n;
+    CUDA_OK(c, launch_pack_rows(index_dev, query_dev, out_dev, count, row_words, (cudaStream_t)stream, &c->launches));
+    return WALLY_OK;
+}

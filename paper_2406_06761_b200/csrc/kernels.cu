@@ -12,6 +12,7 @@
 // P:L1003 / P:L1318-1324 (modulus switch to q_0), Alg 1 P:L664-687 and
 // Alg 4 P:L794-808 (ServerInit / ServerComputation).
 
+#include <algorithm>
 #include <cstdint>
 
 #include "ntt_device.cuh"
@@ -718,7 +719,7 @@ static cudaError_t launch_eval_nl(const BatchArgs &a, cudaStream_t s, int num_sm
     static bool configured = false;
     static int blocks_per_sm = 1;
 #ifndef WALLY_EVAL_V
-#define WALLY_EVAL_V 3
+#define WALLY_EVAL_V 2
 #endif
     if constexpr (N <= 4096 && L <= 3 && WALLY_EVAL_V == 3) {
         const size_t smem = (size_t)L * Gm::TW_LIMB * sizeof(uint2) +
@@ -771,6 +772,34 @@ static cudaError_t launch_eval_n(const BatchArgs &a, cudaStream_t s, int num_sms
         case 4: return launch_eval_nl<N, 4>(a, s, num_sms);
     }
     return cudaErrorInvalidValue;
+}
+
+// Row gather for the multi-GPU query scatter: dst[i] = src[index[i]], rows of
+// row_words uint32 (a multiple of 4), 16-byte copies; one CTA row-slice per
+// (row, 4096-word chunk), grid-strided.
+__global__ void __launch_bounds__(256) pack_rows_kernel(const uint32_t *__restrict__ index,
+                                                        const uint4 *__restrict__ src, uint4 *__restrict__ dst,
+                                                        uint32_t count, uint32_t row_vec) {
+    const uint32_t chunks = (row_vec + 1023) / 1024;
+    for (uint32_t b = blockIdx.x; b < count * chunks; b += gridDim.x) {
+        const uint32_t i = b / chunks, c = b % chunks;
+        const uint4 *s = src + (size_t)index[i] * row_vec;
+        uint4 *d = dst + (size_t)i * row_vec;
+        for (uint32_t v = c * 1024 + threadIdx.x; v < min(row_vec, (c + 1) * 1024); v += blockDim.x)
+            __stcs(d + v, ldg_stream(s + v));
+    }
+}
+
+cudaError_t launch_pack_rows(const uint32_t *index, const uint32_t *src, uint32_t *dst, uint32_t count,
+                             uint32_t row_words, cudaStream_t s, uint64_t *launches) {
+    const uint32_t row_vec = row_words / 4;
+    const uint32_t chunks = (row_vec + 1023) / 1024;
+    const uint64_t work = (uint64_t)count * chunks;
+    const unsigned grid = (unsigned)std::min<uint64_t>(work, 148ull * 16);
+    pack_rows_kernel<<<grid, 256, 0, s>>>(index, reinterpret_cast<const uint4 *>(src), reinterpret_cast<uint4 *>(dst),
+                                          count, row_vec);
+    *launches += 1;
+    return cudaGetLastError();
 }
 
 cudaError_t launch_batcher(const BatchArgs &a, cudaStream_t s, uint64_t *launches) {

@@ -102,6 +102,13 @@ struct NttGeom {
     // one exchange buffer (largest of the two paddings of smem_pad)
     static constexpr int PADW = (N >> C::S0) > (16 * (N >> (C::S0 + C::S1))) ? (N >> C::S0) : 16 * (N >> (C::S0 + C::S1));
     static constexpr int SMEM_WORDS = N + PADW + 32;
+    // The exchange between pass 0 and pass 1 stays inside one warp when a
+    // thread's pass-0 group (V contiguous elements) and its pass-1 group
+    // (one group of R1 elements at stride TB1 = V) together cover exactly the
+    // warp's 32 V elements; then a __syncwarp replaces the group barrier, and
+    // both paddings of smem_pad map the warp's elements to the same private
+    // region of the buffer.
+    static constexpr bool A_IN_WARP = (V == TB1) && (V == R1);
     // pass-major twiddle table offsets (uint2 entries) inside one limb's table
     static constexpr int TW0 = 0, TW1 = N / TB0, TW2 = N / TB0 + N / TB1;
     static constexpr int TW_LIMB = N / TB0 + N / TB1 + N / TB2;
@@ -278,10 +285,10 @@ __device__ __forceinline__ void intt_chain_group(uint32_t (&a)[NC][NttGeom<N>::V
     ntt_pass<N, Gm::TB0, Gm::R0, true, NC, true>(a, tw_smem + Gm::TW0, g, q, q2);
     group_sync(bar_id, Gm::T);
     smem_store<N, Gm::TB0, Gm::R0, NC, 0>(buf, a, g);
-    group_sync(bar_id, Gm::T);
+    if constexpr (Gm::A_IN_WARP) __syncwarp(); else group_sync(bar_id, Gm::T);
     smem_load<N, Gm::TB1, Gm::R1, NC, 0>(buf, a, g);
     ntt_pass<N, Gm::TB1, Gm::R1, true, NC, true>(a, tw_smem + Gm::TW1, g, q, q2);
-    group_sync(bar_id, Gm::T);
+    if constexpr (Gm::A_IN_WARP) __syncwarp(); else group_sync(bar_id, Gm::T);
     smem_store<N, Gm::TB1, Gm::R1, NC, 1>(buf, a, g);
     group_sync(bar_id, Gm::T);
     smem_load<N, Gm::TB2, Gm::R2, NC, 1>(buf, a, g);
@@ -300,7 +307,7 @@ __device__ __forceinline__ void ntt_chain(uint32_t (&a)[NC][NttGeom<N>::V], cons
     smem_load<N, Gm::TB1, Gm::R1, NC, 1>(bufA, a, g);
     ntt_pass<N, Gm::TB1, Gm::R1, false, NC>(a, tw + Gm::TW1, g, q, q2);
     smem_store<N, Gm::TB1, Gm::R1, NC, 0>(bufB, a, g);
-    __syncthreads();
+    if constexpr (Gm::A_IN_WARP) __syncwarp(); else __syncthreads();
     smem_load<N, Gm::TB0, Gm::R0, NC, 0>(bufB, a, g);
     ntt_pass<N, Gm::TB0, Gm::R0, false, NC>(a, tw + Gm::TW0, g, q, q2);
 }

@@ -90,6 +90,8 @@ cudaError_t launch_query_ntt(const BatchArgs &a, cudaStream_t s, uint64_t *launc
 cudaError_t launch_eval(const BatchArgs &a, cudaStream_t s, int num_sms, uint64_t *launches);
 cudaError_t launch_ntt_forward(const KParams &kp, uint32_t n, uint32_t L, const uint2 *tw_fwd, const uint32_t *in,
                                uint32_t *out, uint32_t count, uint32_t *err, cudaStream_t s, uint64_t *launches);
+cudaError_t launch_pack_rows(const uint32_t *index, const uint32_t *src, uint32_t *dst, uint32_t count,
+                             uint32_t row_words, cudaStream_t s, uint64_t *launches);
 cudaError_t launch_ntt_inverse(const KParams &kp, uint32_t n, uint32_t L, const uint2 *tw_inv, const uint32_t *in,
                                uint32_t *out, uint32_t count, cudaStream_t s, uint64_t *launches);
 

@@ -30,7 +30,7 @@ EXPORTED = [
     "wally_response_layout", "wally_workspace_bytes", "wally_eval_batch", "wally_check_batch",
     "wally_fetch_responses", "wally_host_workspace_bytes", "wally_eval_batch_host", "wally_route_queries",
     "wally_ntt_forward", "wally_ntt_inverse", "wally_kernel_launches", "wally_enable_stage_timing",
-    "wally_stage_times",
+    "wally_stage_times", "wally_assign_owners", "wally_route_plan", "wally_pack_queries",
 ]
 
 
@@ -74,6 +74,10 @@ def _load():
         "wally_kernel_launches": ([vp], u64),
         "wally_enable_stage_timing": ([vp, ctypes.c_int], ctypes.c_int),
         "wally_stage_times": ([vp, P(ctypes.c_double), P(u64)], ctypes.c_int),
+        "wally_assign_owners": ([u32, P(ctypes.c_double), u32, P(i32)], ctypes.c_int),
+        "wally_route_plan": ([u32, P(u32), u32, P(u32), P(i32), u32, u32, u32, P(u32), P(u32), P(u64), P(u64)],
+                             ctypes.c_int),
+        "wally_pack_queries": ([vp, u32, vp, vp, vp, vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -107,6 +111,44 @@ def wally_find_moduli(n: int, num_limbs: int) -> list[int]:
     out = np.zeros(num_limbs, dtype=np.uint32)
     _check(lib.wally_find_moduli(n, num_limbs, _u32p(out)))
     return [int(x) for x in out]
+
+
+def wally_assign_owners(weights, world: int) -> np.ndarray:
+    """Cluster -> owning rank, greedy LPT on the given per-cluster weights (C ABI)."""
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    out = np.zeros(w.size, dtype=np.int32)
+    _check(lib.wally_assign_owners(w.size, w.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), world,
+                                   out.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))))
+    return out
+
+
+class RoutePlan:
+    """Result of wally_route_plan (see include/wally.h)."""
+
+    def __init__(self, counts, order, resp_words, gathered_off):
+        self.counts, self.order, self.resp_words, self.gathered_off = counts, order, resp_words, gathered_off
+        self.starts = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+
+    def share(self, rank: int) -> np.ndarray:
+        """Input indices of the queries routed to `rank` (its local query order)."""
+        return self.order[self.starts[rank]:self.starts[rank + 1]]
+
+
+def wally_route_plan(cluster_of_query, cluster_sizes, owner, n: int, d: int, world: int) -> RoutePlan:
+    ids = np.ascontiguousarray(cluster_of_query, dtype=np.uint32)
+    sizes = np.ascontiguousarray(cluster_sizes, dtype=np.uint32)
+    own = None
+    if owner is not None:
+        owner = np.ascontiguousarray(owner, dtype=np.int32)
+        own = owner.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    counts = np.zeros(world, dtype=np.uint32)
+    order = np.zeros(ids.size, dtype=np.uint32)
+    words = np.zeros(world, dtype=np.uint64)
+    goff = np.zeros(ids.size + 1, dtype=np.uint64)
+    _check(lib.wally_route_plan(ids.size, _u32p(ids), sizes.size, _u32p(sizes), own, n, d, world, _u32p(counts),
+                                _u32p(order), words.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                goff.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))))
+    return RoutePlan(counts, order, words, goff)
 
 
 class WallyServer:
@@ -234,6 +276,13 @@ class WallyServer:
         _check(lib.wally_route_queries(self.ctx, ids.size, _u32p(ids),
                                        dest.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))), self.ctx)
         return dest
+
+    def pack_queries(self, index_dev, query_ct_dev, out_dev, stream=None):
+        """out_dev[i] = query_ct_dev[index_dev[i]] (device rows of 2*L*n uint32)."""
+        count = index_dev.numel()
+        assert out_dev.numel() >= count * 2 * self.L * self.n
+        _check(lib.wally_pack_queries(self.ctx, count, index_dev.data_ptr(), query_ct_dev.data_ptr(),
+                                      out_dev.data_ptr(), _stream(stream)), self.ctx)
 
     def ntt_forward(self, x_dev, out_dev, count: int, stream=None):
         _check(lib.wally_ntt_forward(self.ctx, x_dev.data_ptr(), out_dev.data_ptr(), count, _stream(stream)),

@@ -153,6 +153,25 @@ def query_clusters(w: Workload) -> np.ndarray:
     raise ValueError(w.query_kind)
 
 
+def cluster_popularity(w: Workload) -> np.ndarray:
+    """float64 [num_clusters]: the prior probability that a query names each
+    cluster (the distribution query_clusters draws from; used as the expected
+    load when clusters are assigned to ranks)."""
+    if w.query_kind == "single":
+        p = np.zeros(w.num_clusters)
+        p[0] = 1.0
+        return p
+    if w.query_kind in ("uniform", "size_weighted"):
+        return np.full(w.num_clusters, 1.0 / w.num_clusters)
+    if w.query_kind == "zipf":
+        perm = _rng(w.seed, _S_ZIPF).permutation(w.num_clusters)
+        weights = (np.arange(1, w.num_clusters + 1, dtype=np.float64)) ** (-w.zipf_s)
+        p = np.empty(w.num_clusters)
+        p[perm] = weights / weights.sum()
+        return p
+    raise ValueError(w.query_kind)
+
+
 def query_fake_flags(w: Workload) -> np.ndarray:
     g = _rng(w.seed, _S_FAKE)
     if w.fake_share <= 0:

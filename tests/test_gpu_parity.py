@@ -237,3 +237,52 @@ def _sampled_full_config(name, n_pairs=384, real_queries=4):
 @pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
 def test_full_config_sampled_bit_exact(name):
     _sampled_full_config(name)
+
+
+# --------------------------------------------------------------------------
+# Cluster-sharded multi-rank path (emulated on one GPU: one context per rank,
+# run one after another -- no kernel waits on another rank)
+# --------------------------------------------------------------------------
+
+def test_pack_queries_kernel():
+    w = synth.scaled(synth.WORKLOADS["c2"], num_clusters=3, cluster_size=50, num_queries=29)
+    ents = synth.cluster_entries(w)
+    srv = H.make_server(w, ents)
+    cts = synth.uniform_ciphertexts_torch(w, srv.moduli)
+    idx = torch.tensor(np.random.default_rng(1).permutation(29)[:17].astype(np.int32)).cuda()
+    out = torch.empty((17, 2, w.num_limbs, w.n), dtype=torch.int32, device="cuda")
+    srv.pack_queries(idx, cts, out)
+    torch.cuda.synchronize()
+    assert torch.equal(out, cts[idx.long()])
+    srv.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_ranks_bit_identical_to_single_rank(world):
+    from paper_2406_06761_b200 import wally as W
+    w = synth.scaled(synth.WORKLOADS["c5"], num_clusters=40, cluster_size=70, num_queries=97)
+    ents = synth.cluster_entries(w)
+    ids = synth.query_clusters(w)
+    one = H.make_server(w, ents)
+    cts = synth.uniform_ciphertexts_torch(w, one.moduli)
+    ref, ref_off = H.run_batch(one, ids, cts)
+    one.close()
+    sizes = np.full(w.num_clusters, w.cluster_size, np.uint32)
+    owner = W.wally_assign_owners(synth.cluster_popularity(w), world)
+    plan = W.wally_route_plan(ids, sizes, owner, w.n, w.d, world)
+    gathered = np.empty(int(plan.gathered_off[-1]), np.uint32)
+    base = np.concatenate([[0], np.cumsum(plan.resp_words.astype(np.int64))])
+    for r in range(world):
+        srv = H.make_server(w, ents, owner=owner, rank=r)
+        share = plan.share(r)
+        idx = torch.from_numpy(share.astype(np.int32)).cuda()
+        mine = torch.empty((share.size, 2, w.num_limbs, w.n), dtype=torch.int32, device="cuda")
+        srv.pack_queries(idx, cts, mine)
+        resp, _ = H.run_batch(srv, np.ascontiguousarray(ids[share]), mine)
+        assert resp.size == int(plan.resp_words[r])
+        gathered[base[r]:base[r + 1]] = resp
+        srv.close()
+    for q in range(ids.size):
+        words = int(ref_off[q + 1] - ref_off[q])
+        g0 = int(plan.gathered_off[q])
+        assert np.array_equal(gathered[g0:g0 + words], ref[int(ref_off[q]):int(ref_off[q + 1])]), q
