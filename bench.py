@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--quiet", action="store_true")
+    ap.add_argument("--resp", default="compact", choices=["compact", "full"],
+                    help="response format: compact = c0 only at the E result coefficients + c1 (SURVEY 8(f)-1)")
     ap.add_argument("--queries", type=int, default=0,
                     help="profiling only: evaluate just the first Q queries of the batch (not a bench line)")
     return ap.parse_args()
@@ -83,13 +85,13 @@ def modmul_per_pair(n: int, L: int) -> int:
     return 2 * (L * n + L * (n // 2) * lg + n * L * (L - 1) // 2)
 
 
-def hbm_bytes_per_batch(w, nq, pairs, clusters_touched_pts):
+def hbm_bytes_per_batch(w, nq, pairs, clusters_touched_pts, words_per_pt):
     """Algorithmic HBM bytes of the fused kernel for one batch: every needed
     plaintext (values + Shoup companions) read once, every query's NTT form
     read once, every response written once."""
     pt = clusters_touched_pts * w.num_limbs * 2 * w.n * 4
     q = nq * 2 * w.num_limbs * w.n * 4
-    r = pairs * 2 * w.n * 4
+    r = pairs * words_per_pt * 4
     return pt + q + r
 
 
@@ -235,7 +237,8 @@ def run_wally(args, rank, world, local_rank):
     from paper_2406_06761_b200 import wally as W
     # cluster ownership (N > 1): greedy LPT on expected work = prior query share x P_c
     owner = W.wally_assign_owners(synth.cluster_popularity(w) * P, world) if world > 1 else None
-    srv = WallyServer(w.n, w.num_limbs, w.d, w.t, device=local_rank)
+    fmt = W.WALLY_RESP_COMPACT if args.resp == "compact" else W.WALLY_RESP_FULL
+    srv = WallyServer(w.n, w.num_limbs, w.d, w.t, device=local_rank, resp_format=fmt)
     moduli = srv.moduli
     srv.load_clusters(sizes, owner, rank)
     local = srv.local_cluster_ids()
@@ -358,7 +361,8 @@ def run_wally(args, rank, world, local_rank):
                               f"slots/clk/SM, IMAD.HI = 2 slots, measured) x {sm_max:.0f} MHz (sm_max_mhz of "
                               "MEASURED_PEAKS.json)",
                 "fused_ms_per_launch": round(fused_ms, 4),
-                "hbm_algorithmic_GBps": round(hbm_bytes_per_batch(w, nq, pairs, len(np.unique(ids)) * P)
+                "hbm_algorithmic_GBps": round(hbm_bytes_per_batch(w, nq, pairs, len(np.unique(ids)) * P,
+                                                                  srv.words_per_plaintext)
                                               / (fused_ms / 1e3) / 1e9, 1),
                 "hbm_peak_GBps": peaks.get("hbm_gbs")}
 
@@ -370,6 +374,9 @@ def run_wally(args, rank, world, local_rank):
            "config": {"workload": w.name, "description": w.description, "n": w.n, "limbs": w.num_limbs,
                       "d": w.d, "t": w.t, "clusters": w.num_clusters, "cluster_size": w.cluster_size,
                       "queries": int(tot_nq), "pairs_per_step": int(tot_pairs), "dots_per_step": int(tot_dots),
+                      "response_format": args.resp + (" (c0 at the E result coefficients + c1, "
+                                                      f"{srv.words_per_plaintext} words per plaintext)"
+                                                      if args.resp == "compact" else " ([2][n] per plaintext)"),
                       "ownership": ("greedy LPT on expected work (wally_assign_owners); queries resident on "
                                     "rank 0, scattered by NCCL P2P inside every step") if world > 1 else "single rank",
                       "l2": "inputs larger than L2 (plaintext store, query NTTs and responses >> 126 MB)"},

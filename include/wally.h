@@ -25,8 +25,9 @@
  *   - Query ciphertexts: uint32 [nq][2][L][n] in coefficient form, component 0
  *     is c0, component 1 is c1 (input-query order).
  *   - Responses: for query q (input order), P(c_q) ciphertexts in plaintext
- *     order, each uint32 [2][n] mod q_0.  Query q's first word is at
- *     offsets[q] as returned by wally_response_layout (reading S12).
+ *     order, each in the context's response format (uint32 [2][n] mod q_0, or
+ *     the compact form below).  Query q's first word is at offsets[q] as
+ *     returned by wally_response_layout (reading S12).
  *   - "dev" pointers are CUDA device pointers on the context's device; "host"
  *     pointers are CPU memory.  The caller owns every buffer it passes; the
  *     library never frees them.  Device buffers the library needs beyond its
@@ -66,19 +67,34 @@ typedef enum {
 
 typedef struct wally_ctx wally_ctx;
 
+/* Response formats (per (query, plaintext) pair, all words mod q_0):
+ *   WALLY_RESP_FULL     [2][n]: c0' and c1' in full (2n words).
+ *   WALLY_RESP_COMPACT  c0' only at the E result coefficients j*d + d - 1
+ *                       (j < E = floor(n/d)), padded with zeros to
+ *                       E4 = 4*ceil(E/4) words, followed by c1' [n]
+ *                       (E4 + n words).  Decrypting result coefficient k needs
+ *                       c0'[k] and all of c1' (c0' + c1' s), so this
+ *                       carries the same plaintext information in about half
+ *                       the bytes -- the response compression of P:L1003-1007 /
+ *                       P:L1035 ("sparse c0"). */
+#define WALLY_RESP_FULL 0u
+#define WALLY_RESP_COMPACT 1u
+
 /* Scheme parameters.
  *   n          ring degree, a power of two in {1024, 2048, 4096, 8192}
  *   num_limbs  L in [1, 4]
  *   t          plaintext modulus (only used for documentation / validation: t >= 2)
  *   d          embedding dimension, 1 <= d <= n  (d need not divide n)
  *   moduli     q_0 < q_1 < ... < q_{L-1}: distinct primes < 2^30, each = 1 mod 2n,
- *              with q_{L-1} < 2 q_0 ("q_i = 1 mod 2n"; readings S5, S6). */
+ *              with q_{L-1} < 2 q_0 ("q_i = 1 mod 2n"; readings S5, S6).
+ *   resp_format WALLY_RESP_FULL or WALLY_RESP_COMPACT (see above). */
 typedef struct {
     uint32_t n;
     uint32_t num_limbs;
     uint32_t t;
     uint32_t d;
     uint32_t moduli[WALLY_MAX_LIMBS];
+    uint32_t resp_format;
 } wally_params;
 
 /* The L largest primes q < 2^30 with q = 1 (mod 2n), written ascending into
@@ -119,6 +135,10 @@ int wally_local_entry_count(const wally_ctx *ctx, uint64_t *count_out);
  *                context keeps using it until the next encode or destroy. */
 int wally_encode_plaintexts_ntt(wally_ctx *ctx, const int8_t *entries_dev, void *store_dev, size_t store_bytes,
                                 void *stream);
+
+/* Response words per (query, plaintext) pair for the context's format:
+ * 2n (full) or E4 + n (compact). */
+int wally_response_words_per_plaintext(const wally_ctx *ctx, uint64_t *words_out);
 
 /* Response layout of a batch (reading S12).
  *   cluster_of_query_host  uint32 [nq]
@@ -194,6 +214,7 @@ int wally_assign_owners(uint32_t total_clusters, const double *weight_host, uint
  *   cluster_sizes_host     uint32 [total_clusters] (entries per cluster, >= 1)
  *   owner_host             int32 [total_clusters] (rank of each cluster; NULL = all on rank 0)
  *   n, d                   ring degree and dimension (P_c = ceil(size_c / floor(n/d)))
+ *   resp_format            WALLY_RESP_FULL or WALLY_RESP_COMPACT (response words per plaintext)
  * Outputs (caller-allocated):
  *   counts_out        uint32 [world]: queries routed to each rank
  *   order_out         uint32 [nq]: input indices grouped by destination rank
@@ -207,7 +228,7 @@ int wally_assign_owners(uint32_t total_clusters, const double *weight_host, uint
  * in [0, world), bad sizes); nothing is written on error. */
 int wally_route_plan(uint32_t nq, const uint32_t *cluster_of_query_host, uint32_t total_clusters,
                      const uint32_t *cluster_sizes_host, const int32_t *owner_host, uint32_t n, uint32_t d,
-                     uint32_t world, uint32_t *counts_out, uint32_t *order_out, uint64_t *resp_words_out,
+                     uint32_t resp_format, uint32_t world, uint32_t *counts_out, uint32_t *order_out, uint64_t *resp_words_out,
                      uint64_t *gathered_off_out);
 
 /* Scatter-side packing on the ingress rank: out_dev[i] = query_ct_dev[index_dev[i]]

@@ -25,6 +25,7 @@ struct wally_ctx {
     int device = 0;
     int num_sms = 148;
     uint32_t E = 0;
+    uint64_t wpp = 0;  // response words per plaintext
     KParams kp{};
     uint2 *d_tw_fwd = nullptr, *d_tw_inv = nullptr;
     // cluster layout
@@ -107,6 +108,11 @@ static bool is_prime32(uint64_t n) {
         if (comp) return false;
     }
     return true;
+}
+
+static uint64_t resp_words_per_pt(uint32_t n, uint32_t d, uint32_t fmt) {
+    const uint64_t E = n / d;
+    return fmt == WALLY_RESP_COMPACT ? ((E + 3) & ~3ull) + n : 2ull * n;
 }
 
 static uint32_t shoup_companion(uint32_t w, uint32_t q) { return (uint32_t)(((uint64_t)w << 32) / q); }
@@ -230,6 +236,8 @@ extern "C" int wally_create(const wally_params *pp, int device, wally_ctx **out)
         return fail(nullptr, WALLY_E_PARAMS, "num_limbs=%u unsupported (1..%d)", p.num_limbs, WALLY_MAX_LIMBS);
     if (p.d < 1 || p.d > p.n) return fail(nullptr, WALLY_E_PARAMS, "d=%u must be in [1, n]", p.d);
     if (p.t < 2) return fail(nullptr, WALLY_E_PARAMS, "t=%u must be >= 2", p.t);
+    if (p.resp_format != WALLY_RESP_FULL && p.resp_format != WALLY_RESP_COMPACT)
+        return fail(nullptr, WALLY_E_PARAMS, "resp_format=%u unknown", p.resp_format);
     for (uint32_t i = 0; i < p.num_limbs; i++) {
         uint32_t q = p.moduli[i];
         if (q >= (1u << 30) || q % (2 * p.n) != 1 || !is_prime32(q))
@@ -246,6 +254,7 @@ extern "C" int wally_create(const wally_params *pp, int device, wally_ctx **out)
     c->p = p;
     c->device = device;
     c->E = p.n / p.d;
+    c->wpp = resp_words_per_pt(p.n, p.d, p.resp_format);
     if (cudaSetDevice(device) != cudaSuccess) { delete c; return fail(nullptr, WALLY_E_CUDA, "cudaSetDevice"); }
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
 
@@ -361,6 +370,12 @@ extern "C" int wally_load_clusters(wally_ctx *c, uint32_t total_clusters, const 
     return WALLY_OK;
 }
 
+extern "C" int wally_response_words_per_plaintext(const wally_ctx *c, uint64_t *words) {
+    if (!c || !words) return WALLY_E_ARG;
+    *words = c->wpp;
+    return WALLY_OK;
+}
+
 extern "C" int wally_plaintext_store_bytes(const wally_ctx *c, size_t *bytes) {
     if (!c || !bytes) return WALLY_E_ARG;
     if (!c->loaded) return fail(const_cast<wally_ctx *>(c), WALLY_E_STATE, "load_clusters first");
@@ -439,7 +454,7 @@ extern "C" int wally_workspace_bytes(const wally_ctx *c, uint32_t nq, size_t *by
 
 static int layout_impl(const wally_ctx *c, uint32_t nq, const uint32_t *ids, uint64_t *off, uint64_t *total) {
     uint64_t o = 0;
-    const uint64_t per = 2ull * c->p.n;
+    const uint64_t per = c->wpp;
     for (uint32_t q = 0; q < nq; q++) {
         const uint32_t cl = ids[q];
         if (cl >= c->total_clusters || c->local_of_cluster[cl] < 0)
@@ -500,6 +515,10 @@ static int eval_impl(wally_ctx *c, uint32_t nq, const uint32_t *ids, const uint3
     a.kp = c->kp;
     a.n = c->p.n;
     a.L = c->p.num_limbs;
+    a.d = c->p.d;
+    a.E = c->E;
+    a.wpp = (uint32_t)c->wpp;
+    a.compact = c->p.resp_format == WALLY_RESP_COMPACT;
     a.nq = nq;
     a.n_local = c->n_local;
     a.total_clusters = c->total_clusters;
@@ -616,7 +635,7 @@ static HostWs host_ws(const wally_ctx *c, uint32_t sub) {
     HostWs h{};
     h.ws = align256(ws_layout(sub, c->n_local, c->p.n, c->p.num_limbs).total);
     h.qstage = align256((size_t)sub * 2 * c->p.num_limbs * c->p.n * sizeof(uint32_t));
-    h.rstage = align256((size_t)sub * c->max_pt * 2 * c->p.n * sizeof(uint32_t));
+    h.rstage = align256((size_t)sub * c->max_pt * c->wpp * sizeof(uint32_t));
     h.per_slot = h.ws + h.qstage + h.rstage;
     h.total = 2 * h.per_slot;
     return h;
@@ -716,10 +735,11 @@ extern "C" int wally_assign_owners(uint32_t total_clusters, const double *weight
 }
 
 extern "C" int wally_route_plan(uint32_t nq, const uint32_t *ids, uint32_t total_clusters, const uint32_t *sizes,
-                                const int32_t *owner, uint32_t n, uint32_t d, uint32_t world, uint32_t *counts,
+                                const int32_t *owner, uint32_t n, uint32_t d, uint32_t resp_format, uint32_t world,
+                                uint32_t *counts,
                                 uint32_t *order, uint64_t *resp_words, uint64_t *gathered_off) {
     if ((nq && (!ids || !order)) || !sizes || !counts || !resp_words || total_clusters == 0 || world == 0 ||
-        n == 0 || d == 0 || d > n)
+        n == 0 || d == 0 || d > n || (resp_format != WALLY_RESP_FULL && resp_format != WALLY_RESP_COMPACT))
         return fail(nullptr, WALLY_E_ARG, "route_plan: bad arguments");
     for (uint32_t c = 0; c < total_clusters; c++) {
         if (sizes[c] == 0) return fail(nullptr, WALLY_E_ARG, "route_plan: cluster %u is empty", c);
@@ -730,7 +750,7 @@ extern "C" int wally_route_plan(uint32_t nq, const uint32_t *ids, uint32_t total
         if (ids[q] >= total_clusters)
             return fail(nullptr, WALLY_E_UNKNOWN_CLUSTER, "route_plan: query %u names cluster %u >= %u", q, ids[q],
                         total_clusters);
-    const uint64_t E = n / d, per_pt = 2ull * n;
+    const uint64_t E = n / d, per_pt = resp_words_per_pt(n, d, resp_format);
     std::vector<uint32_t> cnt(world, 0), start(world, 0);
     std::vector<uint64_t> words(world, 0);
     for (uint32_t q = 0; q < nq; q++) {

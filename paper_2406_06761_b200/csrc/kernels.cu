@@ -347,10 +347,64 @@ struct ItemCursor {
     }
 };
 
+// Compact responses (WALLY_RESP_COMPACT): which of a thread's pass-2 output
+// elements are result coefficients j*d + d - 1.  In pass-2 group jj the
+// thread holds positions base + kk*TB2 (kk < R2); the solutions of
+// pos = d - 1 (mod d) form an arithmetic progression in kk, whose j = (pos+1)/d - 1
+// step is TB2 / gcd(TB2, d).  Per (group, thread) one word (j0 << 16) | mask,
+// built once per CTA into shared memory.
+template <int N>
+struct ResultMap {
+    static constexpr int G2 = NttGeom<N>::V / NttGeom<N>::R2;
+    static constexpr int WORDS = G2 * NttGeom<N>::T;
+};
+
+template <int N>
+__device__ __forceinline__ void build_result_map(uint32_t *s_rmap, uint32_t d) {
+    using Gm = NttGeom<N>;
+    for (int i = threadIdx.x; i < ResultMap<N>::WORDS; i += blockDim.x) {
+        const int jj = i / Gm::T, gg = i % Gm::T;
+        uint32_t mask = 0, j0 = 0;
+#pragma unroll 1
+        for (int kk = Gm::R2 - 1; kk >= 0; kk--) {
+            const uint32_t pos = pass_index<N, Gm::TB2, Gm::R2>(gg, jj, kk);
+            if ((pos + 1) % d == 0) {
+                mask |= 1u << kk;
+                j0 = (pos + 1) / d - 1;
+            }
+        }
+        s_rmap[i] = (j0 << 16) | mask;
+    }
+}
+
+__device__ __forceinline__ uint32_t result_map_dj(int tb2, uint32_t d) {
+    const uint32_t low = d & (~d + 1u);  // largest power of two dividing d
+    return (uint32_t)tb2 / min((uint32_t)tb2, low);
+}
+
+template <int N>
+__device__ __forceinline__ void write_results(uint32_t *dst, const uint32_t (&a)[NttGeom<N>::V], const uint32_t *s_rmap,
+                                              int g, uint32_t dj) {
+    using Gm = NttGeom<N>;
+#pragma unroll
+    for (int jj = 0; jj < ResultMap<N>::G2; jj++) {
+        const uint32_t m = s_rmap[jj * Gm::T + g];
+        if (m & 0xffffu) {
+            uint32_t j = m >> 16;
+#pragma unroll
+            for (int kk = 0; kk < Gm::R2; kk++)
+                if ((m >> kk) & 1u) {
+                    __stcs(dst + j, a[jj * Gm::R2 + kk]);
+                    j += dj;
+                }
+        }
+    }
+}
+
 // Evaluate work item `item` (cursor already positioned) for one thread group.
 template <int N, int L, bool GRP>
 __device__ __forceinline__ void eval_item(const BatchArgs &ba, const ItemCursor &cur, uint32_t item, int g,
-                                          const ChainCtx &cx) {
+                                          const ChainCtx &cx, const uint32_t *s_rmap) {
     using Gm = NttGeom<N>;
     constexpr int V = Gm::V;
     constexpr int NC = EvalCfg<N>::NC;
@@ -364,7 +418,7 @@ __device__ __forceinline__ void eval_item(const BatchArgs &ba, const ItemCursor 
     const uint32_t *phat = ba.store + (size_t)(ba.pt_base[li] + k) * L * 2 * N;
     for (uint32_t qi = qb; qi < qe; qi++) {
         const uint32_t qo = ba.perm[qi];
-        uint32_t *out_q = ba.resp + ba.resp_off[qo] + (size_t)k * 2 * N;
+        uint32_t *out_q = ba.resp + ba.resp_off[qo] + (size_t)k * ba.wpp;
         const uint32_t *chat_q = ba.chat + (size_t)qo * 2 * L * N;
 #pragma unroll 1
         for (int comp0 = 0; comp0 < 2; comp0 += NC) {
@@ -372,7 +426,13 @@ __device__ __forceinline__ void eval_item(const BatchArgs &ba, const ItemCursor 
             LimbLoop<N, L, NC, L - 1, GRP>::run(st, ba, chat_q, comp0, phat, g, cx);
 #pragma unroll
             for (int c = 0; c < NC; c++) {
-                uint32_t *dst = out_q + (size_t)(comp0 + c) * N;
+                const int comp = comp0 + c;
+                if (ba.compact && comp == 0) {
+                    write_results<N>(out_q, st.a[c], s_rmap, g, result_map_dj(Gm::TB2, ba.d));
+                    if ((uint32_t)g < ba.wpp - N - ba.E) __stcs(out_q + ba.E + g, 0u);  // zero padding to E4
+                    continue;
+                }
+                uint32_t *dst = out_q + (ba.compact ? (size_t)(ba.wpp - N) : (size_t)comp * N);
 #pragma unroll
                 for (int j = 0; j < V / Gm::R2; j++)
 #pragma unroll
@@ -392,6 +452,8 @@ __global__ void __launch_bounds__(NttGeom<N>::T, EvalCfg<N>::MINB) eval_kernel(B
     extern __shared__ uint32_t smem[];
     ChainCtx cx{ba.tw_inv, smem, smem + NC * Gm::SMEM_WORDS, 0};
     __shared__ uint32_t s_item[2];
+    __shared__ uint32_t s_rmap[ResultMap<N>::WORDS];
+    if (ba.compact) build_result_map<N>(s_rmap, ba.d);
     const int g = threadIdx.x;
     const uint32_t total = ba.misc[kMiscTotalItems];
     ItemCursor cur;
@@ -401,7 +463,7 @@ __global__ void __launch_bounds__(NttGeom<N>::T, EvalCfg<N>::MINB) eval_kernel(B
         const uint32_t item = s_item[it & 1];
         if (item >= total) break;
         cur.seek(ba, item);
-        eval_item<N, L, false>(ba, cur, item, g, cx);
+        eval_item<N, L, false>(ba, cur, item, g, cx, s_rmap);
     }
 }
 
@@ -420,11 +482,13 @@ __global__ void __launch_bounds__(kEvalGroups * NttGeom<N>::T, 1) eval_kernel_gr
     uint2 *tw = reinterpret_cast<uint2 *>(smem4);
     uint32_t *xbuf = reinterpret_cast<uint32_t *>(tw + L * Gm::TW_LIMB);
     __shared__ uint32_t s_item[kEvalGroups][2];
+    __shared__ uint32_t s_rmap[ResultMap<N>::WORDS];
     const int grp = threadIdx.x / T, g = threadIdx.x % T;
     {
         const uint4 *src = reinterpret_cast<const uint4 *>(ba.tw_inv);
         for (int i = threadIdx.x; i < L * Gm::TW_LIMB / 2; i += blockDim.x) smem4[i] = __ldg(src + i);
     }
+    if (ba.compact) build_result_map<N>(s_rmap, ba.d);
     if (g == 0) s_item[grp][0] = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
     __syncthreads();
     const ChainCtx cx{tw, xbuf + grp * NC * Gm::SMEM_WORDS, nullptr, 1 + grp};
@@ -436,204 +500,9 @@ __global__ void __launch_bounds__(kEvalGroups * NttGeom<N>::T, 1) eval_kernel_gr
         uint32_t next = 0;
         if (g == 0) next = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
         cur.seek(ba, item);
-        eval_item<N, L, true>(ba, cur, item, g, cx);
+        eval_item<N, L, true>(ba, cur, item, g, cx, s_rmap);
         if (g == 0) s_item[grp][(it + 1) & 1] = next;
         group_sync(1 + grp, T);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Fused kernel v3 (n <= 4096): one polynomial (one ciphertext component of
-// one query) per T-thread group, two groups per CTA sharing the staged
-// inverse twiddles.  A group walks a flat sequence of "tasks" (query,
-// component) over the work items it pulls; the operands of the next limb --
-// this task's limb J-1, or the next task's limb L-1, possibly in the next
-// work item -- are loaded into registers right after the current limb's
-// pointwise product, so their L2/HBM latency hides behind the current limb's
-// inverse NTT (ncu of v2: ~30% of warp stalls were long-scoreboard waits on
-// these loads at every limb start).
-// ---------------------------------------------------------------------------
-
-// Work item -> global plaintext index and query range [qb, qe) of the sorted
-// batch (32-bit indices: pointers are formed from the kernel parameters at
-// use, which keeps the prefetch pipeline's live state in few registers).
-struct ItemInfo {
-    uint32_t pt, k, qb, qe;
-};
-
-template <int N, int L>
-__device__ __forceinline__ ItemInfo decode_item(const BatchArgs &ba, ItemCursor &cur, uint32_t item) {
-    cur.seek(ba, item);
-    const uint32_t li = cur.li;
-    const uint32_t cnt = ba.counts[li];
-    const uint32_t nch = (cnt + kQueryChunk - 1) / kQueryChunk;
-    const uint32_t local = item - cur.b;
-    ItemInfo r;
-    r.k = local / nch;
-    const uint32_t ch = local % nch;
-    r.qb = ba.seg[li] + ch * kQueryChunk;
-    r.qe = min(r.qb + kQueryChunk, ba.seg[li] + cnt);
-    r.pt = ba.pt_base[li] + r.k;
-    return r;
-}
-
-// Prefetched operands of one limb of one polynomial: the query's NTT-domain
-// residues go to registers (V per thread); the plaintext's NTT-domain value
-// and Shoup companion go to a per-group shared-memory stage with cp.async
-// (no registers held while in flight).  Stage layout: 16-byte chunk v of
-// thread g at [v][g] -- a thread reads back exactly the chunks it copied, and
-// consecutive threads hit consecutive chunks (conflict-free LDS.128).
-template <int N>
-struct LimbOps {
-    uint4 c[NttGeom<N>::V / 4];
-};
-
-__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gmem_src) {
-    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem_src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
-template <int N>
-__device__ __forceinline__ void load_ops(LimbOps<N> &o, uint4 *stage, const uint32_t *chat_poly_limb,
-                                         const uint32_t *phat_limb, int g) {
-    constexpr int V = NttGeom<N>::V, T = NttGeom<N>::T;
-    const uint32_t *cv = chat_poly_limb + (size_t)g * V;
-    const uint32_t *pv = phat_limb + (size_t)g * V;
-#pragma unroll
-    for (int v = 0; v < V / 4; v++) {
-        cp_async16(stage + v * T + g, pv + 4 * v);
-        cp_async16(stage + (V / 4 + v) * T + g, pv + N + 4 * v);
-    }
-    cp_async_commit();
-#pragma unroll
-    for (int v = 0; v < V / 4; v++) o.c[v] = ldg_stream(cv + 4 * v);
-}
-
-// The operands of a task: query-NTT polynomial (query qo, component comp)
-// and plaintext pt.  valid = false: no next task.
-struct TaskRef {
-    uint32_t poly;  // qo * 2 + comp
-    uint32_t pt;
-    bool valid;
-};
-
-template <int N, int L>
-__device__ __forceinline__ const uint32_t *chat_limb(const BatchArgs &ba, uint32_t poly, int J) {
-    return ba.chat + ((size_t)poly * L + J) * N;
-}
-template <int N, int L>
-__device__ __forceinline__ const uint32_t *phat_limb(const BatchArgs &ba, uint32_t pt, int J) {
-    return ba.store + ((size_t)pt * L + J) * 2 * N;
-}
-
-template <int N, int L, int J>
-struct LimbLoopV3 {
-    static __device__ __forceinline__ void run(EvalState<N, L, 1> &st, LimbOps<N> &ops, uint4 *stage,
-                                               const BatchArgs &ba, const TaskRef &cur, const TaskRef &nx,
-                                               const uint2 *tw, uint32_t *buf, int bar, int g) {
-        constexpr int V = NttGeom<N>::V, T = NttGeom<N>::T;
-        const uint32_t q = ba.kp.q[J], q2 = ba.kp.q2[J];
-        cp_async_wait_all();
-#pragma unroll
-        for (int v = 0; v < V / 4; v++) {
-            const uint4 p = stage[v * T + g], pp = stage[(V / 4 + v) * T + g];
-            st.a[0][4 * v + 0] = shoup_mul(ops.c[v].x, p.x, pp.x, q);
-            st.a[0][4 * v + 1] = shoup_mul(ops.c[v].y, p.y, pp.y, q);
-            st.a[0][4 * v + 2] = shoup_mul(ops.c[v].z, p.z, pp.z, q);
-            st.a[0][4 * v + 3] = shoup_mul(ops.c[v].w, p.w, pp.w, q);
-        }
-        if constexpr (J > 0) {
-            load_ops<N>(ops, stage, chat_limb<N, L>(ba, cur.poly, J - 1), phat_limb<N, L>(ba, cur.pt, J - 1), g);
-        } else {
-            if (nx.valid)
-                load_ops<N>(ops, stage, chat_limb<N, L>(ba, nx.poly, L - 1), phat_limb<N, L>(ba, nx.pt, L - 1), g);
-        }
-        intt_chain_group<N, 1>(st.a, tw + (size_t)J * NttGeom<N>::TW_LIMB, g, q, q2, buf, bar);
-        ms_step<L, J, V>(st.a[0], st.rtop[0], st.acc[0], ba.kp);
-        if constexpr (J > 0)
-            LimbLoopV3<N, L, J - 1>::run(st, ops, stage, ba, cur, nx, tw, buf, bar, g);
-    }
-};
-
-template <int N, int L>
-__global__ void __launch_bounds__(kEvalGroups * NttGeom<N>::T, 1) eval_kernel_v3(BatchArgs ba) {
-    using Gm = NttGeom<N>;
-    constexpr int V = Gm::V, T = Gm::T;
-    extern __shared__ uint4 smem4[];
-    uint2 *tw = reinterpret_cast<uint2 *>(smem4);
-    uint32_t *xbuf = reinterpret_cast<uint32_t *>(tw + L * Gm::TW_LIMB);
-    __shared__ uint32_t s_item[kEvalGroups][2];
-    const int grp = threadIdx.x / T, g = threadIdx.x % T;
-    {
-        const uint4 *src = reinterpret_cast<const uint4 *>(ba.tw_inv);
-        for (int i = threadIdx.x; i < L * Gm::TW_LIMB / 2; i += blockDim.x) smem4[i] = __ldg(src + i);
-    }
-    if (g == 0) {
-        s_item[grp][0] = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
-        s_item[grp][1] = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
-    }
-    __syncthreads();
-    uint32_t *buf = xbuf + grp * Gm::SMEM_WORDS;
-    uint4 *stage = reinterpret_cast<uint4 *>(xbuf + kEvalGroups * Gm::SMEM_WORDS) + grp * (V / 2) * T;
-    const int bar = 1 + grp;
-    const uint32_t total = ba.misc[kMiscTotalItems];
-    const uint32_t item0 = s_item[grp][0], item1 = s_item[grp][1];
-    if (item0 >= total) return;  // (named barriers below involve this group only)
-    ItemCursor cur_c, nxt_c;
-    ItemInfo ci = decode_item<N, L>(ba, cur_c, item0);
-    bool has_next = item1 < total;
-    ItemInfo ni{};
-    if (has_next) ni = decode_item<N, L>(ba, nxt_c, item1);
-    uint32_t slot = 0;          // s_item slot the fetch issued during the current item writes
-    bool fetch_pending = true;  // that fetch has not been issued yet
-    uint32_t qi = ci.qb, comp = 0;
-    uint32_t qo = ba.perm[qi];
-    LimbOps<N> ops;
-    load_ops<N>(ops, stage, chat_limb<N, L>(ba, qo * 2 + comp, L - 1), phat_limb<N, L>(ba, ci.pt, L - 1), g);
-    for (;;) {
-        // the task after this one
-        TaskRef nx;
-        uint32_t nqi = 0, nqo = 0;
-        bool next_item = false;
-        nx.valid = true;
-        if (comp == 0) {
-            nqi = qi; nqo = qo; nx.pt = ci.pt; nx.poly = qo * 2 + 1;
-        } else if (qi + 1 < ci.qe) {
-            nqi = qi + 1; nqo = ba.perm[nqi]; nx.pt = ci.pt; nx.poly = nqo * 2;
-        } else if (has_next) {
-            nqi = ni.qb; nqo = ba.perm[nqi]; nx.pt = ni.pt; nx.poly = nqo * 2; next_item = true;
-        } else {
-            nx.valid = false; nx.pt = 0; nx.poly = 0;
-        }
-        const TaskRef cur{qo * 2 + comp, ci.pt, true};
-        EvalState<N, L, 1> st;
-        LimbLoopV3<N, L, L - 1>::run(st, ops, stage, ba, cur, nx, tw, buf, bar, g);
-        // (the limb loop passed group barriers: the item fetch of this item can be published)
-        if (fetch_pending) {
-            if (g == 0) s_item[grp][slot] = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
-            fetch_pending = false;
-        }
-        uint32_t *dst = ba.resp + ba.resp_off[qo] + (size_t)ci.k * 2 * N + (size_t)comp * N;
-#pragma unroll
-        for (int j = 0; j < V / Gm::R2; j++)
-#pragma unroll
-            for (int kk = 0; kk < Gm::R2; kk++)
-                __stcs(dst + pass_index<N, Gm::TB2, Gm::R2>(g, j, kk), st.a[0][j * Gm::R2 + kk]);
-        if (!nx.valid) break;
-        if (next_item) {
-            // every thread passed a barrier after the fetch above (comp 1 of the
-            // item's last query ran a limb loop after comp 0 published it)
-            const uint32_t nn = s_item[grp][slot];
-            slot ^= 1;
-            fetch_pending = true;
-            ci = ni;
-            cur_c = nxt_c;
-            has_next = nn < total;
-            if (has_next) ni = decode_item<N, L>(ba, nxt_c, nn);
-        }
-        qi = nqi; comp = nx.poly & 1; qo = nqo;
     }
 }
 
@@ -718,24 +587,7 @@ static cudaError_t launch_eval_nl(const BatchArgs &a, cudaStream_t s, int num_sm
     using Gm = NttGeom<N>;
     static bool configured = false;
     static int blocks_per_sm = 1;
-#ifndef WALLY_EVAL_V
-#define WALLY_EVAL_V 2
-#endif
-    if constexpr (N <= 4096 && L <= 3 && WALLY_EVAL_V == 3) {
-        const size_t smem = (size_t)L * Gm::TW_LIMB * sizeof(uint2) +
-                            (size_t)kEvalGroups * Gm::SMEM_WORDS * sizeof(uint32_t) +
-                            (size_t)kEvalGroups * 2 * N * sizeof(uint32_t);  // plaintext stages
-        if (!configured) {
-            cudaError_t e = allow_smem(eval_kernel_v3<N, L>, smem);
-            if (e != cudaSuccess) return e;
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, eval_kernel_v3<N, L>,
-                                                              kEvalGroups * Gm::T, smem);
-            if (e != cudaSuccess) return e;
-            if (blocks_per_sm < 1) blocks_per_sm = 1;
-            configured = true;
-        }
-        eval_kernel_v3<N, L><<<num_sms * blocks_per_sm, kEvalGroups * Gm::T, smem, s>>>(a);
-    } else if constexpr (N <= 4096) {
+    if constexpr (N <= 4096) {
         const size_t smem = (size_t)L * Gm::TW_LIMB * sizeof(uint2) +
                             (size_t)kEvalGroups * EvalCfg<N>::NC * Gm::SMEM_WORDS * sizeof(uint32_t);
         if (!configured) {

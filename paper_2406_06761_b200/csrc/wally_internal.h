@@ -46,6 +46,9 @@ enum { kErrResidue = 1u };
 struct BatchArgs {
     KParams kp;
     uint32_t n, L;
+    uint32_t d, E;                // dimension, entries per plaintext
+    uint32_t wpp;                 // response words per plaintext (2n or E4 + n)
+    uint32_t compact;             // WALLY_RESP_COMPACT
     uint32_t nq;
     uint32_t n_local;
     uint32_t total_clusters;

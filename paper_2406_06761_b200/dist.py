@@ -34,7 +34,7 @@ class Router:
     host implementation to exercise the collective logic on CPU tensors."""
 
     def __init__(self, cluster_sizes, owner, n: int, d: int, L: int, group=None, src: int = 0, srv=None,
-                 pack=None, device=None):
+                 pack=None, device=None, resp_format: int | None = None):
         import torch
         import torch.distributed as dist
         self.torch, self.dist = torch, dist
@@ -45,6 +45,9 @@ class Router:
         self.sizes = np.ascontiguousarray(cluster_sizes, dtype=np.uint32)
         self.owner = None if owner is None else np.ascontiguousarray(owner, dtype=np.int32)
         self.n, self.d, self.L = n, d, L
+        if resp_format is None:
+            resp_format = srv.resp_format if srv is not None else W.WALLY_RESP_FULL
+        self.resp_format = resp_format
         self.row = 2 * L * n
         self.device = device if device is not None else "cpu"
         if pack is None:
@@ -67,7 +70,7 @@ class Router:
         return t.cpu().numpy().view(np.uint32)
 
     def plan(self, ids: np.ndarray) -> W.RoutePlan:
-        return W.wally_route_plan(ids, self.sizes, self.owner, self.n, self.d, self.world)
+        return W.wally_route_plan(ids, self.sizes, self.owner, self.n, self.d, self.world, self.resp_format)
 
     def scatter(self, plan: W.RoutePlan, cts):
         """cts: [nq][2][L][n] int32 tensor on the ingress (ignored elsewhere).

@@ -31,6 +31,7 @@ EXPORTED = [
     "wally_fetch_responses", "wally_host_workspace_bytes", "wally_eval_batch_host", "wally_route_queries",
     "wally_ntt_forward", "wally_ntt_inverse", "wally_kernel_launches", "wally_enable_stage_timing",
     "wally_stage_times", "wally_assign_owners", "wally_route_plan", "wally_pack_queries",
+    "wally_response_words_per_plaintext",
 ]
 
 
@@ -42,7 +43,12 @@ class WallyError(RuntimeError):
 
 class wally_params(ctypes.Structure):
     _fields_ = [("n", ctypes.c_uint32), ("num_limbs", ctypes.c_uint32), ("t", ctypes.c_uint32),
-                ("d", ctypes.c_uint32), ("moduli", ctypes.c_uint32 * WALLY_MAX_LIMBS)]
+                ("d", ctypes.c_uint32), ("moduli", ctypes.c_uint32 * WALLY_MAX_LIMBS),
+                ("resp_format", ctypes.c_uint32)]
+
+
+WALLY_RESP_FULL = 0
+WALLY_RESP_COMPACT = 1
 
 
 def _load():
@@ -75,8 +81,9 @@ def _load():
         "wally_enable_stage_timing": ([vp, ctypes.c_int], ctypes.c_int),
         "wally_stage_times": ([vp, P(ctypes.c_double), P(u64)], ctypes.c_int),
         "wally_assign_owners": ([u32, P(ctypes.c_double), u32, P(i32)], ctypes.c_int),
-        "wally_route_plan": ([u32, P(u32), u32, P(u32), P(i32), u32, u32, u32, P(u32), P(u32), P(u64), P(u64)],
-                             ctypes.c_int),
+        "wally_route_plan": ([u32, P(u32), u32, P(u32), P(i32), u32, u32, u32, u32, P(u32), P(u32), P(u64),
+                              P(u64)], ctypes.c_int),
+        "wally_response_words_per_plaintext": ([vp, P(u64)], ctypes.c_int),
         "wally_pack_queries": ([vp, u32, vp, vp, vp, vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
@@ -134,7 +141,8 @@ class RoutePlan:
         return self.order[self.starts[rank]:self.starts[rank + 1]]
 
 
-def wally_route_plan(cluster_of_query, cluster_sizes, owner, n: int, d: int, world: int) -> RoutePlan:
+def wally_route_plan(cluster_of_query, cluster_sizes, owner, n: int, d: int, world: int,
+                     resp_format: int = WALLY_RESP_FULL) -> RoutePlan:
     ids = np.ascontiguousarray(cluster_of_query, dtype=np.uint32)
     sizes = np.ascontiguousarray(cluster_sizes, dtype=np.uint32)
     own = None
@@ -145,7 +153,8 @@ def wally_route_plan(cluster_of_query, cluster_sizes, owner, n: int, d: int, wor
     order = np.zeros(ids.size, dtype=np.uint32)
     words = np.zeros(world, dtype=np.uint64)
     goff = np.zeros(ids.size + 1, dtype=np.uint64)
-    _check(lib.wally_route_plan(ids.size, _u32p(ids), sizes.size, _u32p(sizes), own, n, d, world, _u32p(counts),
+    _check(lib.wally_route_plan(ids.size, _u32p(ids), sizes.size, _u32p(sizes), own, n, d, resp_format, world,
+                                _u32p(counts),
                                 _u32p(order), words.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
                                 goff.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))))
     return RoutePlan(counts, order, words, goff)
@@ -157,18 +166,25 @@ class WallyServer:
     Device buffers come from PyTorch: the plaintext store (kept for the
     server's life), per-batch workspaces and response buffers."""
 
-    def __init__(self, n: int, num_limbs: int, d: int, t: int = 65537, moduli=None, device: int = 0):
+    def __init__(self, n: int, num_limbs: int, d: int, t: int = 65537, moduli=None, device: int = 0,
+                 resp_format: int = WALLY_RESP_FULL):
         import torch
         self.torch = torch
         self.n, self.L, self.d, self.t = n, num_limbs, d, t
+        self.resp_format = resp_format
+        self.E = n // d
+        self.E4 = (self.E + 3) // 4 * 4
         self.moduli = list(moduli) if moduli is not None else wally_find_moduli(n, num_limbs)
         self.device = device
-        p = wally_params(n=n, num_limbs=num_limbs, t=t, d=d)
+        p = wally_params(n=n, num_limbs=num_limbs, t=t, d=d, resp_format=resp_format)
         for i, q in enumerate(self.moduli):
             p.moduli[i] = q
         h = ctypes.c_void_p()
         _check(lib.wally_create(ctypes.byref(p), device, ctypes.byref(h)))
         self.ctx = h
+        w = ctypes.c_uint64()
+        _check(lib.wally_response_words_per_plaintext(self.ctx, ctypes.byref(w)), self.ctx)
+        self.words_per_plaintext = w.value
         self.store = None
         self._ws = None
 

@@ -7,11 +7,11 @@ import synth
 from oracle import capi
 
 
-def make_server(w: synth.Workload, entries: np.ndarray, owner=None, rank=0, device=0):
+def make_server(w: synth.Workload, entries: np.ndarray, owner=None, rank=0, device=0, resp_format=0):
     """Build and encode a WallyServer for workload w with entries int8 [C][S][d]."""
     import torch
     from paper_2406_06761_b200.wally import WallyServer
-    srv = WallyServer(w.n, w.num_limbs, w.d, w.t, device=device)
+    srv = WallyServer(w.n, w.num_limbs, w.d, w.t, device=device, resp_format=resp_format)
     C = entries.shape[0]
     sizes = np.full(C, entries.shape[1], dtype=np.uint32)
     srv.load_clusters(sizes, owner=owner, rank=rank)
@@ -22,11 +22,11 @@ def make_server(w: synth.Workload, entries: np.ndarray, owner=None, rank=0, devi
     return srv
 
 
-def make_server_ragged(n, L, d, cluster_entries: list, device=0):
+def make_server_ragged(n, L, d, cluster_entries: list, device=0, resp_format=0):
     """Clusters of different sizes: cluster_entries[c] is int8 [S_c][d]."""
     import torch
     from paper_2406_06761_b200.wally import WallyServer
-    srv = WallyServer(n, L, d, device=device)
+    srv = WallyServer(n, L, d, device=device, resp_format=resp_format)
     sizes = np.array([e.shape[0] for e in cluster_entries], dtype=np.uint32)
     srv.load_clusters(sizes)
     ent = torch.from_numpy(np.ascontiguousarray(np.concatenate(cluster_entries).reshape(-1, d))).cuda(device)
@@ -54,9 +54,45 @@ def oracle_pairs(moduli, cts_host: np.ndarray, pcoefs: np.ndarray, pair_q, pair_
     return out
 
 
-def response_of(resp: np.ndarray, off: np.ndarray, q: int, k: int, n: int) -> np.ndarray:
-    b = int(off[q]) + k * 2 * n
-    return resp[b:b + 2 * n].reshape(2, n)
+def words_per_pt(n: int, d: int, fmt: int) -> int:
+    E = n // d
+    return (E + 3) // 4 * 4 + n if fmt == 1 else 2 * n
+
+
+def response_of(resp: np.ndarray, off: np.ndarray, q: int, k: int, n: int, d: int = 1, fmt: int = 0) -> np.ndarray:
+    """Response words of pair (q, k): [2][n] (full) or the compact word vector."""
+    wpp = words_per_pt(n, d, fmt)
+    b = int(off[q]) + k * wpp
+    r = resp[b:b + wpp]
+    return r.reshape(2, n) if fmt == 0 else r
+
+
+def result_positions(n: int, d: int) -> np.ndarray:
+    E = n // d
+    return np.arange(E) * d + d - 1
+
+
+def matches_oracle(got: np.ndarray, want_full: np.ndarray, n: int, d: int, fmt: int) -> bool:
+    """Full format: every word equal.  Compact format: c0 at the E result
+    coefficients, zero padding to E4, and c1 in full, equal to the oracle's
+    full response (the compact form carries exactly those words)."""
+    if fmt == 0:
+        return np.array_equal(got, want_full)
+    E = n // d
+    E4 = (E + 3) // 4 * 4
+    return (np.array_equal(got[:E], want_full[0][result_positions(n, d)]) and not got[E:E4].any()
+            and np.array_equal(got[E4:], want_full[1]))
+
+
+def expand_compact(got: np.ndarray, n: int, d: int) -> np.ndarray:
+    """[2][n] ciphertext with the compact c0 words at their positions (other
+    c0 coefficients zero): decrypts correctly at the result coefficients."""
+    E = n // d
+    E4 = (E + 3) // 4 * 4
+    full = np.zeros((2, n), np.uint32)
+    full[0][result_positions(n, d)] = got[:E]
+    full[1] = got[E4:]
+    return full
 
 
 def encrypt_queries(w: synth.Workload, moduli, qvecs: np.ndarray, index_base: int = 0) -> tuple:

@@ -59,12 +59,13 @@ def test_ntt_roundtrip_and_product(n, L):
 # Whole path on configs[0] (c1): every pair, real encryptions, decrypt check
 # --------------------------------------------------------------------------
 
-def test_c1_all_pairs_bit_exact_and_decrypts():
+@pytest.mark.parametrize("fmt", [0, 1], ids=["full", "compact"])
+def test_c1_all_pairs_bit_exact_and_decrypts(fmt):
     w = synth.WORKLOADS["c1"]
     ents = synth.cluster_entries(w)
     ids = synth.query_clusters(w)
     qv = synth.query_vectors(w, ids)
-    srv = H.make_server(w, ents)
+    srv = H.make_server(w, ents, resp_format=fmt)
     qs = srv.moduli
     cts, keys = H.encrypt_queries(w, qs, qv)
     resp, off = H.run_batch(srv, ids, cts)
@@ -76,8 +77,10 @@ def test_c1_all_pairs_bit_exact_and_decrypts():
     want = H.oracle_pairs(qs, cts, pcs, pq, pp)
     E = w.n // w.d
     for i, (q, k) in enumerate(zip(pq, pp)):
-        got = H.response_of(resp, off, q, k, w.n)
-        assert np.array_equal(got, want[i]), (q, k)
+        got = H.response_of(resp, off, q, k, w.n, w.d, fmt)
+        assert H.matches_oracle(got, want[i], w.n, w.d, fmt), (q, k)
+        if fmt == 1:
+            got = H.expand_compact(got, w.n, w.d)
         dec = capi.decrypt_q0(qs[0], w.t, got, keys[q].s)
         for j in range(E):
             assert int(dec[j * w.d + w.d - 1]) == int(np.dot(qv[q].astype(np.int64),
@@ -102,12 +105,13 @@ EDGE = [
 ]
 
 
+@pytest.mark.parametrize("fmt", [0, 1], ids=["full", "compact"])
 @pytest.mark.parametrize("cfg", EDGE, ids=[f"n{c['n']}_L{c['L']}_d{c['d']}" for c in EDGE])
-def test_edge_cases_bit_exact(cfg):
+def test_edge_cases_bit_exact(cfg, fmt):
     n, L, d = cfg["n"], cfg["L"], cfg["d"]
     rng = np.random.default_rng(n + 7 * L + d)
     clusters = [rng.integers(-15, 16, size=(s, d)).astype(np.int8) for s in cfg["sizes"]]
-    srv = H.make_server_ragged(n, L, d, clusters)
+    srv = H.make_server_ragged(n, L, d, clusters, resp_format=fmt)
     qs = srv.moduli
     C = len(clusters)
     # skewed ids: cluster 0 gets most queries (> one chunk), the last cluster none
@@ -120,10 +124,10 @@ def test_edge_cases_bit_exact(cfg):
     for q in range(cfg["nq"]):
         c = int(ids[q])
         P = pcs_by_c[c].shape[0]
-        assert int(off[q + 1] - off[q]) == P * 2 * n
+        assert int(off[q + 1] - off[q]) == P * H.words_per_pt(n, d, fmt)
         want = H.oracle_pairs(qs, cts[q:q + 1], pcs_by_c[c], np.zeros(P), np.arange(P))
         for k in range(P):
-            assert np.array_equal(H.response_of(resp, off, q, k, n), want[k]), (q, k)
+            assert H.matches_oracle(H.response_of(resp, off, q, k, n, d, fmt), want[k], n, d, fmt), (q, k)
     assert E >= 1
     srv.close()
 
@@ -179,11 +183,11 @@ def test_host_buffer_path_matches_device_path():
 # Full BASELINE configs, in the bench's launch configuration, sampled pairs
 # --------------------------------------------------------------------------
 
-def _sampled_full_config(name, n_pairs=384, real_queries=4):
+def _sampled_full_config(name, n_pairs=384, real_queries=4, fmt=0):
     w = synth.WORKLOADS[name]
     ents = synth.cluster_entries(w)
     ids = synth.query_clusters(w)
-    srv = H.make_server(w, ents)
+    srv = H.make_server(w, ents, resp_format=fmt)
     qs = srv.moduli
     cts_dev = synth.uniform_ciphertexts_torch(w, qs)
     # a few real encryptions (decrypt check) replace uniform stand-ins
@@ -215,15 +219,20 @@ def _sampled_full_config(name, n_pairs=384, real_queries=4):
     pcs = np.stack([capi.encode_plaintext(ents[c][k * E:(k + 1) * E], w.d, w.n) for c, k in need])
     want = H.oracle_pairs(qs, cts_h, pcs, inv, [pidx[(int(ids[q]), int(k))] for q, k in zip(pq, pp)])
     # only the sampled responses are copied back
+    wpp = H.words_per_pt(w.n, w.d, fmt)
     for i, (q, k) in enumerate(zip(pq, pp)):
-        b = int(off[q]) + int(k) * 2 * w.n
-        got = resp[b:b + 2 * w.n].cpu().numpy().view(np.uint32).reshape(2, w.n)
-        assert np.array_equal(got, want[i]), (name, q, k)
+        b = int(off[q]) + int(k) * wpp
+        got = resp[b:b + wpp].cpu().numpy().view(np.uint32)
+        if fmt == 0:
+            got = got.reshape(2, w.n)
+        assert H.matches_oracle(got, want[i], w.n, w.d, fmt), (name, q, k)
     for i, q in enumerate(real):
         c = int(ids[q])
         for k in (0, P - 1):
-            b = int(off[q]) + k * 2 * w.n
-            got = resp[b:b + 2 * w.n].cpu().numpy().view(np.uint32)
+            b = int(off[q]) + k * wpp
+            got = resp[b:b + wpp].cpu().numpy().view(np.uint32)
+            if fmt == 1:
+                got = H.expand_compact(got, w.n, w.d)
             dec = capi.decrypt_q0(qs[0], w.t, got, keys[i].s)
             cnt = min(E, w.cluster_size - k * E)
             for j in range(cnt):
@@ -234,9 +243,9 @@ def _sampled_full_config(name, n_pairs=384, real_queries=4):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
-def test_full_config_sampled_bit_exact(name):
-    _sampled_full_config(name)
+@pytest.mark.parametrize("name,fmt", [("c2", 0), ("c3", 0), ("c3", 1), ("c4", 1), ("c5", 1)])
+def test_full_config_sampled_bit_exact(name, fmt):
+    _sampled_full_config(name, fmt=fmt)
 
 
 # --------------------------------------------------------------------------
@@ -257,23 +266,23 @@ def test_pack_queries_kernel():
     srv.close()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_ranks_bit_identical_to_single_rank(world):
+@pytest.mark.parametrize("world,fmt", [(2, 0), (3, 1)])
+def test_sharded_ranks_bit_identical_to_single_rank(world, fmt):
     from paper_2406_06761_b200 import wally as W
     w = synth.scaled(synth.WORKLOADS["c5"], num_clusters=40, cluster_size=70, num_queries=97)
     ents = synth.cluster_entries(w)
     ids = synth.query_clusters(w)
-    one = H.make_server(w, ents)
+    one = H.make_server(w, ents, resp_format=fmt)
     cts = synth.uniform_ciphertexts_torch(w, one.moduli)
     ref, ref_off = H.run_batch(one, ids, cts)
     one.close()
     sizes = np.full(w.num_clusters, w.cluster_size, np.uint32)
     owner = W.wally_assign_owners(synth.cluster_popularity(w), world)
-    plan = W.wally_route_plan(ids, sizes, owner, w.n, w.d, world)
+    plan = W.wally_route_plan(ids, sizes, owner, w.n, w.d, world, fmt)
     gathered = np.empty(int(plan.gathered_off[-1]), np.uint32)
     base = np.concatenate([[0], np.cumsum(plan.resp_words.astype(np.int64))])
     for r in range(world):
-        srv = H.make_server(w, ents, owner=owner, rank=r)
+        srv = H.make_server(w, ents, owner=owner, rank=r, resp_format=fmt)
         share = plan.share(r)
         idx = torch.from_numpy(share.astype(np.int32)).cuda()
         mine = torch.empty((share.size, 2, w.num_limbs, w.n), dtype=torch.int32, device="cuda")
