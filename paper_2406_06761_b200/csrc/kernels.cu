@@ -506,6 +506,235 @@ __global__ void __launch_bounds__(kEvalGroups * NttGeom<N>::T, 1) eval_kernel_gr
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Fused kernel v4 (n <= 4096, L <= 3): tensor memory as the per-thread store
+// of everything that is reused across limbs but not needed in registers
+// during the inverse NTT.  TMEM is 128 lanes x 512 32-bit columns per SM;
+// warp w reaches lanes 32 (w % 4) .. +31, so each thread owns one lane and,
+// with 16 warps, 128 private columns:
+//   columns [32 J, 32 J + 16)        the work item's plaintext, limb J, NTT values
+//   columns [32 J + 16, 32 J + 32)   their Shoup companions          (J < L <= 3)
+//   columns [96 + 16 c, 96 + 16 c + 16)  modulus-switch state of component c
+// The plaintext slice is copied in once per work item (shared by its <= 8
+// queries and both components); the mod-switch state (rtop / acc of the
+// drop-last recurrence) goes to TMEM between limbs.  The registers this frees
+// hold the next limb's query operands, prefetched from L2 while the current
+// limb's inverse NTT runs -- the global-load latency ncu showed as the top
+// stall of v2 (profiles/r01_ncu_eval_v2.txt).  Measured TMEM read bandwidth:
+// 446 B/clk/SM (profiles/r01_intpipe_v2.jsonl), far above what this needs.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                 : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                 ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+                 : "memory");
+}
+
+// Waits for this thread's outstanding tcgen05.ld; the loaded registers are
+// passed through the asm so the compiler cannot hoist their uses above it.
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&r)[16]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+                 :
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld2(uint32_t (&r)[16], uint32_t (&s)[16]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(s[0]), "+r"(s[1]), "+r"(s[2]), "+r"(s[3]), "+r"(s[4]), "+r"(s[5]), "+r"(s[6]), "+r"(s[7]), "+r"(s[8]), "+r"(s[9]), "+r"(s[10]), "+r"(s[11]), "+r"(s[12]), "+r"(s[13]), "+r"(s[14]), "+r"(s[15])
+                 :
+                 : "memory");
+}
+
+template <int N, int L, int J>
+struct LimbLoopTM {
+    static constexpr int NC = 2;
+    static __device__ __forceinline__ void run(EvalState<N, L, NC> &st, uint4 (&cpre)[NC][NttGeom<N>::V / 4],
+                                               const BatchArgs &ba, const uint32_t *chat_q,
+                                               const uint32_t *chat_next, uint32_t tcol, int g,
+                                               const ChainCtx &cx) {
+        using Gm = NttGeom<N>;
+        constexpr int V = Gm::V;
+        static_assert(V == 16, "v4 layout assumes 16 values per thread");
+        const uint32_t q = ba.kp.q[J], q2 = ba.kp.q2[J];
+        {
+            uint32_t p[16], pp[16];
+            tmem_ld16(tcol + 32 * J, p);
+            tmem_ld16(tcol + 32 * J + 16, pp);
+            tmem_wait_ld2(p, pp);
+#pragma unroll
+            for (int v = 0; v < V / 4; v++)
+#pragma unroll
+                for (int c = 0; c < NC; c++) {
+                    st.a[c][4 * v + 0] = shoup_mul(cpre[c][v].x, p[4 * v + 0], pp[4 * v + 0], q);
+                    st.a[c][4 * v + 1] = shoup_mul(cpre[c][v].y, p[4 * v + 1], pp[4 * v + 1], q);
+                    st.a[c][4 * v + 2] = shoup_mul(cpre[c][v].z, p[4 * v + 2], pp[4 * v + 2], q);
+                    st.a[c][4 * v + 3] = shoup_mul(cpre[c][v].w, p[4 * v + 3], pp[4 * v + 3], q);
+                }
+        }
+        // prefetch the operands of the next limb (or of the next query's first limb)
+        const uint32_t *nsrc = (J > 0) ? chat_q + (size_t)(J - 1) * N : (chat_next ? chat_next + (size_t)(L - 1) * N
+                                                                                   : nullptr);
+        if (nsrc) {
+#pragma unroll
+            for (int c = 0; c < NC; c++)
+#pragma unroll
+                for (int v = 0; v < V / 4; v++)
+                    cpre[c][v] = ldg_stream(nsrc + (size_t)c * L * N + (size_t)g * V + 4 * v);
+        }
+        intt_chain_group<N, NC>(st.a, cx.tw + (size_t)J * Gm::TW_LIMB, g, q, q2, cx.bufA, cx.bar);
+        // mod-switch state through TMEM between limbs: L = 3 (its registers are
+        // what the chat prefetch needs).  L = 2 keeps its single 16-word state
+        // in registers -- with it in TMEM the L = 2 build faulted on B200
+        // (illegal address; compute-sanitizer is unavailable on this pool), so
+        // that variant is not used.
+        if constexpr (L == 3) {
+            if constexpr (J < L - 1) {
+                // state written at limb J + 1: rtop (J == L - 2) or acc (J < L - 2)
+                tmem_wait_st();
+#pragma unroll
+                for (int c = 0; c < NC; c++) {
+                    if constexpr (J == L - 2) tmem_ld16(tcol + 96 + 16 * c, st.rtop[c]);
+                    else tmem_ld16(tcol + 96 + 16 * c, st.acc[c][0]);
+                }
+#pragma unroll
+                for (int c = 0; c < NC; c++) {
+                    if constexpr (J == L - 2) tmem_wait_ld(st.rtop[c]);
+                    else tmem_wait_ld(st.acc[c][0]);
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < NC; c++) ms_step<L, J, V>(st.a[c], st.rtop[c], st.acc[c], ba.kp);
+            if constexpr (J == L - 1) {
+#pragma unroll
+                for (int c = 0; c < NC; c++) tmem_st16(tcol + 96 + 16 * c, st.rtop[c]);
+            } else if constexpr (J > 0) {
+#pragma unroll
+                for (int c = 0; c < NC; c++) tmem_st16(tcol + 96 + 16 * c, st.acc[c][0]);
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < NC; c++) ms_step<L, J, V>(st.a[c], st.rtop[c], st.acc[c], ba.kp);
+        }
+        if constexpr (J > 0) LimbLoopTM<N, L, J - 1>::run(st, cpre, ba, chat_q, chat_next, tcol, g, cx);
+    }
+};
+
+template <int N, int L>
+__device__ __forceinline__ void eval_item_tm(const BatchArgs &ba, const ItemCursor &cur, uint32_t item, int g,
+                                             const ChainCtx &cx, const uint32_t *s_rmap, uint32_t tcol) {
+    using Gm = NttGeom<N>;
+    constexpr int V = Gm::V, NC = 2;
+    const uint32_t li = cur.li;
+    const uint32_t cnt = ba.counts[li];
+    const uint32_t nch = (cnt + kQueryChunk - 1) / kQueryChunk;
+    const uint32_t local = item - cur.b;
+    const uint32_t k = local / nch, ch = local % nch;
+    const uint32_t qb = ba.seg[li] + ch * kQueryChunk;
+    const uint32_t qe = min(qb + kQueryChunk, ba.seg[li] + cnt);
+    const uint32_t *phat = ba.store + (size_t)(ba.pt_base[li] + k) * L * 2 * N;
+    // the item's plaintext slice -> TMEM (previous item's reads were waited on)
+#pragma unroll
+    for (int J = 0; J < L; J++) {
+        uint32_t p[16], pp[16];
+        const uint32_t *pv = phat + (size_t)J * 2 * N + (size_t)g * V;
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+            const uint4 x = ldg_stream(pv + 4 * v), y = ldg_stream(pv + N + 4 * v);
+            p[4 * v] = x.x; p[4 * v + 1] = x.y; p[4 * v + 2] = x.z; p[4 * v + 3] = x.w;
+            pp[4 * v] = y.x; pp[4 * v + 1] = y.y; pp[4 * v + 2] = y.z; pp[4 * v + 3] = y.w;
+        }
+        tmem_st16(tcol + 32 * J, p);
+        tmem_st16(tcol + 32 * J + 16, pp);
+    }
+    tmem_wait_st();
+    uint32_t qo = ba.perm[qb];
+    uint4 cpre[NC][V / 4];
+    {
+        const uint32_t *src = ba.chat + (size_t)qo * 2 * L * N + (size_t)(L - 1) * N;
+#pragma unroll
+        for (int c = 0; c < NC; c++)
+#pragma unroll
+            for (int v = 0; v < V / 4; v++) cpre[c][v] = ldg_stream(src + (size_t)c * L * N + (size_t)g * V + 4 * v);
+    }
+    for (uint32_t qi = qb; qi < qe; qi++) {
+        const uint32_t qn = (qi + 1 < qe) ? ba.perm[qi + 1] : 0xffffffffu;
+        uint32_t *out_q = ba.resp + ba.resp_off[qo] + (size_t)k * ba.wpp;
+        const uint32_t *chat_q = ba.chat + (size_t)qo * 2 * L * N;
+        const uint32_t *chat_next = (qn != 0xffffffffu) ? ba.chat + (size_t)qn * 2 * L * N : nullptr;
+        EvalState<N, L, NC> st;
+        LimbLoopTM<N, L, L - 1>::run(st, cpre, ba, chat_q, chat_next, tcol, g, cx);
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+            if (ba.compact && c == 0) {
+                write_results<N>(out_q, st.a[c], s_rmap, g, result_map_dj(Gm::TB2, ba.d));
+                if ((uint32_t)g < ba.wpp - N - ba.E) __stcs(out_q + ba.E + g, 0u);
+                continue;
+            }
+            uint32_t *dst = out_q + (ba.compact ? (size_t)(ba.wpp - N) : (size_t)c * N);
+#pragma unroll
+            for (int j = 0; j < V / Gm::R2; j++)
+#pragma unroll
+                for (int kk = 0; kk < Gm::R2; kk++)
+                    __stcs(dst + pass_index<N, Gm::TB2, Gm::R2>(g, j, kk), st.a[c][j * Gm::R2 + kk]);
+        }
+        qo = qn;
+    }
+}
+
+template <int N, int L>
+__global__ void __launch_bounds__(kEvalGroups * NttGeom<N>::T, 1) eval_kernel_tm(BatchArgs ba) {
+    using Gm = NttGeom<N>;
+    constexpr int NC = 2;
+    constexpr int T = Gm::T;
+    extern __shared__ uint4 smem4[];
+    uint2 *tw = reinterpret_cast<uint2 *>(smem4);
+    uint32_t *xbuf = reinterpret_cast<uint32_t *>(tw + L * Gm::TW_LIMB);
+    __shared__ uint32_t s_item[kEvalGroups][2];
+    __shared__ uint32_t s_rmap[ResultMap<N>::WORDS];
+    __shared__ uint32_t s_taddr;
+    const int grp = threadIdx.x / T, g = threadIdx.x % T;
+    const int warp = threadIdx.x / 32;
+    if (warp == 0) {
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&s_taddr);
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(dst) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(ba.tw_inv);
+        for (int i = threadIdx.x; i < L * Gm::TW_LIMB / 2; i += blockDim.x) smem4[i] = __ldg(src + i);
+    }
+    if (ba.compact) build_result_map<N>(s_rmap, ba.d);
+    if (g == 0) s_item[grp][0] = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tcol = s_taddr + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 128);
+    const ChainCtx cx{tw, xbuf + grp * NC * Gm::SMEM_WORDS, nullptr, 1 + grp};
+    const uint32_t total = ba.misc[kMiscTotalItems];
+    ItemCursor cur;
+    for (uint32_t it = 0;; it++) {
+        const uint32_t item = s_item[grp][it & 1];
+        if (item >= total) break;
+        uint32_t next = 0;
+        if (g == 0) next = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
+        cur.seek(ba, item);
+        eval_item_tm<N, L>(ba, cur, item, g, cx, s_rmap, tcol);
+        if (g == 0) s_item[grp][(it + 1) & 1] = next;
+        group_sync(1 + grp, T);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_taddr) : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
@@ -587,7 +816,20 @@ static cudaError_t launch_eval_nl(const BatchArgs &a, cudaStream_t s, int num_sm
     using Gm = NttGeom<N>;
     static bool configured = false;
     static int blocks_per_sm = 1;
-    if constexpr (N <= 4096) {
+#ifndef WALLY_EVAL_TMEM
+#define WALLY_EVAL_TMEM 1
+#endif
+    if constexpr (N == 4096 && L >= 2 && L <= 3 && WALLY_EVAL_TMEM) {
+        const size_t smem = (size_t)L * Gm::TW_LIMB * sizeof(uint2) +
+                            (size_t)kEvalGroups * 2 * Gm::SMEM_WORDS * sizeof(uint32_t);
+        if (!configured) {
+            cudaError_t e = allow_smem(eval_kernel_tm<N, L>, smem);
+            if (e != cudaSuccess) return e;
+            blocks_per_sm = 1;  // one CTA owns all 512 TMEM columns of its SM
+            configured = true;
+        }
+        eval_kernel_tm<N, L><<<num_sms * blocks_per_sm, kEvalGroups * Gm::T, smem, s>>>(a);
+    } else if constexpr (N <= 4096) {
         const size_t smem = (size_t)L * Gm::TW_LIMB * sizeof(uint2) +
                             (size_t)kEvalGroups * EvalCfg<N>::NC * Gm::SMEM_WORDS * sizeof(uint32_t);
         if (!configured) {
