@@ -173,7 +173,8 @@ def ncu_traffic(config: str):
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get(config)
+        e = d.get(config)
+        return int(e["bytes"]) if e else None
     except Exception:
         return None
 

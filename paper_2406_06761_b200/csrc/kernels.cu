@@ -410,9 +410,12 @@ __device__ __forceinline__ void eval_item(const BatchArgs &ba, const ItemCursor 
     constexpr int NC = EvalCfg<N>::NC;
     const uint32_t li = cur.li;
     const uint32_t cnt = ba.counts[li];
-    const uint32_t nch = (cnt + kQueryChunk - 1) / kQueryChunk;
     const uint32_t local = item - cur.b;
-    const uint32_t k = local / nch, ch = local % nch;
+    // chunk-major: the items of one query chunk are its P_c plaintexts in a
+    // row, so the chunk's query NTTs stay in L2 while the plaintexts stream
+    // (a hot cluster's queries can exceed L2; its plaintexts never do)
+    const uint32_t P = ba.n_pt[li];
+    const uint32_t ch = local / P, k = local % P;
     const uint32_t qb = ba.seg[li] + ch * kQueryChunk;
     const uint32_t qe = min(qb + kQueryChunk, ba.seg[li] + cnt);
     const uint32_t *phat = ba.store + (size_t)(ba.pt_base[li] + k) * L * 2 * N;
@@ -633,9 +636,12 @@ __device__ __forceinline__ void eval_item_tm(const BatchArgs &ba, const ItemCurs
     constexpr int V = Gm::V, NC = 2;
     const uint32_t li = cur.li;
     const uint32_t cnt = ba.counts[li];
-    const uint32_t nch = (cnt + kQueryChunk - 1) / kQueryChunk;
     const uint32_t local = item - cur.b;
-    const uint32_t k = local / nch, ch = local % nch;
+    // chunk-major: the items of one query chunk are its P_c plaintexts in a
+    // row, so the chunk's query NTTs stay in L2 while the plaintexts stream
+    // (a hot cluster's queries can exceed L2; its plaintexts never do)
+    const uint32_t P = ba.n_pt[li];
+    const uint32_t ch = local / P, k = local % P;
     const uint32_t qb = ba.seg[li] + ch * kQueryChunk;
     const uint32_t qe = min(qb + kQueryChunk, ba.seg[li] + cnt);
     const uint32_t *phat = ba.store + (size_t)(ba.pt_base[li] + k) * L * 2 * N;
