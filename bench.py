@@ -62,8 +62,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--quiet", action="store_true")
-    ap.add_argument("--resp", default="compact", choices=["compact", "full"],
-                    help="response format: compact = c0 only at the E result coefficients + c1 (SURVEY 8(f)-1)")
+    ap.add_argument("--resp", default="auto", choices=["auto", "compact_drop", "compact", "full"],
+                    help="response format (SURVEY 8(f)-1): compact = c0 only at the E result coefficients + c1; "
+                         "compact_drop = compact with c1's 6 LSBs dropped (24-bit, n <= 4096); auto = compact_drop "
+                         "where allowed, else compact")
     ap.add_argument("--queries", type=int, default=0,
                     help="profiling only: evaluate just the first Q queries of the batch (not a bench line)")
     return ap.parse_args()
@@ -238,7 +240,10 @@ def run_wally(args, rank, world, local_rank):
     from paper_2406_06761_b200 import wally as W
     # cluster ownership (N > 1): greedy LPT on expected work = prior query share x P_c
     owner = W.wally_assign_owners(synth.cluster_popularity(w) * P, world) if world > 1 else None
-    fmt = W.WALLY_RESP_COMPACT if args.resp == "compact" else W.WALLY_RESP_FULL
+    if args.resp == "auto":
+        args.resp = "compact_drop" if w.n <= 4096 else "compact"
+    fmt = {"full": W.WALLY_RESP_FULL, "compact": W.WALLY_RESP_COMPACT,
+           "compact_drop": W.WALLY_RESP_COMPACT_DROP}[args.resp]
     srv = WallyServer(w.n, w.num_limbs, w.d, w.t, device=local_rank, resp_format=fmt)
     moduli = srv.moduli
     srv.load_clusters(sizes, owner, rank)
@@ -375,9 +380,8 @@ def run_wally(args, rank, world, local_rank):
            "config": {"workload": w.name, "description": w.description, "n": w.n, "limbs": w.num_limbs,
                       "d": w.d, "t": w.t, "clusters": w.num_clusters, "cluster_size": w.cluster_size,
                       "queries": int(tot_nq), "pairs_per_step": int(tot_pairs), "dots_per_step": int(tot_dots),
-                      "response_format": args.resp + (" (c0 at the E result coefficients + c1, "
-                                                      f"{srv.words_per_plaintext} words per plaintext)"
-                                                      if args.resp == "compact" else " ([2][n] per plaintext)"),
+                      "response_format": f"{args.resp} ({srv.words_per_plaintext} words per plaintext; "
+                                         "include/wally.h WALLY_RESP_*)",
                       "ownership": ("greedy LPT on expected work (wally_assign_owners); queries resident on "
                                     "rank 0, scattered by NCCL P2P inside every step") if world > 1 else "single rank",
                       "l2": "inputs larger than L2 (plaintext store, query NTTs and responses >> 126 MB)"},

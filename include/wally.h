@@ -79,6 +79,20 @@ typedef struct wally_ctx wally_ctx;
  *                       P:L1035 ("sparse c0"). */
 #define WALLY_RESP_FULL 0u
 #define WALLY_RESP_COMPACT 1u
+/*   WALLY_RESP_COMPACT_DROP  as WALLY_RESP_COMPACT, and c1' additionally has
+ *                       its 6 least significant bits dropped ("Dropping
+ *                       ciphertext LSBs", reading S20: rounded,
+ *                       h = floor((c1' + 32) / 64) < 2^24 because q_0 < 2^30 - 31)
+ *                       and stored as two planes: the low 16 bits of h as
+ *                       uint16 [n], then the high 8 bits as uint8 [n]
+ *                       (E4 + 3n/4 words).  The client decrypts with
+ *                       c1' ~ 64 h mod q_0; the dropped part adds
+ *                       e_drop = -(c1' - 64 h) * s, |c1' - 64 h| <= 32, which keeps
+ *                       ||e + e_drop|| < q_0 / 2t for q_0 ~ 2^30, t = 65537,
+ *                       n <= 4096; wally_create
+ *                       rejects it for n = 8192, where the margin is too thin. */
+#define WALLY_RESP_COMPACT_DROP 2u
+#define WALLY_RESP_DROP_BITS 6u
 
 /* Scheme parameters.
  *   n          ring degree, a power of two in {1024, 2048, 4096, 8192}
@@ -87,7 +101,7 @@ typedef struct wally_ctx wally_ctx;
  *   d          embedding dimension, 1 <= d <= n  (d need not divide n)
  *   moduli     q_0 < q_1 < ... < q_{L-1}: distinct primes < 2^30, each = 1 mod 2n,
  *              with q_{L-1} < 2 q_0 ("q_i = 1 mod 2n"; readings S5, S6).
- *   resp_format WALLY_RESP_FULL or WALLY_RESP_COMPACT (see above). */
+ *   resp_format WALLY_RESP_FULL, WALLY_RESP_COMPACT or WALLY_RESP_COMPACT_DROP (see above). */
 typedef struct {
     uint32_t n;
     uint32_t num_limbs;
@@ -137,7 +151,7 @@ int wally_encode_plaintexts_ntt(wally_ctx *ctx, const int8_t *entries_dev, void 
                                 void *stream);
 
 /* Response words per (query, plaintext) pair for the context's format:
- * 2n (full) or E4 + n (compact). */
+ * 2n (full), E4 + n (compact) or E4 + 3n/4 (compact with dropped LSBs). */
 int wally_response_words_per_plaintext(const wally_ctx *ctx, uint64_t *words_out);
 
 /* Response layout of a batch (reading S12).
@@ -214,7 +228,7 @@ int wally_assign_owners(uint32_t total_clusters, const double *weight_host, uint
  *   cluster_sizes_host     uint32 [total_clusters] (entries per cluster, >= 1)
  *   owner_host             int32 [total_clusters] (rank of each cluster; NULL = all on rank 0)
  *   n, d                   ring degree and dimension (P_c = ceil(size_c / floor(n/d)))
- *   resp_format            WALLY_RESP_FULL or WALLY_RESP_COMPACT (response words per plaintext)
+ *   resp_format            WALLY_RESP_* (response words per plaintext)
  * Outputs (caller-allocated):
  *   counts_out        uint32 [world]: queries routed to each rank
  *   order_out         uint32 [nq]: input indices grouped by destination rank

@@ -59,6 +59,7 @@ def lib():
         L.or_server_pairs.restype = ctypes.c_int
         L.or_encrypt.argtypes = [c_u32, c_u32, u32p, c_u32, i32p, i8p, u32p, i32p, u32p]
         L.or_phase_q0.argtypes = [c_u32, c_u32, u32p, i8p, u32p]
+        L.or_drop_lsb.argtypes = [u32p, c_u32, c_u32, u32p]
         L.or_decrypt_q0.argtypes = [c_u32, c_u32, c_u32, u32p, i8p, u32p]
         L.or_noise_budget_q0.argtypes = [c_u32, c_u32, c_u32, u32p, i8p]
         L.or_noise_budget_q0.restype = ctypes.c_double
@@ -204,6 +205,14 @@ def phase_q0(q0: int, resp, s) -> np.ndarray:
     v = np.zeros(n, dtype=np.uint32)
     lib().or_phase_q0(n, q0, _p(r, ctypes.c_uint32), _p(s, ctypes.c_int8), _p(v, ctypes.c_uint32))
     return v
+
+
+def drop_lsb(c, b: int) -> np.ndarray:
+    """Rounded high part floor((c + 2^(b-1)) / 2^b) of canonical residues (reading S20)."""
+    x = np.ascontiguousarray(c, dtype=np.uint32).ravel()
+    out = np.zeros_like(x)
+    lib().or_drop_lsb(_p(x, ctypes.c_uint32), x.size, b, _p(out, ctypes.c_uint32))
+    return out
 
 
 def noise_budget_q0(q0: int, t: int, resp, s) -> float:

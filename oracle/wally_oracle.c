@@ -489,6 +489,19 @@ void or_decrypt_q0(uint32_t n, uint32_t q0, uint32_t t, const uint32_t *resp, co
     free(v);
 }
 
+/* Dropping ciphertext LSBs (Cheetah's method with the
+ * paper's analysis: c = 2^b c^h + c^l, decryption with 2^b c^h adds
+ * e_drop = -c^l (times s for c1)).  Reading S20: the high part is the
+ * rounded quotient, c^h = floor((c + 2^(b-1)) / 2^b), so |c^l| <= 2^(b-1).
+ * in: canonical residues mod q_0; out: c^h. */
+void or_drop_lsb(const uint32_t *c, uint32_t count, uint32_t b, uint32_t *ch)
+{
+    for (uint32_t i = 0; i < count; i++) {
+        uint64_t x = c[i];
+        ch[i] = (uint32_t)((x + (b ? (1ull << (b - 1)) : 0)) >> b);
+    }
+}
+
 /* Invariant noise budget of a single-limb response (decryption
  * is correct while ||e|| < Q/2t; budget log2(Q) - log2(2t) shrinks as noise
  * grows).  nu = max_i |[t * v_i]_{q_0}| (centered); budget =

@@ -111,8 +111,14 @@ static bool is_prime32(uint64_t n) {
 }
 
 static uint64_t resp_words_per_pt(uint32_t n, uint32_t d, uint32_t fmt) {
-    const uint64_t E = n / d;
-    return fmt == WALLY_RESP_COMPACT ? ((E + 3) & ~3ull) + n : 2ull * n;
+    const uint64_t E4 = ((uint64_t)(n / d) + 3) & ~3ull;
+    if (fmt == WALLY_RESP_COMPACT) return E4 + n;
+    if (fmt == WALLY_RESP_COMPACT_DROP) return E4 + 3ull * n / 4;
+    return 2ull * n;
+}
+
+static bool valid_resp_format(uint32_t fmt) {
+    return fmt == WALLY_RESP_FULL || fmt == WALLY_RESP_COMPACT || fmt == WALLY_RESP_COMPACT_DROP;
 }
 
 static uint32_t shoup_companion(uint32_t w, uint32_t q) { return (uint32_t)(((uint64_t)w << 32) / q); }
@@ -236,8 +242,11 @@ extern "C" int wally_create(const wally_params *pp, int device, wally_ctx **out)
         return fail(nullptr, WALLY_E_PARAMS, "num_limbs=%u unsupported (1..%d)", p.num_limbs, WALLY_MAX_LIMBS);
     if (p.d < 1 || p.d > p.n) return fail(nullptr, WALLY_E_PARAMS, "d=%u must be in [1, n]", p.d);
     if (p.t < 2) return fail(nullptr, WALLY_E_PARAMS, "t=%u must be >= 2", p.t);
-    if (p.resp_format != WALLY_RESP_FULL && p.resp_format != WALLY_RESP_COMPACT)
+    if (!valid_resp_format(p.resp_format))
         return fail(nullptr, WALLY_E_PARAMS, "resp_format=%u unknown", p.resp_format);
+    if (p.resp_format == WALLY_RESP_COMPACT_DROP && p.n > 4096)
+        return fail(nullptr, WALLY_E_PARAMS,
+                    "WALLY_RESP_COMPACT_DROP is specified for n <= 4096 (its noise bound; DESIGN.md)");
     for (uint32_t i = 0; i < p.num_limbs; i++) {
         uint32_t q = p.moduli[i];
         if (q >= (1u << 30) || q % (2 * p.n) != 1 || !is_prime32(q))
@@ -518,7 +527,8 @@ static int eval_impl(wally_ctx *c, uint32_t nq, const uint32_t *ids, const uint3
     a.d = c->p.d;
     a.E = c->E;
     a.wpp = (uint32_t)c->wpp;
-    a.compact = c->p.resp_format == WALLY_RESP_COMPACT;
+    a.compact = c->p.resp_format != WALLY_RESP_FULL;
+    a.drop = c->p.resp_format == WALLY_RESP_COMPACT_DROP;
     a.nq = nq;
     a.n_local = c->n_local;
     a.total_clusters = c->total_clusters;
@@ -739,7 +749,7 @@ extern "C" int wally_route_plan(uint32_t nq, const uint32_t *ids, uint32_t total
                                 uint32_t *counts,
                                 uint32_t *order, uint64_t *resp_words, uint64_t *gathered_off) {
     if ((nq && (!ids || !order)) || !sizes || !counts || !resp_words || total_clusters == 0 || world == 0 ||
-        n == 0 || d == 0 || d > n || (resp_format != WALLY_RESP_FULL && resp_format != WALLY_RESP_COMPACT))
+        n == 0 || d == 0 || d > n || !valid_resp_format(resp_format))
         return fail(nullptr, WALLY_E_ARG, "route_plan: bad arguments");
     for (uint32_t c = 0; c < total_clusters; c++) {
         if (sizes[c] == 0) return fail(nullptr, WALLY_E_ARG, "route_plan: cluster %u is empty", c);

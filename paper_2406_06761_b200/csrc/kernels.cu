@@ -401,12 +401,48 @@ __device__ __forceinline__ void write_results(uint32_t *dst, const uint32_t (&a)
     }
 }
 
+// Write one ciphertext component of a pair's response in the context's
+// format (include/wally.h "Response formats"); a = the component's values
+// in the pass-2 layout, canonical mod q_0.
+template <int N>
+__device__ __forceinline__ void write_component(const BatchArgs &ba, uint32_t *out_q, const uint32_t (&a)[NttGeom<N>::V],
+                                                int comp, int g, const uint32_t *s_rmap) {
+    using Gm = NttGeom<N>;
+    constexpr int V = Gm::V;
+    if (ba.compact && comp == 0) {
+        write_results<N>(out_q, a, s_rmap, g, result_map_dj(Gm::TB2, ba.d));
+        const uint32_t e4 = (ba.E + 3) & ~3u;
+        if ((uint32_t)g < e4 - ba.E) __stcs(out_q + ba.E + g, 0u);  // zero padding to E4
+        return;
+    }
+    if (ba.drop) {
+        // c1 with its 6 LSBs dropped (rounded), 24-bit planes: lo16 [N], hi8 [N]
+        uint32_t *base = out_q + ((ba.E + 3) & ~3u);
+        unsigned short *lo = reinterpret_cast<unsigned short *>(base);
+        unsigned char *hi = reinterpret_cast<unsigned char *>(base + N / 2);
+#pragma unroll
+        for (int j = 0; j < V / Gm::R2; j++)
+#pragma unroll
+            for (int kk = 0; kk < Gm::R2; kk++) {
+                const uint32_t pos = pass_index<N, Gm::TB2, Gm::R2>(g, j, kk);
+                const uint32_t h = (a[j * Gm::R2 + kk] + (1u << (WALLY_RESP_DROP_BITS - 1))) >> WALLY_RESP_DROP_BITS;
+                __stcs(lo + pos, (unsigned short)(h & 0xffffu));
+                __stcs(hi + pos, (unsigned char)(h >> 16));
+            }
+        return;
+    }
+    uint32_t *dst = out_q + (ba.compact ? (size_t)(ba.wpp - N) : (size_t)comp * N);
+#pragma unroll
+    for (int j = 0; j < V / Gm::R2; j++)
+#pragma unroll
+        for (int kk = 0; kk < Gm::R2; kk++)
+            __stcs(dst + pass_index<N, Gm::TB2, Gm::R2>(g, j, kk), a[j * Gm::R2 + kk]);
+}
+
 // Evaluate work item `item` (cursor already positioned) for one thread group.
 template <int N, int L, bool GRP>
 __device__ __forceinline__ void eval_item(const BatchArgs &ba, const ItemCursor &cur, uint32_t item, int g,
                                           const ChainCtx &cx, const uint32_t *s_rmap) {
-    using Gm = NttGeom<N>;
-    constexpr int V = Gm::V;
     constexpr int NC = EvalCfg<N>::NC;
     const uint32_t li = cur.li;
     const uint32_t cnt = ba.counts[li];
@@ -428,20 +464,7 @@ __device__ __forceinline__ void eval_item(const BatchArgs &ba, const ItemCursor 
             EvalState<N, L, NC> st;
             LimbLoop<N, L, NC, L - 1, GRP>::run(st, ba, chat_q, comp0, phat, g, cx);
 #pragma unroll
-            for (int c = 0; c < NC; c++) {
-                const int comp = comp0 + c;
-                if (ba.compact && comp == 0) {
-                    write_results<N>(out_q, st.a[c], s_rmap, g, result_map_dj(Gm::TB2, ba.d));
-                    if ((uint32_t)g < ba.wpp - N - ba.E) __stcs(out_q + ba.E + g, 0u);  // zero padding to E4
-                    continue;
-                }
-                uint32_t *dst = out_q + (ba.compact ? (size_t)(ba.wpp - N) : (size_t)comp * N);
-#pragma unroll
-                for (int j = 0; j < V / Gm::R2; j++)
-#pragma unroll
-                    for (int kk = 0; kk < Gm::R2; kk++)
-                        __stcs(dst + pass_index<N, Gm::TB2, Gm::R2>(g, j, kk), st.a[c][j * Gm::R2 + kk]);
-            }
+            for (int c = 0; c < NC; c++) write_component<N>(ba, out_q, st.a[c], comp0 + c, g, s_rmap);
         }
     }
 }
@@ -677,19 +700,7 @@ __device__ __forceinline__ void eval_item_tm(const BatchArgs &ba, const ItemCurs
         EvalState<N, L, NC> st;
         LimbLoopTM<N, L, L - 1>::run(st, cpre, ba, chat_q, chat_next, tcol, g, cx);
 #pragma unroll
-        for (int c = 0; c < NC; c++) {
-            if (ba.compact && c == 0) {
-                write_results<N>(out_q, st.a[c], s_rmap, g, result_map_dj(Gm::TB2, ba.d));
-                if ((uint32_t)g < ba.wpp - N - ba.E) __stcs(out_q + ba.E + g, 0u);
-                continue;
-            }
-            uint32_t *dst = out_q + (ba.compact ? (size_t)(ba.wpp - N) : (size_t)c * N);
-#pragma unroll
-            for (int j = 0; j < V / Gm::R2; j++)
-#pragma unroll
-                for (int kk = 0; kk < Gm::R2; kk++)
-                    __stcs(dst + pass_index<N, Gm::TB2, Gm::R2>(g, j, kk), st.a[c][j * Gm::R2 + kk]);
-        }
+        for (int c = 0; c < NC; c++) write_component<N>(ba, out_q, st.a[c], c, g, s_rmap);
         qo = qn;
     }
 }

@@ -48,7 +48,8 @@ struct BatchArgs {
     uint32_t n, L;
     uint32_t d, E;                // dimension, entries per plaintext
     uint32_t wpp;                 // response words per plaintext (2n or E4 + n)
-    uint32_t compact;             // WALLY_RESP_COMPACT
+    uint32_t compact;             // WALLY_RESP_COMPACT or _COMPACT_DROP (c0 at the result coefficients only)
+    uint32_t drop;                // WALLY_RESP_COMPACT_DROP (c1 rounded to 2^6, 24-bit planes)
     uint32_t nq;
     uint32_t n_local;
     uint32_t total_clusters;

@@ -49,6 +49,8 @@ class wally_params(ctypes.Structure):
 
 WALLY_RESP_FULL = 0
 WALLY_RESP_COMPACT = 1
+WALLY_RESP_COMPACT_DROP = 2
+WALLY_RESP_DROP_BITS = 6
 
 
 def _load():

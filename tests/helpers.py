@@ -54,9 +54,12 @@ def oracle_pairs(moduli, cts_host: np.ndarray, pcoefs: np.ndarray, pair_q, pair_
     return out
 
 
+DROP_BITS = 6   # WALLY_RESP_DROP_BITS
+
+
 def words_per_pt(n: int, d: int, fmt: int) -> int:
-    E = n // d
-    return (E + 3) // 4 * 4 + n if fmt == 1 else 2 * n
+    E4 = (n // d + 3) // 4 * 4
+    return {0: 2 * n, 1: E4 + n, 2: E4 + 3 * n // 4}[fmt]
 
 
 def response_of(resp: np.ndarray, off: np.ndarray, q: int, k: int, n: int, d: int = 1, fmt: int = 0) -> np.ndarray:
@@ -80,18 +83,30 @@ def matches_oracle(got: np.ndarray, want_full: np.ndarray, n: int, d: int, fmt: 
         return np.array_equal(got, want_full)
     E = n // d
     E4 = (E + 3) // 4 * 4
-    return (np.array_equal(got[:E], want_full[0][result_positions(n, d)]) and not got[E:E4].any()
-            and np.array_equal(got[E4:], want_full[1]))
+    ok = np.array_equal(got[:E], want_full[0][result_positions(n, d)]) and not got[E:E4].any()
+    if fmt == 1:
+        return ok and np.array_equal(got[E4:], want_full[1])
+    h = capi.drop_lsb(want_full[1], DROP_BITS)            # the oracle's dropped c1 (reading S20)
+    body = np.ascontiguousarray(got[E4:])
+    lo = body[: n // 2].view(np.uint16)
+    hi = body[n // 2:].view(np.uint8)
+    return ok and np.array_equal(lo, (h & 0xFFFF).astype(np.uint16)) and np.array_equal(hi, (h >> 16).astype(np.uint8))
 
 
-def expand_compact(got: np.ndarray, n: int, d: int) -> np.ndarray:
+def expand_compact(got: np.ndarray, n: int, d: int, fmt: int = 1, q0: int = 0) -> np.ndarray:
     """[2][n] ciphertext with the compact c0 words at their positions (other
-    c0 coefficients zero): decrypts correctly at the result coefficients."""
+    c0 coefficients zero) and c1 (reconstructed as 64 h mod q_0 when the LSBs
+    were dropped): decrypts correctly at the result coefficients."""
     E = n // d
     E4 = (E + 3) // 4 * 4
     full = np.zeros((2, n), np.uint32)
     full[0][result_positions(n, d)] = got[:E]
-    full[1] = got[E4:]
+    if fmt == 1:
+        full[1] = got[E4:]
+    else:
+        body = np.ascontiguousarray(got[E4:])
+        h = body[: n // 2].view(np.uint16).astype(np.uint64) | (body[n // 2:].view(np.uint8).astype(np.uint64) << 16)
+        full[1] = ((h << DROP_BITS) % q0).astype(np.uint32)
     return full
 
 

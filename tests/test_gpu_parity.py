@@ -59,7 +59,7 @@ def test_ntt_roundtrip_and_product(n, L):
 # Whole path on configs[0] (c1): every pair, real encryptions, decrypt check
 # --------------------------------------------------------------------------
 
-@pytest.mark.parametrize("fmt", [0, 1], ids=["full", "compact"])
+@pytest.mark.parametrize("fmt", [0, 1, 2], ids=["full", "compact", "compact_drop"])
 def test_c1_all_pairs_bit_exact_and_decrypts(fmt):
     w = synth.WORKLOADS["c1"]
     ents = synth.cluster_entries(w)
@@ -79,8 +79,8 @@ def test_c1_all_pairs_bit_exact_and_decrypts(fmt):
     for i, (q, k) in enumerate(zip(pq, pp)):
         got = H.response_of(resp, off, q, k, w.n, w.d, fmt)
         assert H.matches_oracle(got, want[i], w.n, w.d, fmt), (q, k)
-        if fmt == 1:
-            got = H.expand_compact(got, w.n, w.d)
+        if fmt:
+            got = H.expand_compact(got, w.n, w.d, fmt, qs[0])
         dec = capi.decrypt_q0(qs[0], w.t, got, keys[q].s)
         for j in range(E):
             assert int(dec[j * w.d + w.d - 1]) == int(np.dot(qv[q].astype(np.int64),
@@ -105,10 +105,14 @@ EDGE = [
 ]
 
 
-@pytest.mark.parametrize("fmt", [0, 1], ids=["full", "compact"])
+@pytest.mark.parametrize("fmt", [0, 1, 2], ids=["full", "compact", "compact_drop"])
 @pytest.mark.parametrize("cfg", EDGE, ids=[f"n{c['n']}_L{c['L']}_d{c['d']}" for c in EDGE])
 def test_edge_cases_bit_exact(cfg, fmt):
     n, L, d = cfg["n"], cfg["L"], cfg["d"]
+    if fmt == 2 and n > 4096:
+        with pytest.raises(WallyError):
+            WallyServer(n, L, d, resp_format=2)
+        return
     rng = np.random.default_rng(n + 7 * L + d)
     clusters = [rng.integers(-15, 16, size=(s, d)).astype(np.int8) for s in cfg["sizes"]]
     srv = H.make_server_ragged(n, L, d, clusters, resp_format=fmt)
@@ -231,8 +235,8 @@ def _sampled_full_config(name, n_pairs=384, real_queries=4, fmt=0):
         for k in (0, P - 1):
             b = int(off[q]) + k * wpp
             got = resp[b:b + wpp].cpu().numpy().view(np.uint32)
-            if fmt == 1:
-                got = H.expand_compact(got, w.n, w.d)
+            if fmt:
+                got = H.expand_compact(got, w.n, w.d, fmt, qs[0])
             dec = capi.decrypt_q0(qs[0], w.t, got, keys[i].s)
             cnt = min(E, w.cluster_size - k * E)
             for j in range(cnt):
@@ -243,7 +247,7 @@ def _sampled_full_config(name, n_pairs=384, real_queries=4, fmt=0):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("name,fmt", [("c2", 0), ("c3", 0), ("c3", 1), ("c4", 1), ("c5", 1)])
+@pytest.mark.parametrize("name,fmt", [("c2", 0), ("c3", 0), ("c3", 1), ("c3", 2), ("c4", 1), ("c5", 2)])
 def test_full_config_sampled_bit_exact(name, fmt):
     _sampled_full_config(name, fmt=fmt)
 
@@ -266,7 +270,7 @@ def test_pack_queries_kernel():
     srv.close()
 
 
-@pytest.mark.parametrize("world,fmt", [(2, 0), (3, 1)])
+@pytest.mark.parametrize("world,fmt", [(2, 0), (3, 1), (2, 2)])
 def test_sharded_ranks_bit_identical_to_single_rank(world, fmt):
     from paper_2406_06761_b200 import wally as W
     w = synth.scaled(synth.WORKLOADS["c5"], num_clusters=40, cluster_size=70, num_queries=97)

@@ -338,6 +338,56 @@ def test_decrypt_equals_dot_products_and_budget_positive(shape):
             assert int(dec[j * d + d - 1]) == want
 
 
+# --------------------------------------------------------------------------
+# Dropping ciphertext LSBs (reading S20: rounded high part)
+# --------------------------------------------------------------------------
+
+def test_drop_lsb_closed_form():
+    q0 = capi.find_primes(4096, 2)[0]
+    rng = np.random.default_rng(20)
+    c = np.concatenate([rng.integers(0, q0, size=20000), [0, 1, 31, 32, 33, 63, 64, q0 - 33, q0 - 32, q0 - 1]])
+    c = c.astype(np.uint32)
+    for b in (0, 1, 6, 9):
+        h = capi.drop_lsb(c, b).astype(np.int64)
+        low = c.astype(np.int64) - (h << b)
+        if b == 0:
+            assert np.array_equal(h, c)
+        else:
+            assert low.min() >= -(1 << (b - 1)) and low.max() < (1 << (b - 1))   # |c^l| <= 2^(b-1)
+    assert int(capi.drop_lsb(np.array([q0 - 1], np.uint32), 6)[0]) < (1 << 24)  # fits the 24-bit planes
+
+
+@pytest.mark.parametrize("shape", [s for s in SHAPES if SHAPES[s]["n"] <= 4096])
+def test_decrypt_with_dropped_lsbs_exact(shape):
+    """The paper's correctness condition ||e + e_drop|| < q_0 / 2t holds with
+    b1 = 6 dropped bits of c1 at n = 4096: every result decrypts
+    exactly and the phase noise stays below the bound with margin (budget
+    > 1 bit: the largest of n noise coefficients is ~3.5 sigma, so the bound
+    sits at > 7 sigma).  At n = 8192 the margin falls to ~0.7 bit, which is why
+    WALLY_RESP_COMPACT_DROP is limited to n <= 4096."""
+    s = SHAPES[shape]
+    n, L, d, b = s["n"], s["L"], s["d"], s["bound"]
+    qs = capi.find_primes(n, L)
+    t = 65537
+    w = synth.scaled(synth.WORKLOADS["c1"], n=n, num_limbs=L, d=d)
+    rng = np.random.default_rng(7 * n + L + d)
+    E = n // d
+    for trial in range(2):
+        ents = rng.integers(-b, b + 1, size=(E, d)).astype(np.int8)
+        pc = capi.encode_plaintext(ents, d, n)
+        qv = rng.integers(-b, b + 1, size=d).astype(np.int8)
+        km = synth.key_material(w, 100 + trial, qs)
+        ct = capi.encrypt(qs, t, synth.query_message(w, qv), km.s, km.a, km.e)
+        resp = capi.server_pair(qs, ct, pc)
+        h = capi.drop_lsb(resp[1], 6).astype(np.uint64)
+        dropped = resp.copy()
+        dropped[1] = ((h << 6) % qs[0]).astype(np.uint32)
+        assert capi.noise_budget_q0(qs[0], t, dropped, km.s) > 1.0
+        dec = capi.decrypt_q0(qs[0], t, dropped, km.s)
+        for j in range(E):
+            assert int(dec[j * d + d - 1]) == int(np.dot(qv.astype(np.int64), ents[j].astype(np.int64))) % t
+
+
 def test_fake_and_unit_queries():
     """S14: a zero (fake) query decrypts to all zeros; query e_0 returns e_j[0]."""
     n, L, d = 4096, 2, 128
