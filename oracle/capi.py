@@ -60,6 +60,8 @@ def lib():
         L.or_encrypt.argtypes = [c_u32, c_u32, u32p, c_u32, i32p, i8p, u32p, i32p, u32p]
         L.or_phase_q0.argtypes = [c_u32, c_u32, u32p, i8p, u32p]
         L.or_drop_lsb.argtypes = [u32p, c_u32, c_u32, u32p]
+        L.or_plain_crt_signed.argtypes = [c_u32, c_u32, c_u32, c_u32]
+        L.or_plain_crt_signed.restype = ctypes.c_int64
         L.or_decrypt_q0.argtypes = [c_u32, c_u32, c_u32, u32p, i8p, u32p]
         L.or_noise_budget_q0.argtypes = [c_u32, c_u32, c_u32, u32p, i8p]
         L.or_noise_budget_q0.restype = ctypes.c_double
@@ -205,6 +207,11 @@ def phase_q0(q0: int, resp, s) -> np.ndarray:
     v = np.zeros(n, dtype=np.uint32)
     lib().or_phase_q0(n, q0, _p(r, ctypes.c_uint32), _p(s, ctypes.c_int8), _p(v, ctypes.c_uint32))
     return v
+
+
+def plain_crt_signed(m0: int, m1: int, t0: int, t1: int) -> int:
+    """Centered CRT combination of a result decrypted mod t0 and mod t1 (plaintext CRT)."""
+    return int(lib().or_plain_crt_signed(int(m0), int(m1), t0, t1))
 
 
 def drop_lsb(c, b: int) -> np.ndarray:

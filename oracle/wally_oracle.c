@@ -489,6 +489,22 @@ void or_decrypt_q0(uint32_t n, uint32_t q0, uint32_t t, const uint32_t *resp, co
     free(v);
 }
 
+/* Plaintext CRT: the client encrypts
+ * the query mod t0 and mod t1 (NTT-friendly primes; the paper's 16- and
+ * 17-bit limbs) and reconstructs each result in Z_{t0 t1} by the CRT.
+ * Returns the centered representative in (-t0 t1 / 2, t0 t1 / 2]: the exact
+ * signed dot product when it does not wrap around t0 t1.
+ * m0 in [0, t0), m1 in [0, t1); t0, t1 coprime. */
+int64_t or_plain_crt_signed(uint32_t m0, uint32_t m1, uint32_t t0, uint32_t t1)
+{
+    /* x = m0 + t0 * ((m1 - m0) * t0^{-1} mod t1) */
+    uint64_t inv = or_invmod(t0 % t1, t1);   /* t1 prime */
+    uint64_t k = or_mulmod(or_submod(m1 % t1, m0 % t1, t1), inv, t1);
+    uint64_t T = (uint64_t)t0 * t1;
+    uint64_t x = (uint64_t)m0 + (uint64_t)t0 * k;   /* in [0, T) */
+    return x > T / 2 ? (int64_t)x - (int64_t)T : (int64_t)x;
+}
+
 /* Dropping ciphertext LSBs (Cheetah's method with the
  * paper's analysis: c = 2^b c^h + c^l, decryption with 2^b c^h adds
  * e_drop = -c^l (times s for c1)).  Reading S20: the high part is the

@@ -299,3 +299,50 @@ def test_sharded_ranks_bit_identical_to_single_rank(world, fmt):
         words = int(ref_off[q + 1] - ref_off[q])
         g0 = int(plan.gathered_off[q])
         assert np.array_equal(gathered[g0:g0 + words], ref[int(ref_off[q]):int(ref_off[q + 1])]), q
+
+
+# --------------------------------------------------------------------------
+# Plaintext CRT: one query = two ciphertexts (mod t0, t1)
+# tagged with the same cluster; the server path is unchanged and the chunked
+# batcher makes both share every staged plaintext
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("fmt", [0, 1])
+def test_plaintext_crt_through_cuda_path(fmt):
+    T0, T1 = 40961, 65537
+    w = synth.scaled(synth.WORKLOADS["c3"], num_clusters=2, cluster_size=300, num_queries=3)
+    ents = synth.cluster_entries(w)
+    ents[1, 0] = 15
+    srv = H.make_server(w, ents, resp_format=fmt)
+    qs = srv.moduli
+    qv = np.full((3, w.d), 15, np.int8)
+    qv[1] = -15
+    qv[2] = synth.query_vectors(w)[0]
+    cl = np.array([1, 1, 0], np.uint32)
+    cts, keys = [], []
+    for q in range(3):
+        for i, t in enumerate((T0, T1)):
+            km = synth.key_material(w, 10 * q + i, qs)
+            cts.append(capi.encrypt(qs, t, synth.query_message(w, qv[q]), km.s, km.a, km.e))
+            keys.append(km)
+    ids = np.repeat(cl, 2)
+    resp, off = H.run_batch(srv, ids, np.stack(cts))
+    E = w.n // w.d
+    P = -(-w.cluster_size // E)
+    big = 0
+    for q in range(3):
+        c = int(cl[q])
+        for k in range(P):
+            dec = []
+            for i, t in enumerate((T0, T1)):
+                got = H.response_of(resp, off, 2 * q + i, k, w.n, w.d, fmt)
+                if fmt:
+                    got = H.expand_compact(got, w.n, w.d, fmt, qs[0])
+                dec.append(capi.decrypt_q0(qs[0], t, got, keys[2 * q + i].s))
+            for j in range(min(E, w.cluster_size - k * E)):
+                want = int(np.dot(qv[q].astype(np.int64), ents[c][k * E + j].astype(np.int64)))
+                pos = j * w.d + w.d - 1
+                assert capi.plain_crt_signed(int(dec[0][pos]), int(dec[1][pos]), T0, T1) == want
+                big += abs(want) > 32768
+    assert big >= 2      # values a single t = 65537 cannot represent as signed integers
+    srv.close()

@@ -388,6 +388,58 @@ def test_decrypt_with_dropped_lsbs_exact(shape):
             assert int(dec[j * d + d - 1]) == int(np.dot(qv.astype(np.int64), ents[j].astype(np.int64))) % t
 
 
+# --------------------------------------------------------------------------
+# Plaintext CRT: t = t0 t1 with the
+# paper's 16- and 17-bit NTT-friendly limbs
+# --------------------------------------------------------------------------
+
+T0, T1 = 40961, 65537   # 5*8192+1 and 8*8192+1: primes = 1 mod 2n for n <= 4096
+
+
+def test_plaintext_crt_limbs_are_ntt_friendly_primes():
+    for t in (T0, T1):
+        assert capi.is_prime(t) and t % 8192 == 1
+    assert T0.bit_length() == 16 and T1.bit_length() == 17
+
+
+def test_plain_crt_closed_form():
+    rng = np.random.default_rng(9)
+    T = T0 * T1
+    xs = list(rng.integers(-(T // 2) + 1, T // 2, size=2000)) + [0, 1, -1, T // 2, -(T // 2) + 1, 43200, -43200]
+    for x in xs:
+        x = int(x)
+        assert capi.plain_crt_signed(x % T0, x % T1, T0, T1) == x
+
+
+def test_plaintext_crt_recovers_signed_dot_products_beyond_t():
+    """c3 shape: |<q, e>| reaches 43,200 > (65537-1)/2, so one t = 65537 only
+    gives results mod t (reading S11); two ciphertexts mod t0 and t1 give the
+    exact signed value.  The server computation is the same for both."""
+    n, L, d = 4096, 3, 192
+    qs = capi.find_primes(n, L)
+    w = synth.scaled(synth.WORKLOADS["c3"], num_queries=1)
+    rng = np.random.default_rng(33)
+    E = n // d
+    ents = rng.integers(-15, 16, size=(E, d)).astype(np.int8)
+    ents[0] = 15
+    ents[1] = -15
+    pc = capi.encode_plaintext(ents, d, n)
+    qv = np.full(d, 15, np.int8)
+    qv[-1] = -15
+    want = [int(np.dot(qv.astype(np.int64), ents[j].astype(np.int64))) for j in range(E)]
+    assert max(abs(x) for x in want) > (T1 - 1) // 2
+    dec = []
+    for i, t in enumerate((T0, T1)):
+        km = synth.key_material(w, 40 + i, qs)
+        ct = capi.encrypt(qs, t, synth.query_message(w, qv), km.s, km.a, km.e)
+        resp = capi.server_pair(qs, ct, pc)
+        assert capi.noise_budget_q0(qs[0], t, resp, km.s) > 0
+        dec.append(capi.decrypt_q0(qs[0], t, resp, km.s))
+    for j in range(E):
+        pos = j * d + d - 1
+        assert capi.plain_crt_signed(int(dec[0][pos]), int(dec[1][pos]), T0, T1) == want[j]
+
+
 def test_fake_and_unit_queries():
     """S14: a zero (fake) query decrypts to all zeros; query e_0 returns e_j[0]."""
     n, L, d = 4096, 2, 128
