@@ -64,7 +64,7 @@ def parse():
     ap.add_argument("--quiet", action="store_true")
     ap.add_argument("--resp", default="auto", choices=["auto", "compact_drop", "compact", "full"],
                     help="response format (SURVEY 8(f)-1): compact = c0 only at the E result coefficients + c1; "
-                         "compact_drop = compact with c1's 6 LSBs dropped (24-bit, n <= 4096); auto = compact_drop "
+                         "compact_drop = compact with c1's 6 LSBs dropped (24-bit, n = 4096); auto = compact_drop "
                          "where allowed, else compact")
     ap.add_argument("--queries", type=int, default=0,
                     help="profiling only: evaluate just the first Q queries of the batch (not a bench line)")
@@ -241,7 +241,7 @@ def run_wally(args, rank, world, local_rank):
     # cluster ownership (N > 1): greedy LPT on expected work = prior query share x P_c
     owner = W.wally_assign_owners(synth.cluster_popularity(w) * P, world) if world > 1 else None
     if args.resp == "auto":
-        args.resp = "compact_drop" if w.n <= 4096 else "compact"
+        args.resp = "compact_drop" if w.n == 4096 else "compact"
     fmt = {"full": W.WALLY_RESP_FULL, "compact": W.WALLY_RESP_COMPACT,
            "compact_drop": W.WALLY_RESP_COMPACT_DROP}[args.resp]
     srv = WallyServer(w.n, w.num_limbs, w.d, w.t, device=local_rank, resp_format=fmt)

@@ -79,18 +79,19 @@ typedef struct wally_ctx wally_ctx;
  *                       P:L1035 ("sparse c0"). */
 #define WALLY_RESP_FULL 0u
 #define WALLY_RESP_COMPACT 1u
-/*   WALLY_RESP_COMPACT_DROP  as WALLY_RESP_COMPACT, and c1' additionally has
- *                       its 6 least significant bits dropped ("Dropping
- *                       ciphertext LSBs", reading S20: rounded,
- *                       h = floor((c1' + 32) / 64) < 2^24 because q_0 < 2^30 - 31)
- *                       and stored as two planes: the low 16 bits of h as
- *                       uint16 [n], then the high 8 bits as uint8 [n]
- *                       (E4 + 3n/4 words).  The client decrypts with
- *                       c1' ~ 64 h mod q_0; the dropped part adds
- *                       e_drop = -(c1' - 64 h) * s, |c1' - 64 h| <= 32, which keeps
- *                       ||e + e_drop|| < q_0 / 2t for q_0 ~ 2^30, t = 65537,
- *                       n <= 4096; wally_create
- *                       rejects it for n = 8192, where the margin is too thin. */
+/*   WALLY_RESP_COMPACT_DROP  (n = 4096 only) as WALLY_RESP_COMPACT, and c1'
+ *                       additionally has its 6 least significant bits dropped
+ *                       ("Dropping ciphertext LSBs"; reading S20:
+ *                       rounded, h = floor((c1' + 32) / 64) < 2^24 because
+ *                       q_0 < 2^30 - 31), stored as two planes: the low 16 bits
+ *                       of h as uint16 [n], then the high 8 bits as uint8 [n],
+ *                       both in the 16 x 256 transposed order -- coefficient i
+ *                       at position (i mod 256) * 16 + floor(i / 256) -- which
+ *                       is the order the kernel holds them in (E4 + 3n/4 words).
+ *                       The client decrypts with c1' ~ 64 h mod q_0; the dropped
+ *                       part adds e_drop = -(c1' - 64 h) * s with |c1' - 64 h| <= 32,
+ *                       which keeps ||e + e_drop|| < q_0 / 2t for q_0 ~ 2^30,
+ *                       t <= 65537 at n = 4096. */
 #define WALLY_RESP_COMPACT_DROP 2u
 #define WALLY_RESP_DROP_BITS 6u
 

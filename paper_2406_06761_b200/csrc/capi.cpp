@@ -244,9 +244,9 @@ extern "C" int wally_create(const wally_params *pp, int device, wally_ctx **out)
     if (p.t < 2) return fail(nullptr, WALLY_E_PARAMS, "t=%u must be >= 2", p.t);
     if (!valid_resp_format(p.resp_format))
         return fail(nullptr, WALLY_E_PARAMS, "resp_format=%u unknown", p.resp_format);
-    if (p.resp_format == WALLY_RESP_COMPACT_DROP && p.n > 4096)
+    if (p.resp_format == WALLY_RESP_COMPACT_DROP && p.n != 4096)
         return fail(nullptr, WALLY_E_PARAMS,
-                    "WALLY_RESP_COMPACT_DROP is specified for n <= 4096 (its noise bound; DESIGN.md)");
+                    "WALLY_RESP_COMPACT_DROP is specified for n = 4096 (its noise bound and plane order; DESIGN.md)");
     for (uint32_t i = 0; i < p.num_limbs; i++) {
         uint32_t q = p.moduli[i];
         if (q >= (1u << 30) || q % (2 * p.n) != 1 || !is_prime32(q))

@@ -404,34 +404,47 @@ __device__ __forceinline__ void write_results(uint32_t *dst, const uint32_t (&a)
 // Write one ciphertext component of a pair's response in the context's
 // format (include/wally.h "Response formats"); a = the component's values
 // in the pass-2 layout, canonical mod q_0.
-template <int N>
+// FMT = WALLY_RESP_* when known at compile time (the v4 kernel is
+// instantiated per format), -1 = read it from ba at run time.
+template <int N, int FMT = -1>
 __device__ __forceinline__ void write_component(const BatchArgs &ba, uint32_t *out_q, const uint32_t (&a)[NttGeom<N>::V],
                                                 int comp, int g, const uint32_t *s_rmap) {
     using Gm = NttGeom<N>;
     constexpr int V = Gm::V;
-    if (ba.compact && comp == 0) {
+    const bool compact = (FMT < 0) ? (bool)ba.compact : (FMT != (int)WALLY_RESP_FULL);
+    const bool drop = (FMT < 0) ? (bool)ba.drop : (FMT == (int)WALLY_RESP_COMPACT_DROP);
+    if (compact && comp == 0) {
         write_results<N>(out_q, a, s_rmap, g, result_map_dj(Gm::TB2, ba.d));
         const uint32_t e4 = (ba.E + 3) & ~3u;
         if ((uint32_t)g < e4 - ba.E) __stcs(out_q + ba.E + g, 0u);  // zero padding to E4
         return;
     }
-    if (ba.drop) {
-        // c1 with its 6 LSBs dropped (rounded), 24-bit planes: lo16 [N], hi8 [N]
-        uint32_t *base = out_q + ((ba.E + 3) & ~3u);
-        unsigned short *lo = reinterpret_cast<unsigned short *>(base);
-        unsigned char *hi = reinterpret_cast<unsigned char *>(base + N / 2);
+    if constexpr (N == 4096 && (FMT < 0 || FMT == (int)WALLY_RESP_COMPACT_DROP)) {
+        if (drop) {
+            // c1 with its 6 LSBs dropped (rounded), 24-bit planes lo16 [N] and hi8 [N]
+            // in the 16 x 256 transposed order (include/wally.h): this thread's
+            // coefficients k*256 + g sit at positions g*16 + k, so it writes its 16
+            // values as two 16-byte stores (lo) and one (hi) instead of 32 scalar ones
+            static_assert(Gm::TB2 == 256 && Gm::R2 == 16 && V == 16, "transposed planes assume n = 4096 geometry");
+            uint32_t *base = out_q + ((ba.E + 3) & ~3u);
+            uint32_t h[16];
 #pragma unroll
-        for (int j = 0; j < V / Gm::R2; j++)
+            for (int k = 0; k < 16; k++) h[k] = (a[k] + (1u << (WALLY_RESP_DROP_BITS - 1))) >> WALLY_RESP_DROP_BITS;
+            uint4 *lo = reinterpret_cast<uint4 *>(base) + 2 * g;
+            __stcs(lo, make_uint4(__byte_perm(h[0], h[1], 0x5410), __byte_perm(h[2], h[3], 0x5410),
+                                  __byte_perm(h[4], h[5], 0x5410), __byte_perm(h[6], h[7], 0x5410)));
+            __stcs(lo + 1, make_uint4(__byte_perm(h[8], h[9], 0x5410), __byte_perm(h[10], h[11], 0x5410),
+                                      __byte_perm(h[12], h[13], 0x5410), __byte_perm(h[14], h[15], 0x5410)));
+            uint32_t hw[4];
 #pragma unroll
-            for (int kk = 0; kk < Gm::R2; kk++) {
-                const uint32_t pos = pass_index<N, Gm::TB2, Gm::R2>(g, j, kk);
-                const uint32_t h = (a[j * Gm::R2 + kk] + (1u << (WALLY_RESP_DROP_BITS - 1))) >> WALLY_RESP_DROP_BITS;
-                __stcs(lo + pos, (unsigned short)(h & 0xffffu));
-                __stcs(hi + pos, (unsigned char)(h >> 16));
-            }
-        return;
+            for (int i = 0; i < 4; i++)
+                hw[i] = __byte_perm(__byte_perm(h[4 * i], h[4 * i + 1], 0x0062), __byte_perm(h[4 * i + 2], h[4 * i + 3], 0x0062),
+                                    0x5410);
+            __stcs(reinterpret_cast<uint4 *>(base + N / 2) + g, make_uint4(hw[0], hw[1], hw[2], hw[3]));
+            return;
+        }
     }
-    uint32_t *dst = out_q + (ba.compact ? (size_t)(ba.wpp - N) : (size_t)comp * N);
+    uint32_t *dst = out_q + (compact ? (size_t)(ba.wpp - N) : (size_t)comp * N);
 #pragma unroll
     for (int j = 0; j < V / Gm::R2; j++)
 #pragma unroll
@@ -652,9 +665,10 @@ struct LimbLoopTM {
     }
 };
 
-template <int N, int L>
+template <int N, int L, int FMT>
 __device__ __forceinline__ void eval_item_tm(const BatchArgs &ba, const ItemCursor &cur, uint32_t item, int g,
-                                             const ChainCtx &cx, const uint32_t *s_rmap, uint32_t tcol) {
+                                             const ChainCtx &cx, const uint32_t *s_rmap, uint32_t tcol,
+                                             const volatile uint32_t *s_next, ItemCursor &ncur) {
     using Gm = NttGeom<N>;
     constexpr int V = Gm::V, NC = 2;
     const uint32_t li = cur.li;
@@ -699,13 +713,35 @@ __device__ __forceinline__ void eval_item_tm(const BatchArgs &ba, const ItemCurs
         const uint32_t *chat_next = (qn != 0xffffffffu) ? ba.chat + (size_t)qn * 2 * L * N : nullptr;
         EvalState<N, L, NC> st;
         LimbLoopTM<N, L, L - 1>::run(st, cpre, ba, chat_q, chat_next, tcol, g, cx);
+#ifndef WALLY_NO_L2_PREFETCH
+        if (qi == qb) {
+#else
+        if (false) {
+#endif
+            // the group's next work item was published before this item started
+            // (and the limb loop passed group barriers): pull this thread's slice of
+            // its plaintext toward L2 now -- each plaintext is read by one item only,
+            // so its first touch is an HBM miss the item start would otherwise wait on
+            const uint32_t nitem = *s_next;
+            if (nitem < ba.misc[kMiscTotalItems]) {
+                ncur.seek(ba, nitem);
+                const uint32_t nli = ncur.li;
+                const uint32_t nk = (nitem - ncur.b) % ba.n_pt[nli];
+                const uint32_t *np = ba.store + (size_t)(ba.pt_base[nli] + nk) * L * 2 * N + (size_t)g * V;
 #pragma unroll
-        for (int c = 0; c < NC; c++) write_component<N>(ba, out_q, st.a[c], c, g, s_rmap);
+                for (int J = 0; J < L; J++) {
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(np + (size_t)J * 2 * N));
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(np + (size_t)J * 2 * N + N));
+                }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < NC; c++) write_component<N, FMT>(ba, out_q, st.a[c], c, g, s_rmap);
         qo = qn;
     }
 }
 
-template <int N, int L>
+template <int N, int L, int FMT>
 __global__ void __launch_bounds__(kEvalGroups * NttGeom<N>::T, 1) eval_kernel_tm(BatchArgs ba) {
     using Gm = NttGeom<N>;
     constexpr int NC = 2;
@@ -727,7 +763,7 @@ __global__ void __launch_bounds__(kEvalGroups * NttGeom<N>::T, 1) eval_kernel_tm
         const uint4 *src = reinterpret_cast<const uint4 *>(ba.tw_inv);
         for (int i = threadIdx.x; i < L * Gm::TW_LIMB / 2; i += blockDim.x) smem4[i] = __ldg(src + i);
     }
-    if (ba.compact) build_result_map<N>(s_rmap, ba.d);
+    if (FMT != (int)WALLY_RESP_FULL) build_result_map<N>(s_rmap, ba.d);
     if (g == 0) s_item[grp][0] = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -735,15 +771,15 @@ __global__ void __launch_bounds__(kEvalGroups * NttGeom<N>::T, 1) eval_kernel_tm
     const uint32_t tcol = s_taddr + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 128);
     const ChainCtx cx{tw, xbuf + grp * NC * Gm::SMEM_WORDS, nullptr, 1 + grp};
     const uint32_t total = ba.misc[kMiscTotalItems];
-    ItemCursor cur;
+    ItemCursor cur, ncur;
     for (uint32_t it = 0;; it++) {
         const uint32_t item = s_item[grp][it & 1];
         if (item >= total) break;
-        uint32_t next = 0;
-        if (g == 0) next = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
+        // slot (it+1)&1 was last read at the start of iteration it-1 (group barrier since)
+        if (g == 0) s_item[grp][(it + 1) & 1] = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
         cur.seek(ba, item);
-        eval_item_tm<N, L>(ba, cur, item, g, cx, s_rmap, tcol);
-        if (g == 0) s_item[grp][(it + 1) & 1] = next;
+        eval_item_tm<N, L, FMT>(ba, cur, item, g, cx, s_rmap, tcol, &s_item[grp][(it + 1) & 1], ncur);
+        cur = ncur;
         group_sync(1 + grp, T);
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -828,6 +864,22 @@ cudaError_t launch_ntt_inverse(const KParams &kp, uint32_t n, uint32_t L, const 
     return cudaErrorInvalidValue;
 }
 
+template <int N, int L, int FMT>
+static cudaError_t launch_eval_tm(const BatchArgs &a, cudaStream_t s, int num_sms) {
+    using Gm = NttGeom<N>;
+    static bool configured = false;
+    const size_t smem = (size_t)L * Gm::TW_LIMB * sizeof(uint2) +
+                        (size_t)kEvalGroups * 2 * Gm::SMEM_WORDS * sizeof(uint32_t);
+    if (!configured) {
+        cudaError_t e = allow_smem(eval_kernel_tm<N, L, FMT>, smem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    // one CTA per SM: it owns all 512 TMEM columns of its SM
+    eval_kernel_tm<N, L, FMT><<<num_sms, kEvalGroups * Gm::T, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
 template <int N, int L>
 static cudaError_t launch_eval_nl(const BatchArgs &a, cudaStream_t s, int num_sms) {
     using Gm = NttGeom<N>;
@@ -837,15 +889,9 @@ static cudaError_t launch_eval_nl(const BatchArgs &a, cudaStream_t s, int num_sm
 #define WALLY_EVAL_TMEM 1
 #endif
     if constexpr (N == 4096 && L >= 2 && L <= 3 && WALLY_EVAL_TMEM) {
-        const size_t smem = (size_t)L * Gm::TW_LIMB * sizeof(uint2) +
-                            (size_t)kEvalGroups * 2 * Gm::SMEM_WORDS * sizeof(uint32_t);
-        if (!configured) {
-            cudaError_t e = allow_smem(eval_kernel_tm<N, L>, smem);
-            if (e != cudaSuccess) return e;
-            blocks_per_sm = 1;  // one CTA owns all 512 TMEM columns of its SM
-            configured = true;
-        }
-        eval_kernel_tm<N, L><<<num_sms * blocks_per_sm, kEvalGroups * Gm::T, smem, s>>>(a);
+        if (a.drop) return launch_eval_tm<N, L, (int)WALLY_RESP_COMPACT_DROP>(a, s, num_sms);
+        if (a.compact) return launch_eval_tm<N, L, (int)WALLY_RESP_COMPACT>(a, s, num_sms);
+        return launch_eval_tm<N, L, (int)WALLY_RESP_FULL>(a, s, num_sms);
     } else if constexpr (N <= 4096) {
         const size_t smem = (size_t)L * Gm::TW_LIMB * sizeof(uint2) +
                             (size_t)kEvalGroups * EvalCfg<N>::NC * Gm::SMEM_WORDS * sizeof(uint32_t);

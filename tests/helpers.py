@@ -88,9 +88,15 @@ def matches_oracle(got: np.ndarray, want_full: np.ndarray, n: int, d: int, fmt: 
         return ok and np.array_equal(got[E4:], want_full[1])
     h = capi.drop_lsb(want_full[1], DROP_BITS)            # the oracle's dropped c1 (reading S20)
     body = np.ascontiguousarray(got[E4:])
-    lo = body[: n // 2].view(np.uint16)
-    hi = body[n // 2:].view(np.uint8)
+    lo = body[: n // 2].view(np.uint16)[drop_plane_position(n)]
+    hi = body[n // 2:].view(np.uint8)[drop_plane_position(n)]
     return ok and np.array_equal(lo, (h & 0xFFFF).astype(np.uint16)) and np.array_equal(hi, (h >> 16).astype(np.uint8))
+
+
+def drop_plane_position(n: int) -> np.ndarray:
+    """Plane position of coefficient i in WALLY_RESP_COMPACT_DROP (n = 4096): 16 x 256 transpose."""
+    i = np.arange(n)
+    return (i % 256) * 16 + i // 256
 
 
 def expand_compact(got: np.ndarray, n: int, d: int, fmt: int = 1, q0: int = 0) -> np.ndarray:
@@ -105,7 +111,9 @@ def expand_compact(got: np.ndarray, n: int, d: int, fmt: int = 1, q0: int = 0) -
         full[1] = got[E4:]
     else:
         body = np.ascontiguousarray(got[E4:])
-        h = body[: n // 2].view(np.uint16).astype(np.uint64) | (body[n // 2:].view(np.uint8).astype(np.uint64) << 16)
+        pos = drop_plane_position(n)
+        h = (body[: n // 2].view(np.uint16)[pos].astype(np.uint64)
+             | (body[n // 2:].view(np.uint8)[pos].astype(np.uint64) << 16))
         full[1] = ((h << DROP_BITS) % q0).astype(np.uint32)
     return full
 
