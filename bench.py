@@ -238,8 +238,9 @@ def run_wally(args, rank, world, local_rank):
     E = w.n // w.d
     P = -(-w.cluster_size // E)
     from paper_2406_06761_b200 import wally as W
-    # cluster ownership (N > 1): greedy LPT on expected work = prior query share x P_c
-    owner = W.wally_assign_owners(synth.cluster_popularity(w) * P, world) if world > 1 else None
+    # cluster ownership (N > 1): greedy LPT on expected work = prior query share x P_c, with
+    # clusters heavier than the mean rank load replicated (profiles/r01_balance.txt)
+    owner = W.wally_assign_owners_replicated(synth.cluster_popularity(w) * P, world) if world > 1 else None
     if args.resp == "auto":
         args.resp = "compact_drop" if w.n == 4096 else "compact"
     fmt = {"full": W.WALLY_RESP_FULL, "compact": W.WALLY_RESP_COMPACT,
@@ -382,8 +383,9 @@ def run_wally(args, rank, world, local_rank):
                       "queries": int(tot_nq), "pairs_per_step": int(tot_pairs), "dots_per_step": int(tot_dots),
                       "response_format": f"{args.resp} ({srv.words_per_plaintext} words per plaintext; "
                                          "include/wally.h WALLY_RESP_*)",
-                      "ownership": ("greedy LPT on expected work (wally_assign_owners); queries resident on "
-                                    "rank 0, scattered by NCCL P2P inside every step") if world > 1 else "single rank",
+                      "ownership": ("greedy LPT on expected work with hot-cluster replication "
+                                    "(wally_assign_owners_replicated); queries resident on rank 0, scattered by "
+                                    "NCCL P2P inside every step") if world > 1 else "single rank",
                       "l2": "inputs larger than L2 (plaintext store, query NTTs and responses >> 126 MB)"},
            "roofline": roofline,
            "stages_ms_per_step": {"batcher": round(st_batcher / max(nb, 1), 4),

@@ -246,6 +246,34 @@ int wally_route_plan(uint32_t nq, const uint32_t *cluster_of_query_host, uint32_
                      uint32_t resp_format, uint32_t world, uint32_t *counts_out, uint32_t *order_out, uint64_t *resp_words_out,
                      uint64_t *gathered_off_out);
 
+/* Hot-cluster replication (the Zipf skew of configs[4]
+ * puts 15% of all queries on one cluster, so disjoint ownership caps the
+ * 8-rank speedup near 6.6x).  A cluster whose weight exceeds the mean rank
+ * load W/world is split into r = ceil(weight * world / W) equal pieces
+ * (r <= world) placed on r distinct ranks; all pieces are then assigned by
+ * greedy LPT as in wally_assign_owners (descending piece weight, ties by
+ * ascending cluster id; least-loaded rank that does not yet hold the
+ * cluster, ties lowest rank).  Pure host computation.
+ *   weight_host     double [total_clusters] >= 0
+ *   world           1..64
+ *   owner_mask_out  uint64 [total_clusters] out: bit r set = rank r holds a replica */
+int wally_assign_owners_replicated(uint32_t total_clusters, const double *weight_host, uint32_t world,
+                                   uint64_t *owner_mask_out);
+
+/* wally_route_plan for replicated ownership: the j-th query (input order)
+ * naming cluster c goes to the (j mod r_c)-th lowest rank in owner_mask[c]
+ * (r_c = replicas of c).  Outputs as wally_route_plan.  Errors also when a
+ * mask is empty or names a rank >= world. */
+int wally_route_plan_replicated(uint32_t nq, const uint32_t *cluster_of_query_host, uint32_t total_clusters,
+                                const uint32_t *cluster_sizes_host, const uint64_t *owner_mask_host, uint32_t n,
+                                uint32_t d, uint32_t resp_format, uint32_t world, uint32_t *counts_out,
+                                uint32_t *order_out, uint64_t *resp_words_out, uint64_t *gathered_off_out);
+
+/* wally_load_clusters with replicated ownership: cluster c is local to this
+ * context iff bit `rank` of owner_mask_host[c] is set (rank in [0, 64)). */
+int wally_load_clusters_replicated(wally_ctx *ctx, uint32_t total_clusters, const uint32_t *cluster_sizes_host,
+                                   const uint64_t *owner_mask_host, int32_t rank);
+
 /* Scatter-side packing on the ingress rank: out_dev[i] = query_ct_dev[index_dev[i]]
  * for i < count, rows of 2*L*n uint32 (one query ciphertext).  Stream-ordered.
  *   index_dev     uint32 [count] (device), each < nq

@@ -8,6 +8,7 @@
 // queries by cluster).
 
 #include <algorithm>
+#include <cmath>
 #include <array>
 #include <cstdarg>
 #include <cstdio>
@@ -333,9 +334,9 @@ static int upload(wally_ctx *c, T **dst, const std::vector<T> &v) {
     return WALLY_OK;
 }
 
-extern "C" int wally_load_clusters(wally_ctx *c, uint32_t total_clusters, const uint32_t *sizes,
-                                   const int32_t *owner, int32_t rank) {
-    if (!c) return WALLY_E_ARG;
+template <typename IsLocal>
+static int load_clusters_impl(wally_ctx *c, uint32_t total_clusters, const uint32_t *sizes, IsLocal is_local,
+                              std::vector<int32_t> owner, int32_t rank) {
     if (!sizes || total_clusters == 0) return fail(c, WALLY_E_ARG, "load_clusters: need >= 1 cluster and sizes");
     std::vector<int32_t> local(total_clusters, -1);
     std::vector<uint32_t> pt_base, n_pt, pt_li, pt_k, size;
@@ -344,7 +345,7 @@ extern "C" int wally_load_clusters(wally_ctx *c, uint32_t total_clusters, const 
     uint32_t npt = 0, max_pt = 0;
     for (uint32_t cl = 0; cl < total_clusters; cl++) {
         if (sizes[cl] == 0) return fail(c, WALLY_E_ARG, "cluster %u is empty", cl);
-        if (owner && owner[cl] != rank) continue;
+        if (!is_local(cl)) continue;
         const uint32_t li = (uint32_t)pt_base.size();
         const uint32_t P = (sizes[cl] + c->E - 1) / c->E;
         local[cl] = (int32_t)li;
@@ -370,13 +371,33 @@ extern "C" int wally_load_clusters(wally_ctx *c, uint32_t total_clusters, const 
     c->npt = npt;
     c->max_pt = max_pt;
     c->local_of_cluster = std::move(local);
-    c->owner = owner ? std::vector<int32_t>(owner, owner + total_clusters) : std::vector<int32_t>();
+    c->owner = std::move(owner);
     c->rank = rank;
     c->pt_of_local = std::move(n_pt);
     c->local_entries = entries;
     c->store = nullptr;
     c->loaded = true;
     return WALLY_OK;
+}
+
+extern "C" int wally_load_clusters(wally_ctx *c, uint32_t total_clusters, const uint32_t *sizes,
+                                   const int32_t *owner, int32_t rank) {
+    if (!c) return WALLY_E_ARG;
+    return load_clusters_impl(
+        c, total_clusters, sizes, [&](uint32_t cl) { return !owner || owner[cl] == rank; },
+        owner && sizes ? std::vector<int32_t>(owner, owner + total_clusters) : std::vector<int32_t>(), rank);
+}
+
+extern "C" int wally_load_clusters_replicated(wally_ctx *c, uint32_t total_clusters, const uint32_t *sizes,
+                                              const uint64_t *mask, int32_t rank) {
+    if (!c) return WALLY_E_ARG;
+    if (!mask || rank < 0 || rank >= 64) return fail(c, WALLY_E_ARG, "load_clusters_replicated: bad mask or rank");
+    // owner[] (wally_route_queries) reports the lowest replica of each cluster
+    std::vector<int32_t> owner(total_clusters, -1);
+    for (uint32_t cl = 0; cl < total_clusters && sizes; cl++)
+        if (mask[cl]) owner[cl] = __builtin_ctzll(mask[cl]);
+    return load_clusters_impl(
+        c, total_clusters, sizes, [&](uint32_t cl) { return (mask[cl] >> rank) & 1ull; }, std::move(owner), rank);
 }
 
 extern "C" int wally_response_words_per_plaintext(const wally_ctx *c, uint64_t *words) {
@@ -744,10 +765,42 @@ extern "C" int wally_assign_owners(uint32_t total_clusters, const double *weight
     return WALLY_OK;
 }
 
+// Plan from a per-query destination rank (shared by both routing modes).
+static int route_plan_dest(uint32_t nq, const uint32_t *ids, uint32_t total_clusters, const uint32_t *sizes,
+                           const int32_t *dest, uint32_t n, uint32_t d, uint32_t resp_format, uint32_t world,
+                           uint32_t *counts, uint32_t *order, uint64_t *resp_words, uint64_t *gathered_off) {
+    const uint64_t E = n / d, per_pt = resp_words_per_pt(n, d, resp_format);
+    std::vector<uint32_t> cnt(world, 0), start(world, 0);
+    std::vector<uint64_t> words(world, 0);
+    for (uint32_t q = 0; q < nq; q++) {
+        const uint32_t r = (uint32_t)dest[q];
+        cnt[r]++;
+        words[r] += per_pt * ((sizes[ids[q]] + E - 1) / E);
+    }
+    for (uint32_t r = 1; r < world; r++) start[r] = start[r - 1] + cnt[r - 1];
+    std::vector<uint64_t> base(world, 0);
+    for (uint32_t r = 1; r < world; r++) base[r] = base[r - 1] + words[r - 1];
+    std::vector<uint32_t> fill(start);
+    std::vector<uint64_t> wfill(base);
+    for (uint32_t q = 0; q < nq; q++) {
+        const uint32_t r = (uint32_t)dest[q];
+        order[fill[r]++] = q;
+        if (gathered_off) {
+            gathered_off[q] = wfill[r];
+            wfill[r] += per_pt * ((sizes[ids[q]] + E - 1) / E);
+        }
+    }
+    if (gathered_off) gathered_off[nq] = base[world - 1] + words[world - 1];
+    for (uint32_t r = 0; r < world; r++) {
+        counts[r] = cnt[r];
+        resp_words[r] = words[r];
+    }
+    return WALLY_OK;
+}
+
 extern "C" int wally_route_plan(uint32_t nq, const uint32_t *ids, uint32_t total_clusters, const uint32_t *sizes,
                                 const int32_t *owner, uint32_t n, uint32_t d, uint32_t resp_format, uint32_t world,
-                                uint32_t *counts,
-                                uint32_t *order, uint64_t *resp_words, uint64_t *gathered_off) {
+                                uint32_t *counts, uint32_t *order, uint64_t *resp_words, uint64_t *gathered_off) {
     if ((nq && (!ids || !order)) || !sizes || !counts || !resp_words || total_clusters == 0 || world == 0 ||
         n == 0 || d == 0 || d > n || !valid_resp_format(resp_format))
         return fail(nullptr, WALLY_E_ARG, "route_plan: bad arguments");
@@ -760,33 +813,75 @@ extern "C" int wally_route_plan(uint32_t nq, const uint32_t *ids, uint32_t total
         if (ids[q] >= total_clusters)
             return fail(nullptr, WALLY_E_UNKNOWN_CLUSTER, "route_plan: query %u names cluster %u >= %u", q, ids[q],
                         total_clusters);
-    const uint64_t E = n / d, per_pt = resp_words_per_pt(n, d, resp_format);
-    std::vector<uint32_t> cnt(world, 0), start(world, 0);
-    std::vector<uint64_t> words(world, 0);
-    for (uint32_t q = 0; q < nq; q++) {
-        const uint32_t r = owner ? (uint32_t)owner[ids[q]] : 0;
-        cnt[r]++;
-        words[r] += per_pt * ((sizes[ids[q]] + E - 1) / E);
+    std::vector<int32_t> dest(nq);
+    for (uint32_t q = 0; q < nq; q++) dest[q] = owner ? owner[ids[q]] : 0;
+    return route_plan_dest(nq, ids, total_clusters, sizes, dest.data(), n, d, resp_format, world, counts, order,
+                           resp_words, gathered_off);
+}
+
+extern "C" int wally_assign_owners_replicated(uint32_t total_clusters, const double *weight, uint32_t world,
+                                              uint64_t *mask) {
+    if (!weight || !mask || total_clusters == 0 || world == 0 || world > 64)
+        return fail(nullptr, WALLY_E_ARG, "assign_owners_replicated: bad arguments (world 1..64)");
+    double W = 0.0;
+    for (uint32_t c = 0; c < total_clusters; c++) {
+        if (!(weight[c] >= 0.0)) return fail(nullptr, WALLY_E_ARG, "assign_owners_replicated: weight[%u] < 0", c);
+        W += weight[c];
     }
-    for (uint32_t r = 1; r < world; r++) start[r] = start[r - 1] + cnt[r - 1];
-    std::vector<uint64_t> base(world, 0);
-    for (uint32_t r = 1; r < world; r++) base[r] = base[r - 1] + words[r - 1];
-    std::vector<uint32_t> fill(start);
-    std::vector<uint64_t> wfill(base);
-    for (uint32_t q = 0; q < nq; q++) {
-        const uint32_t r = owner ? (uint32_t)owner[ids[q]] : 0;
-        order[fill[r]++] = q;
-        if (gathered_off) {
-            gathered_off[q] = wfill[r];
-            wfill[r] += per_pt * ((sizes[ids[q]] + E - 1) / E);
+    struct Piece { double w; uint32_t c; };
+    std::vector<Piece> pieces;
+    pieces.reserve(total_clusters);
+    const double target = W / world;
+    for (uint32_t c = 0; c < total_clusters; c++) {
+        uint32_t r = 1;
+        if (target > 0.0 && weight[c] > target) r = (uint32_t)std::min<double>(world, std::ceil(weight[c] / target));
+        for (uint32_t i = 0; i < r; i++) pieces.push_back({weight[c] / r, c});
+    }
+    std::stable_sort(pieces.begin(), pieces.end(), [](const Piece &a, const Piece &b) { return a.w > b.w; });
+    std::vector<double> load(world, 0.0);
+    for (uint32_t c = 0; c < total_clusters; c++) mask[c] = 0;
+    for (const Piece &p : pieces) {
+        int best = -1;
+        for (uint32_t r = 0; r < world; r++) {
+            if ((mask[p.c] >> r) & 1ull) continue;
+            if (best < 0 || load[r] < load[(uint32_t)best]) best = (int)r;
         }
-    }
-    if (gathered_off) gathered_off[nq] = world ? base[world - 1] + words[world - 1] : 0;
-    for (uint32_t r = 0; r < world; r++) {
-        counts[r] = cnt[r];
-        resp_words[r] = words[r];
+        mask[p.c] |= 1ull << best;
+        load[(uint32_t)best] += p.w;
     }
     return WALLY_OK;
+}
+
+extern "C" int wally_route_plan_replicated(uint32_t nq, const uint32_t *ids, uint32_t total_clusters,
+                                           const uint32_t *sizes, const uint64_t *mask, uint32_t n, uint32_t d,
+                                           uint32_t resp_format, uint32_t world, uint32_t *counts, uint32_t *order,
+                                           uint64_t *resp_words, uint64_t *gathered_off) {
+    if (!mask || world == 0 || world > 64 || (nq && (!ids || !order)) || !sizes || !counts || !resp_words ||
+        total_clusters == 0 || n == 0 || d == 0 || d > n || !valid_resp_format(resp_format))
+        return fail(nullptr, WALLY_E_ARG, "route_plan_replicated: bad arguments (world 1..64)");
+    for (uint32_t c = 0; c < total_clusters; c++)
+        if (sizes[c] == 0) return fail(nullptr, WALLY_E_ARG, "route_plan_replicated: cluster %u is empty", c);
+    for (uint32_t c = 0; c < total_clusters; c++)
+        if (mask[c] == 0 || (world < 64 && (mask[c] >> world)))
+            return fail(nullptr, WALLY_E_ARG, "route_plan_replicated: mask[%u] empty or names a rank >= %u", c, world);
+    for (uint32_t q = 0; q < nq; q++)
+        if (ids && ids[q] >= total_clusters)
+            return fail(nullptr, WALLY_E_UNKNOWN_CLUSTER, "route_plan: query %u names cluster %u >= %u", q, ids[q],
+                        total_clusters);
+    // destination of every query: the (j mod r_c)-th replica of its cluster
+    std::vector<int32_t> dest(nq);
+    std::vector<uint32_t> seen(total_clusters, 0);
+    for (uint32_t q = 0; q < nq && ids; q++) {
+        const uint32_t c = ids[q];
+        const uint64_t m = mask[c];
+        const uint32_t r = (uint32_t)__builtin_popcountll(m);
+        uint32_t pick = seen[c]++ % r;
+        uint64_t mm = m;
+        while (pick--) mm &= mm - 1;
+        dest[q] = __builtin_ctzll(mm);
+    }
+    return route_plan_dest(nq, ids, total_clusters, sizes, dest.data(), n, d, resp_format, world, counts, order,
+                           resp_words, gathered_off);
 }
 
 extern "C" int wally_pack_queries(wally_ctx *c, uint32_t count, const uint32_t *index_dev, const uint32_t *query_dev,

@@ -6,7 +6,10 @@ rank, with NCCL over NVLink only for query scatter and response gather."
 (SURVEY.md §8(a) row a7, §8(e).)  Alg 4's per-query work is
 independent across queries and plaintexts, so nothing else is exchanged.
 
-  * ownership  : wally_assign_owners (C ABI) -- greedy LPT on expected work
+  * ownership  : wally_assign_owners (C ABI) -- greedy LPT on expected work,
+                 or wally_assign_owners_replicated: clusters heavier than
+                 the mean rank load are split over several ranks (SURVEY
+                 §8(f)-4, the Zipf skew of configs[4])
   * routing    : wally_route_plan (C ABI) -- identical on every rank, so only
                  the ciphertexts move; the ingress broadcasts the cluster ids
   * scatter    : the ingress packs each rank's share contiguously with the
@@ -43,7 +46,13 @@ class Router:
         self.world = dist.get_world_size(group)
         self.src = src
         self.sizes = np.ascontiguousarray(cluster_sizes, dtype=np.uint32)
-        self.owner = None if owner is None else np.ascontiguousarray(owner, dtype=np.int32)
+        # int32 owning rank per cluster, or uint64 replica masks (hot-cluster replication)
+        if owner is None:
+            self.owner = None
+        elif np.asarray(owner).dtype == np.uint64:
+            self.owner = np.ascontiguousarray(owner, dtype=np.uint64)
+        else:
+            self.owner = np.ascontiguousarray(owner, dtype=np.int32)
         self.n, self.d, self.L = n, d, L
         if resp_format is None:
             resp_format = srv.resp_format if srv is not None else W.WALLY_RESP_FULL

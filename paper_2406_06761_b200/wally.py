@@ -31,7 +31,8 @@ EXPORTED = [
     "wally_fetch_responses", "wally_host_workspace_bytes", "wally_eval_batch_host", "wally_route_queries",
     "wally_ntt_forward", "wally_ntt_inverse", "wally_kernel_launches", "wally_enable_stage_timing",
     "wally_stage_times", "wally_assign_owners", "wally_route_plan", "wally_pack_queries",
-    "wally_response_words_per_plaintext",
+    "wally_response_words_per_plaintext", "wally_assign_owners_replicated", "wally_route_plan_replicated",
+    "wally_load_clusters_replicated",
 ]
 
 
@@ -86,6 +87,10 @@ def _load():
         "wally_route_plan": ([u32, P(u32), u32, P(u32), P(i32), u32, u32, u32, u32, P(u32), P(u32), P(u64),
                               P(u64)], ctypes.c_int),
         "wally_response_words_per_plaintext": ([vp, P(u64)], ctypes.c_int),
+        "wally_assign_owners_replicated": ([u32, P(ctypes.c_double), u32, P(u64)], ctypes.c_int),
+        "wally_route_plan_replicated": ([u32, P(u32), u32, P(u32), P(u64), u32, u32, u32, u32, P(u32), P(u32),
+                                         P(u64), P(u64)], ctypes.c_int),
+        "wally_load_clusters_replicated": ([vp, u32, P(u32), P(u64), i32], ctypes.c_int),
         "wally_pack_queries": ([vp, u32, vp, vp, vp, vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
@@ -131,6 +136,19 @@ def wally_assign_owners(weights, world: int) -> np.ndarray:
     return out
 
 
+def wally_assign_owners_replicated(weights, world: int) -> np.ndarray:
+    """uint64 [clusters] replica masks: heavy clusters split over several ranks (C ABI)."""
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    out = np.zeros(w.size, dtype=np.uint64)
+    _check(lib.wally_assign_owners_replicated(w.size, w.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), world,
+                                              out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))))
+    return out
+
+
+def mask_ranks(mask: int) -> list[int]:
+    return [r for r in range(64) if (int(mask) >> r) & 1]
+
+
 class RoutePlan:
     """Result of wally_route_plan (see include/wally.h)."""
 
@@ -145,16 +163,26 @@ class RoutePlan:
 
 def wally_route_plan(cluster_of_query, cluster_sizes, owner, n: int, d: int, world: int,
                      resp_format: int = WALLY_RESP_FULL) -> RoutePlan:
+    """owner: int32 [clusters] rank per cluster, None (all on rank 0), or a uint64
+    replica-mask array (wally_assign_owners_replicated)."""
     ids = np.ascontiguousarray(cluster_of_query, dtype=np.uint32)
     sizes = np.ascontiguousarray(cluster_sizes, dtype=np.uint32)
-    own = None
-    if owner is not None:
-        owner = np.ascontiguousarray(owner, dtype=np.int32)
-        own = owner.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
     counts = np.zeros(world, dtype=np.uint32)
     order = np.zeros(ids.size, dtype=np.uint32)
     words = np.zeros(world, dtype=np.uint64)
     goff = np.zeros(ids.size + 1, dtype=np.uint64)
+    if owner is not None and np.asarray(owner).dtype == np.uint64:
+        mask = np.ascontiguousarray(owner, dtype=np.uint64)
+        _check(lib.wally_route_plan_replicated(ids.size, _u32p(ids), sizes.size, _u32p(sizes),
+                                               mask.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), n, d,
+                                               resp_format, world, _u32p(counts), _u32p(order),
+                                               words.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                               goff.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))))
+        return RoutePlan(counts, order, words, goff)
+    own = None
+    if owner is not None:
+        owner = np.ascontiguousarray(owner, dtype=np.int32)
+        own = owner.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
     _check(lib.wally_route_plan(ids.size, _u32p(ids), sizes.size, _u32p(sizes), own, n, d, resp_format, world,
                                 _u32p(counts),
                                 _u32p(order), words.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
@@ -203,12 +231,20 @@ class WallyServer:
 
     # ---- ServerInit ----
     def load_clusters(self, cluster_sizes, owner=None, rank: int = 0):
+        """owner: None (all local), int32 [clusters] owning rank, or uint64 [clusters]
+        replica masks (wally_assign_owners_replicated)."""
         sizes = np.ascontiguousarray(cluster_sizes, dtype=np.uint32)
-        own = None
-        if owner is not None:
-            owner = np.ascontiguousarray(owner, dtype=np.int32)
-            own = owner.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
-        _check(lib.wally_load_clusters(self.ctx, sizes.size, _u32p(sizes), own, rank), self.ctx)
+        if owner is not None and np.asarray(owner).dtype == np.uint64:
+            owner = np.ascontiguousarray(owner, dtype=np.uint64)
+            _check(lib.wally_load_clusters_replicated(self.ctx, sizes.size, _u32p(sizes),
+                                                      owner.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), rank),
+                   self.ctx)
+        else:
+            own = None
+            if owner is not None:
+                owner = np.ascontiguousarray(owner, dtype=np.int32)
+                own = owner.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+            _check(lib.wally_load_clusters(self.ctx, sizes.size, _u32p(sizes), own, rank), self.ctx)
         self.total_clusters = sizes.size
         self._sizes, self._owner, self._rank = sizes, owner, rank
         b = ctypes.c_size_t()
@@ -222,6 +258,8 @@ class WallyServer:
         """Ascending ids of the clusters this context owns (the order of the entries array)."""
         if self._owner is None:
             return np.arange(self.total_clusters, dtype=np.uint32)
+        if self._owner.dtype == np.uint64:
+            return np.nonzero((self._owner >> np.uint64(self._rank)) & np.uint64(1))[0].astype(np.uint32)
         return np.nonzero(self._owner == self._rank)[0].astype(np.uint32)
 
     def encode(self, entries_dev, stream=None):

@@ -78,6 +78,70 @@ def test_assign_owners_lpt(W):
     assert ld.max() - ld.min() <= zipf.max() + 1e-12
 
 
+def test_assign_owners_replicated_splits_only_heavy_clusters(W):
+    zipf = np.arange(1, 1001) ** -1.1
+    for world in (1, 2, 4, 8, 16):
+        m = W.wally_assign_owners_replicated(zipf, world)
+        reps = np.array([bin(int(x)).count("1") for x in m])
+        assert (reps >= 1).all() and (reps <= world).all()
+        assert all(max(W.mask_ranks(x)) < world for x in m)
+        target = zipf.sum() / world
+        # a cluster is replicated iff it is heavier than the mean rank load
+        assert np.array_equal(reps > 1, zipf > target) or world == 1
+        load = np.zeros(world)
+        for c, x in enumerate(m):
+            for r in W.mask_ranks(x):
+                load[r] += zipf[c] / reps[c]
+        assert load.max() - load.min() <= (zipf / reps).max() + 1e-12
+    # equal weights: no replication while clusters >= ranks ...
+    m = W.wally_assign_owners_replicated(np.ones(7), 5)
+    assert all(bin(int(x)).count("1") == 1 for x in m)
+    # ... and with more ranks than clusters every cluster (weight 1 > 3/5) gets
+    # ceil(1 / 0.6) = 2 replicas, spread so that every rank holds work
+    m = W.wally_assign_owners_replicated(np.ones(3), 5)
+    assert all(bin(int(x)).count("1") == 2 for x in m)
+    assert sorted(set(r for x in m for r in W.mask_ranks(x))) == [0, 1, 2, 3, 4]
+
+
+def _ref_plan_replicated(ids, sizes, mask, n, d, world):
+    """Definition written out: the j-th query of cluster c goes to the
+    (j mod r_c)-th lowest replica rank of c."""
+    E = n // d
+    seen = {}
+    dest = []
+    for c in ids:
+        ranks = [r for r in range(64) if (int(mask[c]) >> r) & 1]
+        j = seen.get(int(c), 0)
+        seen[int(c)] = j + 1
+        dest.append(ranks[j % len(ranks)])
+    order = [q for r in range(world) for q in range(len(ids)) if dest[q] == r]
+    counts = [dest.count(r) for r in range(world)]
+    words = [sum(2 * n * -(-int(sizes[ids[q]]) // E) for q in range(len(ids)) if dest[q] == r) for r in range(world)]
+    return counts, order, words
+
+
+def test_route_plan_replicated_matches_definition(W):
+    rng = np.random.default_rng(4)
+    C, n, d, world = 29, 1024, 100, 6
+    sizes = rng.integers(1, 300, size=C).astype(np.uint32)
+    w = rng.random(C) ** 6
+    w[3] = 2 * w.sum()                  # a hot cluster: heavier than the mean rank load
+    mask = W.wally_assign_owners_replicated(w, world)
+    assert any(bin(int(x)).count("1") > 1 for x in mask)
+    ids = rng.choice(C, size=500, p=w / w.sum()).astype(np.uint32)
+    p = W.wally_route_plan(ids, sizes, mask, n, d, world)
+    counts, order, words = _ref_plan_replicated(ids, sizes, mask, n, d, world)
+    assert p.counts.tolist() == counts and p.order.tolist() == order and p.resp_words.tolist() == words
+    with pytest.raises(W.WallyError):
+        bad = mask.copy()
+        bad[0] = np.uint64(0)
+        W.wally_route_plan(ids, sizes, bad, n, d, world)
+    with pytest.raises(W.WallyError):
+        bad = mask.copy()
+        bad[0] = np.uint64(1 << world)
+        W.wally_route_plan(ids, sizes, bad, n, d, world)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -86,7 +150,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, outq):
+def _worker(rank, world, port, outq, replicated=False):
     try:
         import torch.distributed as dist
         os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -99,7 +163,13 @@ def _worker(rank, world, port, outq):
         sizes = rng.integers(1, 40, size=C).astype(np.uint32)
         ids_all = rng.integers(0, C, size=nq).astype(np.uint32)
         cts_all = torch.from_numpy(rng.integers(0, 2**30, size=(nq, 2, L, n)).astype(np.int32))
-        owner = W.wally_assign_owners(sizes.astype(np.float64), world)
+        if replicated:
+            wts = sizes.astype(np.float64)
+            wts[2] = wts.sum()          # one hot cluster, heavier than the mean rank load
+            owner = W.wally_assign_owners_replicated(wts, world)
+            assert bin(int(owner[2])).count("1") == world
+        else:
+            owner = W.wally_assign_owners(sizes.astype(np.float64), world)
 
         def host_pack(index, cts):
             return cts[torch.from_numpy(index.astype(np.int64))].contiguous()
@@ -135,13 +205,13 @@ def _worker(rank, world, port, outq):
         outq.put((rank, traceback.format_exc()))
 
 
-@pytest.mark.parametrize("world", [2])
-def test_scatter_gather_gloo(W, world):
+@pytest.mark.parametrize("world,replicated", [(2, False), (2, True)])
+def test_scatter_gather_gloo(W, world, replicated):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, replicated)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=180) for _ in procs)

@@ -270,8 +270,8 @@ def test_pack_queries_kernel():
     srv.close()
 
 
-@pytest.mark.parametrize("world,fmt", [(2, 0), (3, 1), (2, 2)])
-def test_sharded_ranks_bit_identical_to_single_rank(world, fmt):
+@pytest.mark.parametrize("world,fmt,replicated", [(2, 0, False), (3, 1, False), (2, 2, False), (4, 2, True)])
+def test_sharded_ranks_bit_identical_to_single_rank(world, fmt, replicated):
     from paper_2406_06761_b200 import wally as W
     w = synth.scaled(synth.WORKLOADS["c5"], num_clusters=40, cluster_size=70, num_queries=97)
     ents = synth.cluster_entries(w)
@@ -281,7 +281,11 @@ def test_sharded_ranks_bit_identical_to_single_rank(world, fmt):
     ref, ref_off = H.run_batch(one, ids, cts)
     one.close()
     sizes = np.full(w.num_clusters, w.cluster_size, np.uint32)
-    owner = W.wally_assign_owners(synth.cluster_popularity(w), world)
+    if replicated:
+        owner = W.wally_assign_owners_replicated(synth.cluster_popularity(w), world)
+        assert any(bin(int(x)).count("1") > 1 for x in owner)     # the Zipf head is split
+    else:
+        owner = W.wally_assign_owners(synth.cluster_popularity(w), world)
     plan = W.wally_route_plan(ids, sizes, owner, w.n, w.d, world, fmt)
     gathered = np.empty(int(plan.gathered_off[-1]), np.uint32)
     base = np.concatenate([[0], np.cumsum(plan.resp_words.astype(np.int64))])
