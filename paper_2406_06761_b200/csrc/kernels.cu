@@ -16,6 +16,7 @@
 #include <cstdint>
 
 #include "ntt_device.cuh"
+#include "tmem.cuh"
 #include "wally_internal.h"
 
 namespace wally {
@@ -217,42 +218,49 @@ __device__ __forceinline__ uint32_t ms_term(uint32_t r, uint32_t h_m, uint32_t q
 //   r_m = (c_m + h_m) mod q_m,  c_l <- (c_l + h_m - r_m) q_m^{-1}  for l < m,
 // accumulating  A_l = sum_{m>l} (h_m - r_m) prod_{k=l+1..m} q_k^{-1}  so that
 // c_l(final) = c_l F_l + A_l.  Limb 0's final value is the response word.
-template <int L, int J, int V, int NA>
-__device__ __forceinline__ void ms_step(uint32_t (&a)[V], uint32_t (&rtop)[V], uint32_t (&acc)[NA][V],
-                                        const KParams &kp) {
+// Element form of the recurrence (limb J; rtop / acc = this coefficient's
+// state, NA = max(L - 2, 1) accumulators).
+template <int L, int J, int NA>
+__device__ __forceinline__ void ms_elem(uint32_t &a, uint32_t &rtop, uint32_t (&acc)[NA], const KParams &kp) {
     const uint32_t qj = kp.q[J];
-#pragma unroll
-    for (int v = 0; v < V; v++) a[v] = csub(a[v], qj);
+    a = csub(a, qj);
     if constexpr (L == 1) {
         return;
     } else if constexpr (J == L - 1) {
-#pragma unroll
-        for (int v = 0; v < V; v++) rtop[v] = csub(a[v] + kp.h[J], qj);
+        rtop = csub(a + kp.h[J], qj);
     } else {
-#pragma unroll
-        for (int v = 0; v < V; v++) {
-            uint32_t A;
-            if constexpr (J == L - 2)
-                A = ms_term(rtop[v], kp.h[L - 1], qj, kp.C[J][L - 1], kp.Cp[J][L - 1]);
-            else
-                A = acc[J][v];
-            a[v] = csub(a[v] + A, qj);
-        }
+        uint32_t A;
+        if constexpr (J == L - 2)
+            A = ms_term(rtop, kp.h[L - 1], qj, kp.C[J][L - 1], kp.Cp[J][L - 1]);
+        else
+            A = acc[J];
+        a = csub(a + A, qj);
         if constexpr (J > 0) {
+            const uint32_t r = csub(a + kp.h[J], qj);
 #pragma unroll
-            for (int v = 0; v < V; v++) {
-                const uint32_t r = csub(a[v] + kp.h[J], qj);
-#pragma unroll
-                for (int l = 0; l < J; l++) {
-                    const uint32_t ql = kp.q[l];
-                    const uint32_t term = ms_term(r, kp.h[J], ql, kp.C[l][J], kp.Cp[l][J]);
-                    if constexpr (J == L - 2)
-                        acc[l][v] = csub(ms_term(rtop[v], kp.h[L - 1], ql, kp.C[l][L - 1], kp.Cp[l][L - 1]) + term, ql);
-                    else
-                        acc[l][v] = csub(acc[l][v] + term, ql);
-                }
+            for (int l = 0; l < J; l++) {
+                const uint32_t ql = kp.q[l];
+                const uint32_t term = ms_term(r, kp.h[J], ql, kp.C[l][J], kp.Cp[l][J]);
+                if constexpr (J == L - 2)
+                    acc[l] = csub(ms_term(rtop, kp.h[L - 1], ql, kp.C[l][L - 1], kp.Cp[l][L - 1]) + term, ql);
+                else
+                    acc[l] = csub(acc[l] + term, ql);
             }
         }
+    }
+}
+
+template <int L, int J, int V, int NA>
+__device__ __forceinline__ void ms_step(uint32_t (&a)[V], uint32_t (&rtop)[V], uint32_t (&acc)[NA][V],
+                                        const KParams &kp) {
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+        uint32_t ac[NA];
+#pragma unroll
+        for (int l = 0; l < NA; l++) ac[l] = acc[l][v];
+        ms_elem<L, J, NA>(a[v], rtop[v], ac, kp);
+#pragma unroll
+        for (int l = 0; l < NA; l++) acc[l][v] = ac[l];
     }
 }
 
@@ -563,27 +571,6 @@ __global__ void __launch_bounds__(kEvalGroups * NttGeom<N>::T, 1) eval_kernel_gr
 // stall of v2 (profiles/r01_ncu_eval_v2.txt).  Measured TMEM read bandwidth:
 // 446 B/clk/SM (profiles/r01_intpipe_v2.jsonl), far above what this needs.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-                 : "r"(taddr));
-}
-
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
-                 ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
-                 : "memory");
-}
-
-// Waits for this thread's outstanding tcgen05.ld; the loaded registers are
-// passed through the asm so the compiler cannot hoist their uses above it.
-__device__ __forceinline__ void tmem_wait_ld(uint32_t (&r)[16]) {
-    asm volatile("tcgen05.wait::ld.sync.aligned;"
-                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
-                 :
-                 : "memory");
-}
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_ld2(uint32_t (&r)[16], uint32_t (&s)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;"
                  : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(s[0]), "+r"(s[1]), "+r"(s[2]), "+r"(s[3]), "+r"(s[4]), "+r"(s[5]), "+r"(s[6]), "+r"(s[7]), "+r"(s[8]), "+r"(s[9]), "+r"(s[10]), "+r"(s[11]), "+r"(s[12]), "+r"(s[13]), "+r"(s[14]), "+r"(s[15])
@@ -604,8 +591,8 @@ struct LimbLoopTM {
         const uint32_t q = ba.kp.q[J], q2 = ba.kp.q2[J];
         {
             uint32_t p[16], pp[16];
-            tmem_ld16(tcol + 32 * J, p);
-            tmem_ld16(tcol + 32 * J + 16, pp);
+            tmem_ld<16>(tcol + 32 * J, p);
+            tmem_ld<16>(tcol + 32 * J + 16, pp);
             tmem_wait_ld2(p, pp);
 #pragma unroll
             for (int v = 0; v < V / 4; v++)
@@ -636,26 +623,26 @@ struct LimbLoopTM {
         if constexpr (L == 3) {
             if constexpr (J < L - 1) {
                 // state written at limb J + 1: rtop (J == L - 2) or acc (J < L - 2)
-                tmem_wait_st();
+                tmem_wait_st_all();
 #pragma unroll
                 for (int c = 0; c < NC; c++) {
-                    if constexpr (J == L - 2) tmem_ld16(tcol + 96 + 16 * c, st.rtop[c]);
-                    else tmem_ld16(tcol + 96 + 16 * c, st.acc[c][0]);
+                    if constexpr (J == L - 2) tmem_ld<16>(tcol + 96 + 16 * c, st.rtop[c]);
+                    else tmem_ld<16>(tcol + 96 + 16 * c, st.acc[c][0]);
                 }
 #pragma unroll
                 for (int c = 0; c < NC; c++) {
-                    if constexpr (J == L - 2) tmem_wait_ld(st.rtop[c]);
-                    else tmem_wait_ld(st.acc[c][0]);
+                    if constexpr (J == L - 2) tmem_wait_ld<16>(st.rtop[c]);
+                    else tmem_wait_ld<16>(st.acc[c][0]);
                 }
             }
 #pragma unroll
             for (int c = 0; c < NC; c++) ms_step<L, J, V>(st.a[c], st.rtop[c], st.acc[c], ba.kp);
             if constexpr (J == L - 1) {
 #pragma unroll
-                for (int c = 0; c < NC; c++) tmem_st16(tcol + 96 + 16 * c, st.rtop[c]);
+                for (int c = 0; c < NC; c++) tmem_st<16>(tcol + 96 + 16 * c, st.rtop[c]);
             } else if constexpr (J > 0) {
 #pragma unroll
-                for (int c = 0; c < NC; c++) tmem_st16(tcol + 96 + 16 * c, st.acc[c][0]);
+                for (int c = 0; c < NC; c++) tmem_st<16>(tcol + 96 + 16 * c, st.acc[c][0]);
             }
         } else {
 #pragma unroll
@@ -693,10 +680,10 @@ __device__ __forceinline__ void eval_item_tm(const BatchArgs &ba, const ItemCurs
             p[4 * v] = x.x; p[4 * v + 1] = x.y; p[4 * v + 2] = x.z; p[4 * v + 3] = x.w;
             pp[4 * v] = y.x; pp[4 * v + 1] = y.y; pp[4 * v + 2] = y.z; pp[4 * v + 3] = y.w;
         }
-        tmem_st16(tcol + 32 * J, p);
-        tmem_st16(tcol + 32 * J + 16, pp);
+        tmem_st<16>(tcol + 32 * J, p);
+        tmem_st<16>(tcol + 32 * J + 16, pp);
     }
-    tmem_wait_st();
+    tmem_wait_st_all();
     uint32_t qo = ba.perm[qb];
     uint4 cpre[NC][V / 4];
     {
@@ -863,6 +850,7 @@ cudaError_t launch_ntt_inverse(const KParams &kp, uint32_t n, uint32_t L, const 
     }
     return cudaErrorInvalidValue;
 }
+
 
 template <int N, int L, int FMT>
 static cudaError_t launch_eval_tm(const BatchArgs &a, cudaStream_t s, int num_sms) {
