@@ -29,6 +29,7 @@ struct wally_ctx {
     uint64_t wpp = 0;  // response words per plaintext
     KParams kp{};
     uint2 *d_tw_fwd = nullptr, *d_tw_inv = nullptr;
+    uint2 *d_tw_mrg = nullptr;  // [L][n] merged inverse table psi^{-brev(i)} (pruned c0 transform)
     // cluster layout
     bool loaded = false;
     uint32_t total_clusters = 0, n_local = 0, npt = 0, max_pt = 0;
@@ -215,6 +216,7 @@ extern "C" void wally_destroy(wally_ctx *c) {
     cudaDeviceSynchronize();
     cudaFree(c->d_tw_fwd);
     cudaFree(c->d_tw_inv);
+    cudaFree(c->d_tw_mrg);
     cudaFree(c->d_local_of_cluster);
     cudaFree(c->d_pt_base);
     cudaFree(c->d_n_pt);
@@ -273,7 +275,7 @@ extern "C" int wally_create(const wally_params *pp, int device, wally_ctx **out)
     while ((1u << logn) < n) logn++;
     KParams &kp = c->kp;
     const size_t tw_limb = tw_limb_entries(n);
-    std::vector<uint2> twf((size_t)L * tw_limb), twi((size_t)L * tw_limb);
+    std::vector<uint2> twf((size_t)L * tw_limb), twi((size_t)L * tw_limb), twm((size_t)L * n);
     for (uint32_t l = 0; l < L; l++) {
         const uint64_t q = p.moduli[l];
         kp.q[l] = (uint32_t)q;
@@ -303,14 +305,17 @@ extern "C" int wally_create(const wally_params *pp, int device, wally_ctx **out)
             pi[i] = make_uint2(wi, shoup_companion(wi, (uint32_t)q));
         }
         build_pass_tables(n, pf.data(), pi.data(), twf.data() + l * tw_limb, twi.data() + l * tw_limb);
+        std::copy(pi.begin(), pi.end(), twm.begin() + (size_t)l * n);
     }
     const size_t tb = sizeof(uint2) * twf.size();
-    if (cudaMalloc(&c->d_tw_fwd, tb) != cudaSuccess || cudaMalloc(&c->d_tw_inv, tb) != cudaSuccess) {
+    if (cudaMalloc(&c->d_tw_fwd, tb) != cudaSuccess || cudaMalloc(&c->d_tw_inv, tb) != cudaSuccess ||
+        cudaMalloc(&c->d_tw_mrg, sizeof(uint2) * twm.size()) != cudaSuccess) {
         wally_destroy(c);
         return fail(nullptr, WALLY_E_OOM, "twiddle table allocation failed");
     }
     cudaMemcpy(c->d_tw_fwd, twf.data(), tb, cudaMemcpyHostToDevice);
     cudaMemcpy(c->d_tw_inv, twi.data(), tb, cudaMemcpyHostToDevice);
+    cudaMemcpy(c->d_tw_mrg, twm.data(), sizeof(uint2) * twm.size(), cudaMemcpyHostToDevice);
     for (auto &s : c->slot) cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming);
     cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
     if (cudaGetLastError() != cudaSuccess) {
@@ -555,6 +560,7 @@ static int eval_impl(wally_ctx *c, uint32_t nq, const uint32_t *ids, const uint3
     a.total_clusters = c->total_clusters;
     a.tw_fwd = c->d_tw_fwd;
     a.tw_inv = c->d_tw_inv;
+    a.tw_mrg = c->d_tw_mrg;
     a.local_of_cluster = c->d_local_of_cluster;
     a.pt_base = c->d_pt_base;
     a.n_pt = c->d_n_pt;

@@ -852,6 +852,297 @@ cudaError_t launch_ntt_inverse(const KParams &kp, uint32_t n, uint32_t L, const 
 }
 
 
+
+// ---------------------------------------------------------------------------
+// Fused kernel v6 (n = 4096, L <= 3, compact responses, 16 | d): pruned
+// inverse NTT for c0.  A compact response keeps c0 only at the result
+// coefficients j d + d - 1, all of which are = -1 (mod M), M = 2^v2(d).  In
+// the Gentleman-Sande order used here (stage s pairs positions B + o and
+// B + o + 2^s), those outputs need, at every stage s < log2 M, only the Y
+// output of the last butterfly of each block, and at every later stage only
+// the butterflies at offsets o = -1 (mod M): N/(2M) per stage.  For c3
+// (d = 192, M = 64) that is 4,224 of c0's 24,576 butterflies per limb, and the
+// modulus switch of c0 runs on N/M = 64 coefficients instead of 4,096 -- the
+// pair's modular multiplications drop by about a third, with the compact
+// response bit-identical (the oracle is compared at the result coefficients).
+//   * pass 0 (stages 0..3): every thread keeps only its group's last Y
+//     output (15 Shoup products instead of 32 butterflies), position 16 g + 15;
+//   * stages 4..11 on those 256 values: warp 0 of the group, in shared memory,
+//     twiddles from the plain merged table (global, L1-cached), then the
+//     modulus switch of the N/M surviving coefficients (state in shared
+//     memory), and after limb 0 the write of the E result words;
+//   * c1 runs the full transform (NC = 1) of the v4 kernel, its plaintext
+//     slice and (L = 3) mod-switch state in tensor memory.
+// ---------------------------------------------------------------------------
+template <int S>
+__device__ __forceinline__ void c0_yonly_stage(uint32_t (&a)[16], const uint2 *tw0, int g, uint32_t q, uint32_t q2) {
+    using Gm = NttGeom<4096>;
+    constexpr int T = Gm::T, R = 16;
+    constexpr int t = 1 << S, NB = R >> (S + 1), OFF = R - (R >> S);
+    const uint4 *t4 = reinterpret_cast<const uint4 *>(tw0) + g;
+    uint2 w[NB];
+    if constexpr (NB >= 2) {
+#pragma unroll
+        for (int b = 0; b < NB / 2; b++) {
+            const uint4 x = t4[(OFF / 2 + b) * T];
+            w[2 * b] = make_uint2(x.x, x.y);
+            w[2 * b + 1] = make_uint2(x.z, x.w);
+        }
+    } else {
+        w[0] = reinterpret_cast<const uint2 *>(t4 + (OFF / 2) * T)[OFF % 2];
+    }
+#pragma unroll
+    for (int b = 0; b < NB; b++) {
+        const uint32_t X = a[b * 2 * t + t - 1], Y = a[b * 2 * t + 2 * t - 1];
+        a[b * 2 * t + 2 * t - 1] = shoup_mul(X - Y + q2, w[b].x, w[b].y, q);
+    }
+}
+
+// Stages 4..11 of c0 on z[c] = x[16 c + 15] (shared memory), then the
+// modulus-switch step of limb J on the N/M surviving coefficients.  Warp 0
+// of the group only; lanes stride over butterflies / coefficients.
+template <int L, int J>
+__device__ __forceinline__ void c0_tail(uint32_t *z, uint32_t *cst, const uint2 *mrg, int lane, int mu,
+                                        const KParams &kp) {
+    constexpr int N = 4096, LOGN = 12;
+    constexpr int NA = (L > 2) ? (L - 2) : 1;
+    const uint32_t q = kp.q[J], q2 = kp.q2[J];
+    const int M = 1 << mu;
+#pragma unroll 1
+    for (int s = 4; s < LOGN; s++) {
+        const int t = 1 << s, m = N / (2 * t);
+        if (s < mu) {
+            for (int blk = lane; blk < N / (2 * t); blk += 32) {
+                const int B = blk * 2 * t;
+                const int cx = (B + t - 16) >> 4, cy = (B + 2 * t - 16) >> 4;
+                const uint2 w = __ldg(mrg + m + blk);
+                z[cy] = shoup_mul(z[cx] - z[cy] + q2, w.x, w.y, q);
+            }
+        } else {
+            const int per = t / M;
+            for (int i = lane; i < N / (2 * M); i += 32) {
+                const int blk = i / per, o = M - 1 + (i % per) * M;
+                const int B = blk * 2 * t;
+                const int cx = (B + o - 15) >> 4, cy = (B + o + t - 15) >> 4;
+                const uint2 w = __ldg(mrg + m + blk);
+                const uint32_t X = z[cx], Y = z[cy];
+                z[cx] = csub(X + Y, q2);
+                z[cy] = shoup_mul(X - Y + q2, w.x, w.y, q);
+            }
+        }
+        __syncwarp();
+    }
+    // modulus switch of the coefficients k M + M - 1 (state [k][1 + NA] words)
+    for (int k = lane; k < N / M; k += 32) {
+        const int c = k * (M >> 4) + (M >> 4) - 1;
+        uint32_t x = z[c], rtop = cst[k * (1 + NA)], acc[NA];
+#pragma unroll
+        for (int l = 0; l < NA; l++) acc[l] = cst[k * (1 + NA) + 1 + l];
+        ms_elem<L, J, NA>(x, rtop, acc, kp);
+        cst[k * (1 + NA)] = rtop;
+#pragma unroll
+        for (int l = 0; l < NA; l++) cst[k * (1 + NA) + 1 + l] = acc[l];
+        z[c] = x;
+    }
+    __syncwarp();
+}
+
+template <int L, int J>
+struct LimbLoopPR {
+    static constexpr int N = 4096;
+    static __device__ __forceinline__ void run(EvalState<N, L, 1> &st, uint32_t (&a0)[16], uint4 (&cpre)[2][4],
+                                               const BatchArgs &ba, const uint32_t *chat_q,
+                                               const uint32_t *chat_next, uint32_t tcol, int g, const ChainCtx &cx,
+                                               uint32_t *ybuf, uint32_t &par, uint32_t *cst, int mu) {
+        using Gm = NttGeom<N>;
+        constexpr int V = Gm::V;
+        const uint32_t q = ba.kp.q[J], q2 = ba.kp.q2[J];
+        {
+            uint32_t p[16], pp[16];
+            tmem_ld<16>(tcol + 32 * J, p);
+            tmem_ld<16>(tcol + 32 * J + 16, pp);
+            tmem_wait_ld2(p, pp);
+#pragma unroll
+            for (int v = 0; v < V / 4; v++) {
+                a0[4 * v + 0] = shoup_mul(cpre[0][v].x, p[4 * v + 0], pp[4 * v + 0], q);
+                a0[4 * v + 1] = shoup_mul(cpre[0][v].y, p[4 * v + 1], pp[4 * v + 1], q);
+                a0[4 * v + 2] = shoup_mul(cpre[0][v].z, p[4 * v + 2], pp[4 * v + 2], q);
+                a0[4 * v + 3] = shoup_mul(cpre[0][v].w, p[4 * v + 3], pp[4 * v + 3], q);
+                st.a[0][4 * v + 0] = shoup_mul(cpre[1][v].x, p[4 * v + 0], pp[4 * v + 0], q);
+                st.a[0][4 * v + 1] = shoup_mul(cpre[1][v].y, p[4 * v + 1], pp[4 * v + 1], q);
+                st.a[0][4 * v + 2] = shoup_mul(cpre[1][v].z, p[4 * v + 2], pp[4 * v + 2], q);
+                st.a[0][4 * v + 3] = shoup_mul(cpre[1][v].w, p[4 * v + 3], pp[4 * v + 3], q);
+            }
+        }
+        const uint32_t *nsrc = (J > 0) ? chat_q + (size_t)(J - 1) * N : (chat_next ? chat_next + (size_t)(L - 1) * N
+                                                                                   : nullptr);
+        if (nsrc) {
+#pragma unroll
+            for (int c = 0; c < 2; c++)
+#pragma unroll
+                for (int v = 0; v < V / 4; v++)
+                    cpre[c][v] = ldg_stream(nsrc + (size_t)c * L * N + (size_t)g * V + 4 * v);
+        }
+        // c0: pass 0 keeping the last Y output of each block -> one value per thread
+        const uint2 *twJ = cx.tw + (size_t)J * Gm::TW_LIMB;
+        c0_yonly_stage<0>(a0, twJ, g, q, q2);
+        c0_yonly_stage<1>(a0, twJ, g, q, q2);
+        c0_yonly_stage<2>(a0, twJ, g, q, q2);
+        c0_yonly_stage<3>(a0, twJ, g, q, q2);
+        uint32_t *z = ybuf + par * Gm::T;
+        z[g] = a0[15];
+        // c1: full transform (its group barriers also publish z)
+        intt_chain_group<N, 1>(st.a, twJ, g, q, q2, cx.bufA, cx.bar);
+        if (g < 32) c0_tail<L, J>(z, cst, ba.tw_mrg + (size_t)J * N, g, mu, ba.kp);
+        par ^= 1u;
+        if constexpr (L == 3) {
+            if constexpr (J < L - 1) {
+                tmem_wait_st_all();
+                if constexpr (J == L - 2) {
+                    tmem_ld<16>(tcol + 96, st.rtop[0]);
+                    tmem_wait_ld<16>(st.rtop[0]);
+                } else {
+                    tmem_ld<16>(tcol + 96, st.acc[0][0]);
+                    tmem_wait_ld<16>(st.acc[0][0]);
+                }
+            }
+            ms_step<L, J, V>(st.a[0], st.rtop[0], st.acc[0], ba.kp);
+            if constexpr (J == L - 1) tmem_st<16>(tcol + 96, st.rtop[0]);
+            else if constexpr (J > 0) tmem_st<16>(tcol + 96, st.acc[0][0]);
+        } else {
+            ms_step<L, J, V>(st.a[0], st.rtop[0], st.acc[0], ba.kp);
+        }
+        if constexpr (J > 0)
+            LimbLoopPR<L, J - 1>::run(st, a0, cpre, ba, chat_q, chat_next, tcol, g, cx, ybuf, par, cst, mu);
+    }
+};
+
+template <int L, int FMT>
+__device__ __forceinline__ void eval_item_pr(const BatchArgs &ba, const ItemCursor &cur, uint32_t item, int g,
+                                             const ChainCtx &cx, const uint32_t *s_rmap, uint32_t tcol,
+                                             uint32_t *ybuf, uint32_t &par, uint32_t *cst, int mu) {
+    constexpr int N = 4096;
+    using Gm = NttGeom<N>;
+    constexpr int V = Gm::V;
+    const uint32_t li = cur.li;
+    const uint32_t cnt = ba.counts[li];
+    const uint32_t local = item - cur.b;
+    const uint32_t P = ba.n_pt[li];
+    const uint32_t ch = local / P, k = local % P;
+    const uint32_t qb = ba.seg[li] + ch * kQueryChunk;
+    const uint32_t qe = min(qb + kQueryChunk, ba.seg[li] + cnt);
+    const uint32_t *phat = ba.store + (size_t)(ba.pt_base[li] + k) * L * 2 * N;
+#pragma unroll
+    for (int J = 0; J < L; J++) {
+        uint32_t p[16], pp[16];
+        const uint32_t *pv = phat + (size_t)J * 2 * N + (size_t)g * V;
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+            const uint4 x = ldg_stream(pv + 4 * v), y = ldg_stream(pv + N + 4 * v);
+            p[4 * v] = x.x; p[4 * v + 1] = x.y; p[4 * v + 2] = x.z; p[4 * v + 3] = x.w;
+            pp[4 * v] = y.x; pp[4 * v + 1] = y.y; pp[4 * v + 2] = y.z; pp[4 * v + 3] = y.w;
+        }
+        tmem_st<16>(tcol + 32 * J, p);
+        tmem_st<16>(tcol + 32 * J + 16, pp);
+    }
+    tmem_wait_st_all();
+    uint32_t qo = ba.perm[qb];
+    uint4 cpre[2][V / 4];
+    {
+        const uint32_t *src = ba.chat + (size_t)qo * 2 * L * N + (size_t)(L - 1) * N;
+#pragma unroll
+        for (int c = 0; c < 2; c++)
+#pragma unroll
+            for (int v = 0; v < V / 4; v++) cpre[c][v] = ldg_stream(src + (size_t)c * L * N + (size_t)g * V + 4 * v);
+    }
+    const int M = 1 << mu;
+    for (uint32_t qi = qb; qi < qe; qi++) {
+        const uint32_t qn = (qi + 1 < qe) ? ba.perm[qi + 1] : 0xffffffffu;
+        uint32_t *out_q = ba.resp + ba.resp_off[qo] + (size_t)k * ba.wpp;
+        const uint32_t *chat_q = ba.chat + (size_t)qo * 2 * L * N;
+        const uint32_t *chat_next = (qn != 0xffffffffu) ? ba.chat + (size_t)qn * 2 * L * N : nullptr;
+        EvalState<N, L, 1> st;
+        uint32_t a0[16];
+        LimbLoopPR<L, L - 1>::run(st, a0, cpre, ba, chat_q, chat_next, tcol, g, cx, ybuf, par, cst, mu);
+        // c0 results: coefficient k M + M - 1 is result j when (k M + M) = (j + 1) d
+        if (g < 32) {
+            const uint32_t *z = ybuf + (par ^ 1u) * Gm::T;  // the buffer limb 0 used
+            for (int kk = g; kk < N / M; kk += 32) {
+                const uint32_t pos1 = (uint32_t)(kk * M + M);
+                if (pos1 % ba.d == 0) __stcs(out_q + pos1 / ba.d - 1, z[kk * (M >> 4) + (M >> 4) - 1]);
+            }
+            const uint32_t e4 = (ba.E + 3) & ~3u;
+            if ((uint32_t)g < e4 - ba.E) __stcs(out_q + ba.E + g, 0u);
+        }
+        write_component<N, FMT>(ba, out_q, st.a[0], 1, g, s_rmap);
+        qo = qn;
+    }
+}
+
+template <int L, int FMT>
+__global__ void __launch_bounds__(kEvalGroups * NttGeom<4096>::T, 1) eval_kernel_pr(BatchArgs ba) {
+    constexpr int N = 4096;
+    using Gm = NttGeom<N>;
+    constexpr int T = Gm::T;
+    constexpr int NA = (L > 2) ? (L - 2) : 1;
+    extern __shared__ uint4 smem4[];
+    uint2 *tw = reinterpret_cast<uint2 *>(smem4);
+    uint32_t *xbuf = reinterpret_cast<uint32_t *>(tw + L * Gm::TW_LIMB);
+    __shared__ uint32_t s_item[kEvalGroups][2];
+    __shared__ uint32_t s_rmap[ResultMap<N>::WORDS];
+    __shared__ uint32_t s_ybuf[kEvalGroups][2 * T];
+    __shared__ uint32_t s_cst[kEvalGroups][(N / 16) * (1 + NA)];
+    __shared__ uint32_t s_taddr;
+    const int grp = threadIdx.x / T, g = threadIdx.x % T;
+    const int warp = threadIdx.x / 32;
+    if (warp == 0) {
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&s_taddr);
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(dst) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(ba.tw_inv);
+        for (int i = threadIdx.x; i < L * Gm::TW_LIMB / 2; i += blockDim.x) smem4[i] = __ldg(src + i);
+    }
+    build_result_map<N>(s_rmap, ba.d);
+    if (g == 0) s_item[grp][0] = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tcol = s_taddr + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 128);
+    const ChainCtx cx{tw, xbuf + grp * Gm::SMEM_WORDS, nullptr, 1 + grp};
+    const int mu = min(__ffs((int)ba.d) - 1, 12);
+    const uint32_t total = ba.misc[kMiscTotalItems];
+    uint32_t par = 0;
+    ItemCursor cur;
+    for (uint32_t it = 0;; it++) {
+        const uint32_t item = s_item[grp][it & 1];
+        if (item >= total) break;
+        if (g == 0) s_item[grp][(it + 1) & 1] = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
+        cur.seek(ba, item);
+        eval_item_pr<L, FMT>(ba, cur, item, g, cx, s_rmap, tcol, s_ybuf[grp], par, s_cst[grp], mu);
+        group_sync(1 + grp, T);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_taddr) : "memory");
+}
+
+template <int L, int FMT>
+static cudaError_t launch_eval_pr(const BatchArgs &a, cudaStream_t s, int num_sms) {
+    using Gm = NttGeom<4096>;
+    static bool configured = false;
+    const size_t smem = (size_t)L * Gm::TW_LIMB * sizeof(uint2) + (size_t)kEvalGroups * Gm::SMEM_WORDS * sizeof(uint32_t);
+    if (!configured) {
+        cudaError_t e = allow_smem(eval_kernel_pr<L, FMT>, smem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    eval_kernel_pr<L, FMT><<<num_sms, kEvalGroups * Gm::T, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
 template <int N, int L, int FMT>
 static cudaError_t launch_eval_tm(const BatchArgs &a, cudaStream_t s, int num_sms) {
     using Gm = NttGeom<N>;
@@ -876,6 +1167,16 @@ static cudaError_t launch_eval_nl(const BatchArgs &a, cudaStream_t s, int num_sm
 #ifndef WALLY_EVAL_TMEM
 #define WALLY_EVAL_TMEM 1
 #endif
+#ifndef WALLY_EVAL_PRUNE
+#define WALLY_EVAL_PRUNE 1
+#endif
+    if constexpr (N == 4096 && L >= 2 && L <= 3 && WALLY_EVAL_TMEM && WALLY_EVAL_PRUNE) {
+        // compact responses with 16 | d: pruned c0 transform (v6)
+        if (a.compact && (a.d & 15u) == 0) {
+            if (a.drop) return launch_eval_pr<L, (int)WALLY_RESP_COMPACT_DROP>(a, s, num_sms);
+            return launch_eval_pr<L, (int)WALLY_RESP_COMPACT>(a, s, num_sms);
+        }
+    }
     if constexpr (N == 4096 && L >= 2 && L <= 3 && WALLY_EVAL_TMEM) {
         if (a.drop) return launch_eval_tm<N, L, (int)WALLY_RESP_COMPACT_DROP>(a, s, num_sms);
         if (a.compact) return launch_eval_tm<N, L, (int)WALLY_RESP_COMPACT>(a, s, num_sms);

@@ -54,7 +54,8 @@ struct BatchArgs {
     uint32_t n_local;
     uint32_t total_clusters;
     const uint2 *tw_fwd;          // [L][n] (w, w') psi^{brev(i)}
-    const uint2 *tw_inv;          // [L][n] (w, w') psi^{-brev(i)}
+    const uint2 *tw_inv;          // [L] pass-major inverse tables (ntt_device.cuh)
+    const uint2 *tw_mrg;          // [L][n] (w, w') psi^{-brev(i)}, plain merged order
     const int32_t *local_of_cluster;  // [total_clusters]
     const uint32_t *pt_base;      // [n_local]
     const uint32_t *n_pt;         // [n_local]

@@ -102,6 +102,11 @@ EDGE = [
     dict(n=4096, L=4, d=128, sizes=[65, 1024], nq=17),
     dict(n=8192, L=4, d=512, sizes=[17, 33], nq=12),
     dict(n=8192, L=2, d=300, sizes=[100], nq=9),
+    # pruned c0 transform (compact formats, 16 | d) at several M = 2^v2(d)
+    dict(n=4096, L=3, d=16, sizes=[300, 7], nq=11),
+    dict(n=4096, L=3, d=48, sizes=[200], nq=9),
+    dict(n=4096, L=2, d=4096, sizes=[3, 1], nq=5),
+    dict(n=4096, L=2, d=1024, sizes=[9], nq=20),
 ]
 
 
