@@ -898,9 +898,33 @@ __device__ __forceinline__ void c0_yonly_stage(uint32_t (&a)[16], const uint2 *t
     }
 }
 
-// Stages 4..11 of c0 on z[c] = x[16 c + 15] (shared memory), then the
+// Stages 8..11 of c0 on z[c] = x[16 c + 15] (shared memory), then the
 // modulus-switch step of limb J on the N/M surviving coefficients.  Warp 0
-// of the group only; lanes stride over butterflies / coefficients.
+// of the group only; lanes stride over butterflies / coefficients.  mrg =
+// the limb's merged inverse table entries 0..255, staged in shared memory
+// (stage s uses entry 2^(11-s) + block).  (A register/shuffle variant of
+// this tail measured slower: 140 vs 110 ms on c3, from register pressure.)
+// Stages 4..7 of c0 for every thread of the group: thread g holds
+// z[g] = x[16 g + 15]; stage s pairs threads g and g ^ 2^(s-4), inside a
+// warp, so one shuffle per stage.  Same pruning rule as the tail.
+__device__ __forceinline__ uint32_t c0_mid(uint32_t y, int g, int mu, const uint2 *mrg, uint32_t q, uint32_t q2) {
+    const int Mc = 1 << (mu - 4);
+#pragma unroll
+    for (int s = 4; s < 8; s++) {
+        const int D = 1 << (s - 4), m = 2048 >> s;
+        const uint32_t other = __shfl_xor_sync(0xffffffffu, y, D);
+        const bool upper = (g & D) != 0;
+        const int o = (g & (2 * D - 1)) & (D - 1);      // offset of the pair inside its block
+        const uint2 w = mrg[m + g / (2 * D)];
+        if (s < mu) {
+            if (upper && o == D - 1) y = shoup_mul(other - y + q2, w.x, w.y, q);
+        } else if (((o + 1) & (Mc - 1)) == 0) {
+            y = upper ? shoup_mul(other - y + q2, w.x, w.y, q) : csub(y + other, q2);
+        }
+    }
+    return y;
+}
+
 template <int L, int J>
 __device__ __forceinline__ void c0_tail(uint32_t *z, uint32_t *cst, const uint2 *mrg, int lane, int mu,
                                         const KParams &kp) {
@@ -909,13 +933,13 @@ __device__ __forceinline__ void c0_tail(uint32_t *z, uint32_t *cst, const uint2 
     const uint32_t q = kp.q[J], q2 = kp.q2[J];
     const int M = 1 << mu;
 #pragma unroll 1
-    for (int s = 4; s < LOGN; s++) {
+    for (int s = 8; s < LOGN; s++) {
         const int t = 1 << s, m = N / (2 * t);
         if (s < mu) {
             for (int blk = lane; blk < N / (2 * t); blk += 32) {
                 const int B = blk * 2 * t;
                 const int cx = (B + t - 16) >> 4, cy = (B + 2 * t - 16) >> 4;
-                const uint2 w = __ldg(mrg + m + blk);
+                const uint2 w = mrg[m + blk];
                 z[cy] = shoup_mul(z[cx] - z[cy] + q2, w.x, w.y, q);
             }
         } else {
@@ -924,7 +948,7 @@ __device__ __forceinline__ void c0_tail(uint32_t *z, uint32_t *cst, const uint2 
                 const int blk = i / per, o = M - 1 + (i % per) * M;
                 const int B = blk * 2 * t;
                 const int cx = (B + o - 15) >> 4, cy = (B + o + t - 15) >> 4;
-                const uint2 w = __ldg(mrg + m + blk);
+                const uint2 w = mrg[m + blk];
                 const uint32_t X = z[cx], Y = z[cy];
                 z[cx] = csub(X + Y, q2);
                 z[cy] = shoup_mul(X - Y + q2, w.x, w.y, q);
@@ -953,7 +977,8 @@ struct LimbLoopPR {
     static __device__ __forceinline__ void run(EvalState<N, L, 1> &st, uint32_t (&a0)[16], uint4 (&cpre)[2][4],
                                                const BatchArgs &ba, const uint32_t *chat_q,
                                                const uint32_t *chat_next, uint32_t tcol, int g, const ChainCtx &cx,
-                                               uint32_t *ybuf, uint32_t &par, uint32_t *cst, int mu) {
+                                               uint32_t *ybuf, uint32_t &par, uint32_t *cst, int mu,
+                                               const uint2 *s_mrg) {
         using Gm = NttGeom<N>;
         constexpr int V = Gm::V;
         const uint32_t q = ba.kp.q[J], q2 = ba.kp.q2[J];
@@ -990,10 +1015,10 @@ struct LimbLoopPR {
         c0_yonly_stage<2>(a0, twJ, g, q, q2);
         c0_yonly_stage<3>(a0, twJ, g, q, q2);
         uint32_t *z = ybuf + par * Gm::T;
-        z[g] = a0[15];
+        z[g] = c0_mid(a0[15], g, mu, s_mrg + J * 256, q, q2);
         // c1: full transform (its group barriers also publish z)
         intt_chain_group<N, 1>(st.a, twJ, g, q, q2, cx.bufA, cx.bar);
-        if (g < 32) c0_tail<L, J>(z, cst, ba.tw_mrg + (size_t)J * N, g, mu, ba.kp);
+        if (g < 32) c0_tail<L, J>(z, cst, s_mrg + J * 256, g, mu, ba.kp);
         par ^= 1u;
         if constexpr (L == 3) {
             if constexpr (J < L - 1) {
@@ -1013,14 +1038,15 @@ struct LimbLoopPR {
             ms_step<L, J, V>(st.a[0], st.rtop[0], st.acc[0], ba.kp);
         }
         if constexpr (J > 0)
-            LimbLoopPR<L, J - 1>::run(st, a0, cpre, ba, chat_q, chat_next, tcol, g, cx, ybuf, par, cst, mu);
+            LimbLoopPR<L, J - 1>::run(st, a0, cpre, ba, chat_q, chat_next, tcol, g, cx, ybuf, par, cst, mu, s_mrg);
     }
 };
 
 template <int L, int FMT>
 __device__ __forceinline__ void eval_item_pr(const BatchArgs &ba, const ItemCursor &cur, uint32_t item, int g,
                                              const ChainCtx &cx, const uint32_t *s_rmap, uint32_t tcol,
-                                             uint32_t *ybuf, uint32_t &par, uint32_t *cst, int mu) {
+                                             uint32_t *ybuf, uint32_t &par, uint32_t *cst, int mu,
+                                             const uint2 *s_mrg) {
     constexpr int N = 4096;
     using Gm = NttGeom<N>;
     constexpr int V = Gm::V;
@@ -1063,7 +1089,7 @@ __device__ __forceinline__ void eval_item_pr(const BatchArgs &ba, const ItemCurs
         const uint32_t *chat_next = (qn != 0xffffffffu) ? ba.chat + (size_t)qn * 2 * L * N : nullptr;
         EvalState<N, L, 1> st;
         uint32_t a0[16];
-        LimbLoopPR<L, L - 1>::run(st, a0, cpre, ba, chat_q, chat_next, tcol, g, cx, ybuf, par, cst, mu);
+        LimbLoopPR<L, L - 1>::run(st, a0, cpre, ba, chat_q, chat_next, tcol, g, cx, ybuf, par, cst, mu, s_mrg);
         // c0 results: coefficient k M + M - 1 is result j when (k M + M) = (j + 1) d
         if (g < 32) {
             const uint32_t *z = ybuf + (par ^ 1u) * Gm::T;  // the buffer limb 0 used
@@ -1090,8 +1116,9 @@ __global__ void __launch_bounds__(kEvalGroups * NttGeom<4096>::T, 1) eval_kernel
     uint32_t *xbuf = reinterpret_cast<uint32_t *>(tw + L * Gm::TW_LIMB);
     __shared__ uint32_t s_item[kEvalGroups][2];
     __shared__ uint32_t s_rmap[ResultMap<N>::WORDS];
-    __shared__ uint32_t s_ybuf[kEvalGroups][2 * T];
+    __shared__ __align__(16) uint32_t s_ybuf[kEvalGroups][2 * T];
     __shared__ uint32_t s_cst[kEvalGroups][(N / 16) * (1 + NA)];
+    __shared__ uint2 s_mrg[L * 256];   // merged inverse table entries 0..255 of every limb (c0 tail)
     __shared__ uint32_t s_taddr;
     const int grp = threadIdx.x / T, g = threadIdx.x % T;
     const int warp = threadIdx.x / 32;
@@ -1105,6 +1132,7 @@ __global__ void __launch_bounds__(kEvalGroups * NttGeom<4096>::T, 1) eval_kernel
         for (int i = threadIdx.x; i < L * Gm::TW_LIMB / 2; i += blockDim.x) smem4[i] = __ldg(src + i);
     }
     build_result_map<N>(s_rmap, ba.d);
+    for (int i = threadIdx.x; i < L * 256; i += blockDim.x) s_mrg[i] = __ldg(ba.tw_mrg + (size_t)(i >> 8) * N + (i & 255));
     if (g == 0) s_item[grp][0] = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -1120,7 +1148,7 @@ __global__ void __launch_bounds__(kEvalGroups * NttGeom<4096>::T, 1) eval_kernel
         if (item >= total) break;
         if (g == 0) s_item[grp][(it + 1) & 1] = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
         cur.seek(ba, item);
-        eval_item_pr<L, FMT>(ba, cur, item, g, cx, s_rmap, tcol, s_ybuf[grp], par, s_cst[grp], mu);
+        eval_item_pr<L, FMT>(ba, cur, item, g, cx, s_rmap, tcol, s_ybuf[grp], par, s_cst[grp], mu, s_mrg);
         group_sync(1 + grp, T);
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
