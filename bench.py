@@ -350,7 +350,8 @@ def run_wally(args, rank, world, local_rank):
     peaks = measured_peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     clocks = clk.summary(t_clk0, t_clk1)
-    mm = modmul_per_pair(w.n, w.num_limbs)
+    mm = srv.modmuls_per_pair()                   # of the kernel variant this context runs
+    mm_full = modmul_per_pair(w.n, w.num_limbs)
     modmul_per_launch = float(mm) * pairs          # this rank's launch
     fused_ms = st_fused / max(nb, 1)
     achieved = modmul_per_launch / (fused_ms / 1e3) / 1e12
@@ -362,8 +363,11 @@ def run_wally(args, rank, world, local_rank):
                 "frac_vs_microbench": round(achieved / (SM_COUNT * MEASURED_MODMUL_PER_CLK_PER_SM * sm_max * 1e6 / 1e12),
                                             4),
                 "frac_vs_3imad_model": round(achieved * 3 / (SM_COUNT * 64 * sm_max * 1e6 / 1e12), 4),
+                "modmul_per_pair": int(mm), "modmul_per_pair_unpruned": int(mm_full),
+                "frac_unpruned_equiv": round(mm_full * pairs / (fused_ms / 1e3) / 1e12 / peak, 4),
                 "kernel": "eval_kernel (fused pointwise Shoup modmul + inverse NTT + RNS mod-switch)",
-                "per_launch": f"{pairs} pairs x {mm} modmul (SURVEY.md 8(d) M_pair)",
+                "per_launch": f"{pairs} pairs x {mm} modmul (wally_modmuls_per_pair: SURVEY.md 8(d) M_pair"
+                              f"{', c0 pruned to the result coefficients' if mm < mm_full else ''})",
                 "peak_basis": f"{SM_COUNT} SMs x {MODMUL_PER_CLK_PER_SM:.0f} Shoup modmul/clk/SM (64 FMA-heavy IMAD "
                               f"slots/clk/SM, IMAD.HI = 2 slots, measured) x {sm_max:.0f} MHz (sm_max_mhz of "
                               "MEASURED_PEAKS.json)",

@@ -155,6 +155,14 @@ int wally_encode_plaintexts_ntt(wally_ctx *ctx, const int8_t *entries_dev, void 
  * 2n (full), E4 + n (compact) or E4 + 3n/4 (compact with dropped LSBs). */
 int wally_response_words_per_plaintext(const wally_ctx *ctx, uint64_t *words_out);
 
+/* Algorithmic modular multiplications per (query, plaintext) pair of the
+ * fused kernel this context runs: 2 [L n + L (n/2) log2 n + n L(L-1)/2]
+ * (SURVEY.md §8(d) M_pair), or, for compact responses with 16 | d at
+ * n = 4096, that count with c0's inverse NTT and modulus switch pruned to
+ * the result coefficients.  Used for the
+ * roofline; pure host computation. */
+int wally_modmuls_per_pair(const wally_ctx *ctx, uint64_t *modmuls_out);
+
 /* Response layout of a batch (reading S12).
  *   cluster_of_query_host  uint32 [nq]
  *   offsets_host           uint64 [nq + 1] out: word offset of query q's responses;

@@ -411,6 +411,13 @@ extern "C" int wally_response_words_per_plaintext(const wally_ctx *c, uint64_t *
     return WALLY_OK;
 }
 
+extern "C" int wally_modmuls_per_pair(const wally_ctx *c, uint64_t *out) {
+    if (!c || !out) return WALLY_E_ARG;
+    const bool compact = c->p.resp_format != WALLY_RESP_FULL;
+    *out = modmuls_per_pair(c->p.n, c->p.num_limbs, c->p.d, pruned_c0_path(c->p.n, c->p.num_limbs, c->p.d, compact));
+    return WALLY_OK;
+}
+
 extern "C" int wally_plaintext_store_bytes(const wally_ctx *c, size_t *bytes) {
     if (!c || !bytes) return WALLY_E_ARG;
     if (!c->loaded) return fail(const_cast<wally_ctx *>(c), WALLY_E_STATE, "load_clusters first");

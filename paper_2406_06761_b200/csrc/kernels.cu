@@ -982,21 +982,24 @@ struct LimbLoopPR {
         using Gm = NttGeom<N>;
         constexpr int V = Gm::V;
         const uint32_t q = ba.kp.q[J], q2 = ba.kp.q2[J];
-        {
-            uint32_t p[16], pp[16];
-            tmem_ld<16>(tcol + 32 * J, p);
-            tmem_ld<16>(tcol + 32 * J + 16, pp);
-            tmem_wait_ld2(p, pp);
 #pragma unroll
-            for (int v = 0; v < V / 4; v++) {
-                a0[4 * v + 0] = shoup_mul(cpre[0][v].x, p[4 * v + 0], pp[4 * v + 0], q);
-                a0[4 * v + 1] = shoup_mul(cpre[0][v].y, p[4 * v + 1], pp[4 * v + 1], q);
-                a0[4 * v + 2] = shoup_mul(cpre[0][v].z, p[4 * v + 2], pp[4 * v + 2], q);
-                a0[4 * v + 3] = shoup_mul(cpre[0][v].w, p[4 * v + 3], pp[4 * v + 3], q);
-                st.a[0][4 * v + 0] = shoup_mul(cpre[1][v].x, p[4 * v + 0], pp[4 * v + 0], q);
-                st.a[0][4 * v + 1] = shoup_mul(cpre[1][v].y, p[4 * v + 1], pp[4 * v + 1], q);
-                st.a[0][4 * v + 2] = shoup_mul(cpre[1][v].z, p[4 * v + 2], pp[4 * v + 2], q);
-                st.a[0][4 * v + 3] = shoup_mul(cpre[1][v].w, p[4 * v + 3], pp[4 * v + 3], q);
+        for (int h = 0; h < 2; h++) {           // two halves of 8 values: fewer live registers
+            uint32_t p[8], pp[8];
+            tmem_ld<8>(tcol + 32 * J + 8 * h, p);
+            tmem_ld<8>(tcol + 32 * J + 16 + 8 * h, pp);
+            tmem_wait_ld<8>(p);
+            tmem_wait_ld<8>(pp);
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+                const int v = 2 * h + u;
+                a0[4 * v + 0] = shoup_mul(cpre[0][v].x, p[4 * u + 0], pp[4 * u + 0], q);
+                a0[4 * v + 1] = shoup_mul(cpre[0][v].y, p[4 * u + 1], pp[4 * u + 1], q);
+                a0[4 * v + 2] = shoup_mul(cpre[0][v].z, p[4 * u + 2], pp[4 * u + 2], q);
+                a0[4 * v + 3] = shoup_mul(cpre[0][v].w, p[4 * u + 3], pp[4 * u + 3], q);
+                st.a[0][4 * v + 0] = shoup_mul(cpre[1][v].x, p[4 * u + 0], pp[4 * u + 0], q);
+                st.a[0][4 * v + 1] = shoup_mul(cpre[1][v].y, p[4 * u + 1], pp[4 * u + 1], q);
+                st.a[0][4 * v + 2] = shoup_mul(cpre[1][v].z, p[4 * u + 2], pp[4 * u + 2], q);
+                st.a[0][4 * v + 3] = shoup_mul(cpre[1][v].w, p[4 * u + 3], pp[4 * u + 3], q);
             }
         }
         const uint32_t *nsrc = (J > 0) ? chat_q + (size_t)(J - 1) * N : (chat_next ? chat_next + (size_t)(L - 1) * N
@@ -1195,12 +1198,9 @@ static cudaError_t launch_eval_nl(const BatchArgs &a, cudaStream_t s, int num_sm
 #ifndef WALLY_EVAL_TMEM
 #define WALLY_EVAL_TMEM 1
 #endif
-#ifndef WALLY_EVAL_PRUNE
-#define WALLY_EVAL_PRUNE 1
-#endif
-    if constexpr (N == 4096 && L >= 2 && L <= 3 && WALLY_EVAL_TMEM && WALLY_EVAL_PRUNE) {
+    if constexpr (N == 4096 && L >= 2 && L <= 3 && WALLY_EVAL_TMEM) {
         // compact responses with 16 | d: pruned c0 transform (v6)
-        if (a.compact && (a.d & 15u) == 0) {
+        if (pruned_c0_path(N, L, a.d, a.compact)) {
             if (a.drop) return launch_eval_pr<L, (int)WALLY_RESP_COMPACT_DROP>(a, s, num_sms);
             return launch_eval_pr<L, (int)WALLY_RESP_COMPACT>(a, s, num_sms);
         }

@@ -87,6 +87,34 @@ struct EncodeArgs {
     uint32_t *store;              // [npt][L][2][n]
 };
 
+// Does a batch take the pruned-c0 fused kernel (kernels.cu "Fused kernel
+// v6")?  Shared by the launcher and wally_modmuls_per_pair.
+#ifndef WALLY_EVAL_PRUNE
+#define WALLY_EVAL_PRUNE 1
+#endif
+inline bool pruned_c0_path(uint32_t n, uint32_t L, uint32_t d, bool compact) {
+    return WALLY_EVAL_PRUNE && n == 4096 && L >= 2 && L <= 3 && compact && (d & 15u) == 0;
+}
+
+// Algorithmic modular multiplications per (query, plaintext) pair of the
+// fused kernel: pointwise + inverse-NTT butterflies + modulus switch for both
+// components (SURVEY.md §8(d) M_pair), with c0's transform pruned to the
+// result coefficients when pruned_c0_path() holds.
+inline uint64_t modmuls_per_pair(uint32_t n, uint32_t L, uint32_t d, bool pruned) {
+    uint32_t logn = 0;
+    while ((1u << logn) < n) logn++;
+    const uint64_t ms = (uint64_t)L * (L - 1) / 2;
+    const uint64_t full = (uint64_t)L * n + (uint64_t)L * (n / 2) * logn + (uint64_t)n * ms;
+    if (!pruned) return 2 * full;
+    uint32_t mu = 0;
+    while (mu < logn && ((d >> mu) & 1u) == 0) mu++;
+    const uint64_t M = 1ull << mu;
+    uint64_t bf = 0;
+    for (uint32_t s = 0; s < logn; s++) bf += (s < mu) ? (n >> (s + 1)) : n / (2 * M);
+    const uint64_t c0 = (uint64_t)L * n + (uint64_t)L * bf + (n / M) * ms;
+    return full + c0;
+}
+
 // Kernel launchers (kernels.cu).  Each returns the cudaError_t of the launch
 // and adds the number of kernels launched to *launches.
 cudaError_t launch_encode(const EncodeArgs &a, cudaStream_t s, uint64_t *launches);

@@ -32,7 +32,7 @@ EXPORTED = [
     "wally_ntt_forward", "wally_ntt_inverse", "wally_kernel_launches", "wally_enable_stage_timing",
     "wally_stage_times", "wally_assign_owners", "wally_route_plan", "wally_pack_queries",
     "wally_response_words_per_plaintext", "wally_assign_owners_replicated", "wally_route_plan_replicated",
-    "wally_load_clusters_replicated",
+    "wally_load_clusters_replicated", "wally_modmuls_per_pair",
 ]
 
 
@@ -91,6 +91,7 @@ def _load():
         "wally_route_plan_replicated": ([u32, P(u32), u32, P(u32), P(u64), u32, u32, u32, u32, P(u32), P(u32),
                                          P(u64), P(u64)], ctypes.c_int),
         "wally_load_clusters_replicated": ([vp, u32, P(u32), P(u64), i32], ctypes.c_int),
+        "wally_modmuls_per_pair": ([vp, P(u64)], ctypes.c_int),
         "wally_pack_queries": ([vp, u32, vp, vp, vp, vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
@@ -347,6 +348,12 @@ class WallyServer:
     def ntt_inverse(self, x_dev, out_dev, count: int, stream=None):
         _check(lib.wally_ntt_inverse(self.ctx, x_dev.data_ptr(), out_dev.data_ptr(), count, _stream(stream)),
                self.ctx)
+
+    def modmuls_per_pair(self) -> int:
+        """Algorithmic modmuls per (query, plaintext) pair of the kernel this context runs."""
+        m = ctypes.c_uint64()
+        _check(lib.wally_modmuls_per_pair(self.ctx, ctypes.byref(m)), self.ctx)
+        return m.value
 
     def kernel_launches(self) -> int:
         return int(lib.wally_kernel_launches(self.ctx))

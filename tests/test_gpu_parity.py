@@ -355,3 +355,35 @@ def test_plaintext_crt_through_cuda_path(fmt):
                 big += abs(want) > 32768
     assert big >= 2      # values a single t = 65537 cannot represent as signed integers
     srv.close()
+
+
+def _pruned_butterflies(n, d):
+    """Butterflies the pruned c0 transform needs, counted backward from its
+    outputs (every position = -1 mod 2^v2(d), a superset of the result
+    coefficients j d + d - 1): at each stage, a butterfly is needed if one of
+    its outputs is, and then both of its inputs are."""
+    mu = (d & -d).bit_length() - 1
+    need = set(i for i in range(n) if i % (1 << mu) == (1 << mu) - 1)
+    total, s = 0, n.bit_length() - 2
+    while s >= 0:
+        t = 1 << s
+        bf = set((i // (2 * t)) * 2 * t + i % t for i in need)
+        total += len(bf)
+        need = bf | set(b + t for b in bf)
+        s -= 1
+    return total
+
+
+@pytest.mark.parametrize("L,d,fmt", [(3, 192, 0), (3, 192, 1), (3, 192, 2), (2, 128, 1), (3, 100, 1), (2, 16, 2)])
+def test_modmuls_per_pair_counts(L, d, fmt):
+    n = 4096
+    srv = WallyServer(n, L, d, resp_format=fmt)
+    full = 2 * (L * n + L * (n // 2) * 12 + n * L * (L - 1) // 2)
+    got = srv.modmuls_per_pair()
+    if fmt == 0 or d % 16:
+        assert got == full
+    else:
+        mu = (d & -d).bit_length() - 1
+        c0 = L * n + L * _pruned_butterflies(n, d) + (n >> mu) * L * (L - 1) // 2
+        assert got == full // 2 + c0 and got < full
+    srv.close()
