@@ -874,22 +874,27 @@ cudaError_t launch_ntt_inverse(const KParams &kp, uint32_t n, uint32_t L, const 
 //   * c1 runs the full transform (NC = 1) of the v4 kernel, its plaintext
 //     slice and (L = 3) mod-switch state in tensor memory.
 // ---------------------------------------------------------------------------
-template <int S>
-__device__ __forceinline__ void c0_yonly_stage(uint32_t (&a)[16], const uint2 *tw0, int g, uint32_t q, uint32_t q2) {
-    using Gm = NttGeom<4096>;
-    constexpr int T = Gm::T, R = 16;
+// Pass-0 stage S of c0 keeping only the Y output of each block's last
+// butterfly.  Thread g holds the V contiguous elements of its pass-0 group;
+// twiddles from the pass-major pass-0 table (slot-pair-major), in shared
+// memory (TWS) or global memory.
+template <int N, int S, bool TWS>
+__device__ __forceinline__ void c0_yonly_stage(uint32_t (&a)[NttGeom<N>::V], const uint2 *tw0, int g, uint32_t q,
+                                               uint32_t q2) {
+    using Gm = NttGeom<N>;
+    constexpr int T = Gm::T, R = Gm::R0;
     constexpr int t = 1 << S, NB = R >> (S + 1), OFF = R - (R >> S);
     const uint4 *t4 = reinterpret_cast<const uint4 *>(tw0) + g;
     uint2 w[NB];
     if constexpr (NB >= 2) {
 #pragma unroll
         for (int b = 0; b < NB / 2; b++) {
-            const uint4 x = t4[(OFF / 2 + b) * T];
+            const uint4 x = tw_ld4<TWS>(t4 + (OFF / 2 + b) * T);
             w[2 * b] = make_uint2(x.x, x.y);
             w[2 * b + 1] = make_uint2(x.z, x.w);
         }
     } else {
-        w[0] = reinterpret_cast<const uint2 *>(t4 + (OFF / 2) * T)[OFF % 2];
+        w[0] = tw_ld2<TWS>(reinterpret_cast<const uint2 *>(t4 + (OFF / 2) * T) + (OFF % 2));
     }
 #pragma unroll
     for (int b = 0; b < NB; b++) {
@@ -898,23 +903,29 @@ __device__ __forceinline__ void c0_yonly_stage(uint32_t (&a)[16], const uint2 *t
     }
 }
 
-// Stages 8..11 of c0 on z[c] = x[16 c + 15] (shared memory), then the
-// modulus-switch step of limb J on the N/M surviving coefficients.  Warp 0
-// of the group only; lanes stride over butterflies / coefficients.  mrg =
-// the limb's merged inverse table entries 0..255, staged in shared memory
-// (stage s uses entry 2^(11-s) + block).  (A register/shuffle variant of
-// this tail measured slower: 140 vs 110 ms on c3, from register pressure.)
-// Stages 4..7 of c0 for every thread of the group: thread g holds
-// z[g] = x[16 g + 15]; stage s pairs threads g and g ^ 2^(s-4), inside a
-// warp, so one shuffle per stage.  Same pruning rule as the tail.
+template <int N, int S, bool TWS>
+struct C0Pass0 {
+    static __device__ __forceinline__ void run(uint32_t (&a)[NttGeom<N>::V], const uint2 *tw0, int g, uint32_t q,
+                                               uint32_t q2) {
+        c0_yonly_stage<N, S, TWS>(a, tw0, g, q, q2);
+        if constexpr (S + 1 < NttCfg<N>::S0) C0Pass0<N, S + 1, TWS>::run(a, tw0, g, q, q2);
+    }
+};
+
+// After pass 0 thread g keeps z[g] = x[V g + V - 1] (S_LO = log2 V).  The
+// next five stages pair threads g and g ^ 2^(s - S_LO) inside a warp, one
+// shuffle each.  mrg = the limb's merged inverse table entries 0..255
+// (stage s uses entry N/2^(s+1) + block).  Requires mu >= S_LO.
+template <int N>
 __device__ __forceinline__ uint32_t c0_mid(uint32_t y, int g, int mu, const uint2 *mrg, uint32_t q, uint32_t q2) {
-    const int Mc = 1 << (mu - 4);
+    constexpr int SLO = Log2<NttGeom<N>::V>::v;
+    const int Mc = 1 << (mu - SLO);
 #pragma unroll
-    for (int s = 4; s < 8; s++) {
-        const int D = 1 << (s - 4), m = 2048 >> s;
+    for (int s = SLO; s < SLO + 5; s++) {
+        const int D = 1 << (s - SLO), m = N >> (s + 1);
         const uint32_t other = __shfl_xor_sync(0xffffffffu, y, D);
         const bool upper = (g & D) != 0;
-        const int o = (g & (2 * D - 1)) & (D - 1);      // offset of the pair inside its block
+        const int o = g & (D - 1);                        // offset of the pair inside its block
         const uint2 w = mrg[m + g / (2 * D)];
         if (s < mu) {
             if (upper && o == D - 1) y = shoup_mul(other - y + q2, w.x, w.y, q);
@@ -925,20 +936,25 @@ __device__ __forceinline__ uint32_t c0_mid(uint32_t y, int g, int mu, const uint
     return y;
 }
 
-template <int L, int J>
+// The remaining stages S_LO + 5 .. log2 N - 1 of c0 on z[c] = x[V c + V - 1]
+// (shared memory), then the modulus-switch step of limb J on the N/M
+// surviving coefficients (state cst[k][1 + NA]).  Warp 0 only; lanes stride
+// over butterflies / coefficients.  (A variant keeping these values in
+// registers measured slower: 140 vs 110 ms on c3, from register pressure.)
+template <int N, int L, int J>
 __device__ __forceinline__ void c0_tail(uint32_t *z, uint32_t *cst, const uint2 *mrg, int lane, int mu,
                                         const KParams &kp) {
-    constexpr int N = 4096, LOGN = 12;
+    constexpr int V = NttGeom<N>::V, SLO = Log2<V>::v, LOGN = Log2<N>::v;
     constexpr int NA = (L > 2) ? (L - 2) : 1;
     const uint32_t q = kp.q[J], q2 = kp.q2[J];
-    const int M = 1 << mu;
+    const int M = 1 << mu, Mc = M >> SLO;
 #pragma unroll 1
-    for (int s = 8; s < LOGN; s++) {
+    for (int s = SLO + 5; s < LOGN; s++) {
         const int t = 1 << s, m = N / (2 * t);
         if (s < mu) {
             for (int blk = lane; blk < N / (2 * t); blk += 32) {
                 const int B = blk * 2 * t;
-                const int cx = (B + t - 16) >> 4, cy = (B + 2 * t - 16) >> 4;
+                const int cx = (B + t - V) >> SLO, cy = (B + 2 * t - V) >> SLO;
                 const uint2 w = mrg[m + blk];
                 z[cy] = shoup_mul(z[cx] - z[cy] + q2, w.x, w.y, q);
             }
@@ -947,7 +963,7 @@ __device__ __forceinline__ void c0_tail(uint32_t *z, uint32_t *cst, const uint2 
             for (int i = lane; i < N / (2 * M); i += 32) {
                 const int blk = i / per, o = M - 1 + (i % per) * M;
                 const int B = blk * 2 * t;
-                const int cx = (B + o - 15) >> 4, cy = (B + o + t - 15) >> 4;
+                const int cx = (B + o - (V - 1)) >> SLO, cy = (B + o + t - (V - 1)) >> SLO;
                 const uint2 w = mrg[m + blk];
                 const uint32_t X = z[cx], Y = z[cy];
                 z[cx] = csub(X + Y, q2);
@@ -956,9 +972,8 @@ __device__ __forceinline__ void c0_tail(uint32_t *z, uint32_t *cst, const uint2 
         }
         __syncwarp();
     }
-    // modulus switch of the coefficients k M + M - 1 (state [k][1 + NA] words)
     for (int k = lane; k < N / M; k += 32) {
-        const int c = k * (M >> 4) + (M >> 4) - 1;
+        const int c = k * Mc + Mc - 1;
         uint32_t x = z[c], rtop = cst[k * (1 + NA)], acc[NA];
 #pragma unroll
         for (int l = 0; l < NA; l++) acc[l] = cst[k * (1 + NA) + 1 + l];
@@ -969,6 +984,20 @@ __device__ __forceinline__ void c0_tail(uint32_t *z, uint32_t *cst, const uint2 
         z[c] = x;
     }
     __syncwarp();
+}
+
+// c0 result words of one pair from the survivors of limb 0 (warp 0).
+template <int N>
+__device__ __forceinline__ void c0_write_results(const BatchArgs &ba, uint32_t *out_q, const uint32_t *z, int lane,
+                                                 int mu) {
+    constexpr int SLO = Log2<NttGeom<N>::V>::v;
+    const int M = 1 << mu, Mc = M >> SLO;
+    for (int kk = lane; kk < N / M; kk += 32) {
+        const uint32_t pos1 = (uint32_t)(kk * M + M);
+        if (pos1 % ba.d == 0) __stcs(out_q + pos1 / ba.d - 1, z[kk * Mc + Mc - 1]);
+    }
+    const uint32_t e4 = (ba.E + 3) & ~3u;
+    if ((uint32_t)lane < e4 - ba.E) __stcs(out_q + ba.E + lane, 0u);
 }
 
 template <int L, int J>
@@ -1013,15 +1042,12 @@ struct LimbLoopPR {
         }
         // c0: pass 0 keeping the last Y output of each block -> one value per thread
         const uint2 *twJ = cx.tw + (size_t)J * Gm::TW_LIMB;
-        c0_yonly_stage<0>(a0, twJ, g, q, q2);
-        c0_yonly_stage<1>(a0, twJ, g, q, q2);
-        c0_yonly_stage<2>(a0, twJ, g, q, q2);
-        c0_yonly_stage<3>(a0, twJ, g, q, q2);
+        C0Pass0<N, 0, true>::run(a0, twJ, g, q, q2);
         uint32_t *z = ybuf + par * Gm::T;
-        z[g] = c0_mid(a0[15], g, mu, s_mrg + J * 256, q, q2);
+        z[g] = c0_mid<N>(a0[15], g, mu, s_mrg + J * 256, q, q2);
         // c1: full transform (its group barriers also publish z)
         intt_chain_group<N, 1>(st.a, twJ, g, q, q2, cx.bufA, cx.bar);
-        if (g < 32) c0_tail<L, J>(z, cst, s_mrg + J * 256, g, mu, ba.kp);
+        if (g < 32) c0_tail<N, L, J>(z, cst, s_mrg + J * 256, g, mu, ba.kp);
         par ^= 1u;
         if constexpr (L == 3) {
             if constexpr (J < L - 1) {
@@ -1093,16 +1119,7 @@ __device__ __forceinline__ void eval_item_pr(const BatchArgs &ba, const ItemCurs
         EvalState<N, L, 1> st;
         uint32_t a0[16];
         LimbLoopPR<L, L - 1>::run(st, a0, cpre, ba, chat_q, chat_next, tcol, g, cx, ybuf, par, cst, mu, s_mrg);
-        // c0 results: coefficient k M + M - 1 is result j when (k M + M) = (j + 1) d
-        if (g < 32) {
-            const uint32_t *z = ybuf + (par ^ 1u) * Gm::T;  // the buffer limb 0 used
-            for (int kk = g; kk < N / M; kk += 32) {
-                const uint32_t pos1 = (uint32_t)(kk * M + M);
-                if (pos1 % ba.d == 0) __stcs(out_q + pos1 / ba.d - 1, z[kk * (M >> 4) + (M >> 4) - 1]);
-            }
-            const uint32_t e4 = (ba.E + 3) & ~3u;
-            if ((uint32_t)g < e4 - ba.E) __stcs(out_q + ba.E + g, 0u);
-        }
+        if (g < 32) c0_write_results<N>(ba, out_q, ybuf + (par ^ 1u) * Gm::T, g, mu);  // buffer of limb 0
         write_component<N, FMT>(ba, out_q, st.a[0], 1, g, s_rmap);
         qo = qn;
     }
@@ -1174,6 +1191,101 @@ static cudaError_t launch_eval_pr(const BatchArgs &a, cudaStream_t s, int num_sm
     return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------------------
+// n = 8192 with compact responses and 32 | d (c4): the whole-CTA kernel with
+// c0's transform pruned as in v6 (pass 0 on V = 32 values per thread, five
+// shuffle stages, the rest on warp 0); c1 unchanged.
+// ---------------------------------------------------------------------------
+template <int L, int J>
+struct LimbLoopP8 {
+    static constexpr int N = 8192;
+    static __device__ __forceinline__ void run(uint32_t (&a)[NttGeom<N>::V], const BatchArgs &ba,
+                                               const uint32_t *chat0, const uint32_t *phat, int g, uint32_t *ybuf,
+                                               uint32_t &par, uint32_t *cst, int mu, const uint2 *s_mrg) {
+        using Gm = NttGeom<N>;
+        constexpr int V = Gm::V;
+        const uint32_t q = ba.kp.q[J], q2 = ba.kp.q2[J];
+        const uint32_t *pv = phat + (size_t)J * 2 * N + (size_t)g * V;
+        const uint32_t *cv = chat0 + (size_t)J * N + (size_t)g * V;
+#pragma unroll
+        for (int v = 0; v < V / 4; v++) {
+            const uint4 p = ldg_stream(pv + 4 * v), pp = ldg_stream(pv + N + 4 * v), x = ldg_stream(cv + 4 * v);
+            a[4 * v + 0] = shoup_mul(x.x, p.x, pp.x, q);
+            a[4 * v + 1] = shoup_mul(x.y, p.y, pp.y, q);
+            a[4 * v + 2] = shoup_mul(x.z, p.z, pp.z, q);
+            a[4 * v + 3] = shoup_mul(x.w, p.w, pp.w, q);
+        }
+        C0Pass0<N, 0, false>::run(a, ba.tw_inv + (size_t)J * Gm::TW_LIMB, g, q, q2);
+        uint32_t *z = ybuf + par * Gm::T;
+        z[g] = c0_mid<N>(a[V - 1], g, mu, s_mrg + J * 256, q, q2);
+        __syncthreads();
+        if (g < 32) c0_tail<N, L, J>(z, cst, s_mrg + J * 256, g, mu, ba.kp);
+        par ^= 1u;
+        if constexpr (J > 0) LimbLoopP8<L, J - 1>::run(a, ba, chat0, phat, g, ybuf, par, cst, mu, s_mrg);
+    }
+};
+
+template <int L, int FMT>
+__global__ void __launch_bounds__(NttGeom<8192>::T, 1) eval_kernel_p8(BatchArgs ba) {
+    constexpr int N = 8192;
+    using Gm = NttGeom<N>;
+    constexpr int NA = (L > 2) ? (L - 2) : 1;
+    extern __shared__ uint32_t smem[];
+    ChainCtx cx{ba.tw_inv, smem, smem + Gm::SMEM_WORDS, 0};
+    __shared__ uint32_t s_item[2];
+    __shared__ uint32_t s_rmap[ResultMap<N>::WORDS];
+    __shared__ uint32_t s_ybuf[2 * Gm::T];
+    __shared__ uint32_t s_cst[(N / 32) * (1 + NA)];
+    __shared__ uint2 s_mrg[L * 256];
+    for (int i = threadIdx.x; i < L * 256; i += blockDim.x) s_mrg[i] = __ldg(ba.tw_mrg + (size_t)(i >> 8) * N + (i & 255));
+    const int g = threadIdx.x;
+    const int mu = min(__ffs((int)ba.d) - 1, 13);
+    const uint32_t total = ba.misc[kMiscTotalItems];
+    uint32_t par = 0;
+    ItemCursor cur;
+    for (uint32_t it = 0;; it++) {
+        if (g == 0) s_item[it & 1] = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
+        __syncthreads();
+        const uint32_t item = s_item[it & 1];
+        if (item >= total) break;
+        cur.seek(ba, item);
+        const uint32_t li = cur.li;
+        const uint32_t cnt = ba.counts[li];
+        const uint32_t P = ba.n_pt[li];
+        const uint32_t ch = (item - cur.b) / P, k = (item - cur.b) % P;
+        const uint32_t qb = ba.seg[li] + ch * kQueryChunk;
+        const uint32_t qe = min(qb + kQueryChunk, ba.seg[li] + cnt);
+        const uint32_t *phat = ba.store + (size_t)(ba.pt_base[li] + k) * L * 2 * N;
+        for (uint32_t qi = qb; qi < qe; qi++) {
+            const uint32_t qo = ba.perm[qi];
+            uint32_t *out_q = ba.resp + ba.resp_off[qo] + (size_t)k * ba.wpp;
+            const uint32_t *chat_q = ba.chat + (size_t)qo * 2 * L * N;
+            {
+                uint32_t a[Gm::V];
+                LimbLoopP8<L, L - 1>::run(a, ba, chat_q, phat, g, s_ybuf, par, s_cst, mu, s_mrg);
+                if (g < 32) c0_write_results<N>(ba, out_q, s_ybuf + (par ^ 1u) * Gm::T, g, mu);
+            }
+            EvalState<N, L, 1> st;
+            LimbLoop<N, L, 1, L - 1, false>::run(st, ba, chat_q, 1, phat, g, cx);
+            write_component<N, FMT>(ba, out_q, st.a[0], 1, g, s_rmap);
+        }
+    }
+}
+
+template <int L, int FMT>
+static cudaError_t launch_eval_p8(const BatchArgs &a, cudaStream_t s, int num_sms) {
+    static bool configured = false;
+    const size_t smem = chain_smem<8192>(1);
+    if (!configured) {
+        cudaError_t e = allow_smem(eval_kernel_p8<L, FMT>, smem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    eval_kernel_p8<L, FMT><<<num_sms, NttGeom<8192>::T, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
 template <int N, int L, int FMT>
 static cudaError_t launch_eval_tm(const BatchArgs &a, cudaStream_t s, int num_sms) {
     using Gm = NttGeom<N>;
@@ -1223,6 +1335,9 @@ static cudaError_t launch_eval_nl(const BatchArgs &a, cudaStream_t s, int num_sm
         }
         eval_kernel_grp<N, L><<<num_sms * blocks_per_sm, kEvalGroups * Gm::T, smem, s>>>(a);
     } else {
+        if constexpr (N == 8192 && WALLY_EVAL_TMEM) {
+            if (pruned_c0_path(N, L, a.d, a.compact)) return launch_eval_p8<L, (int)WALLY_RESP_COMPACT>(a, s, num_sms);
+        }
         const size_t smem = chain_smem<N>(EvalCfg<N>::NC);
         if (!configured) {
             cudaError_t e = allow_smem(eval_kernel<N, L>, smem);

@@ -93,7 +93,10 @@ struct EncodeArgs {
 #define WALLY_EVAL_PRUNE 1
 #endif
 inline bool pruned_c0_path(uint32_t n, uint32_t L, uint32_t d, bool compact) {
-    return WALLY_EVAL_PRUNE && n == 4096 && L >= 2 && L <= 3 && compact && (d & 15u) == 0;
+    if (!WALLY_EVAL_PRUNE || !compact) return false;
+    if (n == 4096) return L >= 2 && L <= 3 && (d & 15u) == 0;   // v6 (two groups, TMEM)
+    if (n == 8192) return (d & 31u) == 0;                      // whole-CTA kernel (c4)
+    return false;
 }
 
 // Algorithmic modular multiplications per (query, plaintext) pair of the
