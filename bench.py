@@ -469,8 +469,10 @@ def run_reference(args):
     P = -(-w.cluster_size // E)
     cores = len(os.sched_getaffinity(0))
     rng = np.random.default_rng(11)
-    # one fixed sample of pairs per step, sized for ~ a few seconds of oracle work
-    npairs = max(cores, 2 * cores)
+    # one fixed sample of pairs per step, sized for ~3 s of oracle work: the plain
+    # oracle takes ~11 ms per c3 pair per core (profiles/r01_bench_c3_final.json cpu_baseline)
+    per_core = {"c1": 400, "c2": 270, "c3": 270, "c4": 90, "c5": 400}.get(w.name, 200)
+    npairs = max(cores, per_core * cores)
     qsel = rng.integers(0, ids.size, size=npairs)
     ksel = rng.integers(0, P, size=npairs)
     uq, inv = np.unique(qsel, return_inverse=True)
