@@ -1000,6 +1000,56 @@ __device__ __forceinline__ void c0_write_results(const BatchArgs &ba, uint32_t *
     if ((uint32_t)lane < e4 - ba.E) __stcs(out_q + ba.E + lane, 0u);
 }
 
+// Register tail for n = 4096 and mu = 6 (c3: d = 192) or mu = 7 (d = 128:
+// c1, c2, c5): after stage 8 the survivors are c = k Mc + Mc - 1 (Mc = M/16),
+// 64 or 32 of them; lane l holds k = l (and k = l + 32 for mu = 6), so
+// stages 9..11 are lane shuffles (and, for mu = 6, one lane-local pair), and
+// the modulus switch runs on the lane's one or two values.
+template <int L, int J>
+__device__ __forceinline__ void c0_tail_fast(uint32_t *z, uint32_t *cst, const uint2 *mrg, int lane, int mu,
+                                             const KParams &kp) {
+    constexpr int NA = (L > 2) ? (L - 2) : 1;
+    const uint32_t q = kp.q[J], q2 = kp.q2[J];
+    auto ms = [&](uint32_t &x, int k) {
+        uint32_t rtop = cst[k * (1 + NA)], acc[NA];
+#pragma unroll
+        for (int l = 0; l < NA; l++) acc[l] = cst[k * (1 + NA) + 1 + l];
+        ms_elem<L, J, NA>(x, rtop, acc, kp);
+        cst[k * (1 + NA)] = rtop;
+#pragma unroll
+        for (int l = 0; l < NA; l++) cst[k * (1 + NA) + 1 + l] = acc[l];
+    };
+    auto bfly = [&](uint32_t &v, int xo, const uint2 w) {
+        const uint32_t other = __shfl_xor_sync(0xffffffffu, v, xo);
+        v = (lane & xo) ? shoup_mul(other - v + q2, w.x, w.y, q) : csub(v + other, q2);
+    };
+    if (mu == 6) {
+        uint32_t v0 = z[4 * lane + 3], v1 = z[4 * lane + 131];
+        bfly(v0, 8, mrg[4 + lane / 16]);
+        bfly(v1, 8, mrg[4 + (lane + 32) / 16]);
+        bfly(v0, 16, mrg[2 + lane / 32]);
+        bfly(v1, 16, mrg[2 + (lane + 32) / 32]);
+        {
+            const uint2 w = mrg[1];
+            const uint32_t X = v0, Y = v1;
+            v0 = csub(X + Y, q2);
+            v1 = shoup_mul(X - Y + q2, w.x, w.y, q);
+        }
+        ms(v0, lane);
+        ms(v1, lane + 32);
+        z[4 * lane + 3] = v0;
+        z[4 * lane + 131] = v1;
+    } else {  // mu == 7
+        uint32_t v = z[8 * lane + 7];
+        bfly(v, 4, mrg[4 + lane / 8]);
+        bfly(v, 8, mrg[2 + lane / 16]);
+        bfly(v, 16, mrg[1]);
+        ms(v, lane);
+        z[8 * lane + 7] = v;
+    }
+    __syncwarp();
+}
+
 template <int L, int J>
 struct LimbLoopPR {
     static constexpr int N = 4096;
@@ -1047,7 +1097,10 @@ struct LimbLoopPR {
         z[g] = c0_mid<N>(a0[15], g, mu, s_mrg + J * 256, q, q2);
         // c1: full transform (its group barriers also publish z)
         intt_chain_group<N, 1>(st.a, twJ, g, q, q2, cx.bufA, cx.bar);
-        if (g < 32) c0_tail<N, L, J>(z, cst, s_mrg + J * 256, g, mu, ba.kp);
+        if (g < 32) {
+            if (mu == 6 || mu == 7) c0_tail_fast<L, J>(z, cst, s_mrg + J * 256, g, mu, ba.kp);
+            else c0_tail<N, L, J>(z, cst, s_mrg + J * 256, g, mu, ba.kp);
+        }
         par ^= 1u;
         if constexpr (L == 3) {
             if constexpr (J < L - 1) {
@@ -1220,7 +1273,10 @@ struct LimbLoopP8 {
         uint32_t *z = ybuf + par * Gm::T;
         z[g] = c0_mid<N>(a[V - 1], g, mu, s_mrg + J * 256, q, q2);
         __syncthreads();
-        if (g < 32) c0_tail<N, L, J>(z, cst, s_mrg + J * 256, g, mu, ba.kp);
+        if (g < 32) {
+            if (mu == 6 || mu == 7) c0_tail_fast<L, J>(z, cst, s_mrg + J * 256, g, mu, ba.kp);
+            else c0_tail<N, L, J>(z, cst, s_mrg + J * 256, g, mu, ba.kp);
+        }
         par ^= 1u;
         if constexpr (J > 0) LimbLoopP8<L, J - 1>::run(a, ba, chat0, phat, g, ybuf, par, cst, mu, s_mrg);
     }
