@@ -916,6 +916,23 @@ struct C0Pass0 {
 // next five stages pair threads g and g ^ 2^(s - S_LO) inside a warp, one
 // shuffle each.  mrg = the limb's merged inverse table entries 0..255
 // (stage s uses entry N/2^(s+1) + block).  Requires mu >= S_LO.
+template <int N, int S>
+__device__ __forceinline__ uint32_t c0_mid_stage(uint32_t y, int g, int mu, const uint2 *mrg, uint32_t q, uint32_t q2) {
+    constexpr int SLO = Log2<NttGeom<N>::V>::v;
+    const int Mc = 1 << (mu - SLO);
+    constexpr int D = 1 << (S - SLO), m = N >> (S + 1);
+    const uint32_t other = __shfl_xor_sync(0xffffffffu, y, D);
+    const bool upper = (g & D) != 0;
+    const int o = g & (D - 1);
+    const uint2 w = mrg[m + g / (2 * D)];
+    if (S < mu) {
+        if (upper && o == D - 1) y = shoup_mul(other - y + q2, w.x, w.y, q);
+    } else if (((o + 1) & (Mc - 1)) == 0) {
+        y = upper ? shoup_mul(other - y + q2, w.x, w.y, q) : csub(y + other, q2);
+    }
+    return y;
+}
+
 template <int N>
 __device__ __forceinline__ uint32_t c0_mid(uint32_t y, int g, int mu, const uint2 *mrg, uint32_t q, uint32_t q2) {
     constexpr int SLO = Log2<NttGeom<N>::V>::v;
@@ -1092,11 +1109,25 @@ struct LimbLoopPR {
         }
         // c0: pass 0 keeping the last Y output of each block -> one value per thread
         const uint2 *twJ = cx.tw + (size_t)J * Gm::TW_LIMB;
+        // c0's pass 0 (Y outputs only), then c1's pass 0 stage by stage with
+        // c0's shuffle stages 4..7 interleaved: the shuffle chain is latency
+        // bound, c1's register-local butterflies fill the gaps
         C0Pass0<N, 0, true>::run(a0, twJ, g, q, q2);
+        const uint2 *mrgJ = s_mrg + J * 256;
+        uint32_t y = a0[15];
+        ntt_stage<N, Gm::TB0, Gm::R0, 0, true, 1, true>(st.a, twJ, g, q, q2);
+        y = c0_mid_stage<N, 4>(y, g, mu, mrgJ, q, q2);
+        ntt_stage<N, Gm::TB0, Gm::R0, 1, true, 1, true>(st.a, twJ, g, q, q2);
+        y = c0_mid_stage<N, 5>(y, g, mu, mrgJ, q, q2);
+        ntt_stage<N, Gm::TB0, Gm::R0, 2, true, 1, true>(st.a, twJ, g, q, q2);
+        y = c0_mid_stage<N, 6>(y, g, mu, mrgJ, q, q2);
+        ntt_stage<N, Gm::TB0, Gm::R0, 3, true, 1, true>(st.a, twJ, g, q, q2);
+        y = c0_mid_stage<N, 7>(y, g, mu, mrgJ, q, q2);
+        y = c0_mid_stage<N, 8>(y, g, mu, mrgJ, q, q2);
         uint32_t *z = ybuf + par * Gm::T;
-        z[g] = c0_mid<N>(a0[15], g, mu, s_mrg + J * 256, q, q2);
-        // c1: full transform (its group barriers also publish z)
-        intt_chain_group<N, 1>(st.a, twJ, g, q, q2, cx.bufA, cx.bar);
+        z[g] = y;
+        // the rest of c1's transform (its group barriers also publish z)
+        intt_chain_group_tail<N, 1>(st.a, twJ, g, q, q2, cx.bufA, cx.bar);
         if (g < 32) {
             if (mu == 6 || mu == 7) c0_tail_fast<L, J>(z, cst, s_mrg + J * 256, g, mu, ba.kp);
             else c0_tail<N, L, J>(z, cst, s_mrg + J * 256, g, mu, ba.kp);

@@ -295,6 +295,24 @@ __device__ __forceinline__ void intt_chain_group(uint32_t (&a)[NC][NttGeom<N>::V
     ntt_pass<N, Gm::TB2, Gm::R2, true, NC, true>(a, tw_smem + Gm::TW2, g, q, q2);
 }
 
+// intt_chain_group without its pass 0 (the caller ran it, e.g. interleaved
+// with other work): the two exchanges and passes 1 and 2.
+template <int N, int NC>
+__device__ __forceinline__ void intt_chain_group_tail(uint32_t (&a)[NC][NttGeom<N>::V], const uint2 *tw_smem, int g,
+                                                      uint32_t q, uint32_t q2, uint32_t *buf, int bar_id) {
+    using Gm = NttGeom<N>;
+    group_sync(bar_id, Gm::T);
+    smem_store<N, Gm::TB0, Gm::R0, NC, 0>(buf, a, g);
+    if constexpr (Gm::A_IN_WARP) __syncwarp(); else group_sync(bar_id, Gm::T);
+    smem_load<N, Gm::TB1, Gm::R1, NC, 0>(buf, a, g);
+    ntt_pass<N, Gm::TB1, Gm::R1, true, NC, true>(a, tw_smem + Gm::TW1, g, q, q2);
+    if constexpr (Gm::A_IN_WARP) __syncwarp(); else group_sync(bar_id, Gm::T);
+    smem_store<N, Gm::TB1, Gm::R1, NC, 1>(buf, a, g);
+    group_sync(bar_id, Gm::T);
+    smem_load<N, Gm::TB2, Gm::R2, NC, 1>(buf, a, g);
+    ntt_pass<N, Gm::TB2, Gm::R2, true, NC, true>(a, tw_smem + Gm::TW2, g, q, q2);
+}
+
 // Whole forward transform: on entry the thread owns pass-2 groups, on exit
 // pass-0 groups (contiguous V elements, bit-reversed NTT order).
 template <int N, int NC>
