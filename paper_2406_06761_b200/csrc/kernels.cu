@@ -1281,6 +1281,36 @@ static cudaError_t launch_eval_pr(const BatchArgs &a, cudaStream_t s, int num_sm
 // c0's transform pruned as in v6 (pass 0 on V = 32 values per thread, five
 // shuffle stages, the rest on warp 0); c1 unchanged.
 // ---------------------------------------------------------------------------
+// Register tail for n = 8192 and mu = 9 (c4: d = 512): after stage 9 the
+// survivors are positions 512 k + 511, c = 16 k + 15 (k < 16); lanes 0..15
+// hold one each, and stages 10..12 pair k with k ^ 2, k ^ 4, k ^ 8.
+template <int L, int J>
+__device__ __forceinline__ void c0_tail_fast8(uint32_t *z, uint32_t *cst, const uint2 *mrg, int lane,
+                                              const KParams &kp) {
+    constexpr int NA = (L > 2) ? (L - 2) : 1;
+    const uint32_t q = kp.q[J], q2 = kp.q2[J];
+    const int k = lane & 15;
+    uint32_t v = z[16 * k + 15];
+    auto bfly = [&](int xo, const uint2 w) {
+        const uint32_t other = __shfl_xor_sync(0xffffffffu, v, xo);
+        v = (k & xo) ? shoup_mul(other - v + q2, w.x, w.y, q) : csub(v + other, q2);
+    };
+    bfly(2, mrg[4 + k / 4]);     // stage 10: survivors 512 k + 511 pair with k ^ 2, block p / 2048
+    bfly(4, mrg[2 + k / 8]);     // stage 11: k ^ 4, block p / 4096
+    bfly(8, mrg[1]);             // stage 12: k ^ 8, one block
+    if (lane < 16) {
+        uint32_t rtop = cst[k * (1 + NA)], acc[NA];
+#pragma unroll
+        for (int l = 0; l < NA; l++) acc[l] = cst[k * (1 + NA) + 1 + l];
+        ms_elem<L, J, NA>(v, rtop, acc, kp);
+        cst[k * (1 + NA)] = rtop;
+#pragma unroll
+        for (int l = 0; l < NA; l++) cst[k * (1 + NA) + 1 + l] = acc[l];
+        z[16 * k + 15] = v;
+    }
+    __syncwarp();
+}
+
 template <int L, int J>
 struct LimbLoopP8 {
     static constexpr int N = 8192;
