@@ -1126,8 +1126,9 @@ struct LimbLoopPR {
         y = c0_mid_stage<N, 8>(y, g, mu, mrgJ, q, q2);
         uint32_t *z = ybuf + par * Gm::T;
         z[g] = y;
-        // the rest of c1's transform (its group barriers also publish z)
-        intt_chain_group_tail<N, 1>(st.a, twJ, g, q, q2, cx.bufA, cx.bar);
+        // the rest of c1's transform (its group barrier also publishes z); the
+        // exchange buffer alternates with the limb parity
+        intt_chain_group_tail<N, 1, true>(st.a, twJ, g, q, q2, cx.bufA + par * Gm::SMEM_WORDS, cx.bar);
         if (g < 32) {
             if (mu == 6 || mu == 7) c0_tail_fast<L, J>(z, cst, s_mrg + J * 256, g, mu, ba.kp);
             else c0_tail<N, L, J>(z, cst, s_mrg + J * 256, g, mu, ba.kp);
@@ -1242,7 +1243,7 @@ __global__ void __launch_bounds__(kEvalGroups * NttGeom<4096>::T, 1) eval_kernel
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tcol = s_taddr + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 128);
-    const ChainCtx cx{tw, xbuf + grp * Gm::SMEM_WORDS, nullptr, 1 + grp};
+    const ChainCtx cx{tw, xbuf + grp * 2 * Gm::SMEM_WORDS, nullptr, 1 + grp};
     const int mu = min(__ffs((int)ba.d) - 1, 12);
     const uint32_t total = ba.misc[kMiscTotalItems];
     uint32_t par = 0;
@@ -1265,7 +1266,8 @@ template <int L, int FMT>
 static cudaError_t launch_eval_pr(const BatchArgs &a, cudaStream_t s, int num_sms) {
     using Gm = NttGeom<4096>;
     static bool configured = false;
-    const size_t smem = (size_t)L * Gm::TW_LIMB * sizeof(uint2) + (size_t)kEvalGroups * Gm::SMEM_WORDS * sizeof(uint32_t);
+    const size_t smem =
+        (size_t)L * Gm::TW_LIMB * sizeof(uint2) + (size_t)kEvalGroups * 2 * Gm::SMEM_WORDS * sizeof(uint32_t);
     if (!configured) {
         cudaError_t e = allow_smem(eval_kernel_pr<L, FMT>, smem);
         if (e != cudaSuccess) return e;

@@ -296,12 +296,15 @@ __device__ __forceinline__ void intt_chain_group(uint32_t (&a)[NC][NttGeom<N>::V
 }
 
 // intt_chain_group without its pass 0 (the caller ran it, e.g. interleaved
-// with other work): the two exchanges and passes 1 and 2.
-template <int N, int NC>
+// with other work): the two exchanges and passes 1 and 2.  FRESH_BUF: the
+// caller alternates exchange buffers between consecutive calls, so the
+// barrier protecting the buffer against the previous call's reads is not
+// needed (the call before the previous one ended with a group barrier).
+template <int N, int NC, bool FRESH_BUF = false>
 __device__ __forceinline__ void intt_chain_group_tail(uint32_t (&a)[NC][NttGeom<N>::V], const uint2 *tw_smem, int g,
                                                       uint32_t q, uint32_t q2, uint32_t *buf, int bar_id) {
     using Gm = NttGeom<N>;
-    group_sync(bar_id, Gm::T);
+    if constexpr (!FRESH_BUF || !Gm::A_IN_WARP) group_sync(bar_id, Gm::T);
     smem_store<N, Gm::TB0, Gm::R0, NC, 0>(buf, a, g);
     if constexpr (Gm::A_IN_WARP) __syncwarp(); else group_sync(bar_id, Gm::T);
     smem_load<N, Gm::TB1, Gm::R1, NC, 0>(buf, a, g);
