@@ -1067,6 +1067,35 @@ __device__ __forceinline__ void c0_tail_fast(uint32_t *z, uint32_t *cst, const u
     __syncwarp();
 }
 
+// Pass-0 stage S for both components of v6: the twiddles are loaded once;
+// c1 gets full GS butterflies, c0 only the Y output of each block's last one.
+template <int S>
+__device__ __forceinline__ void pass0_stage_both(uint32_t (&a0)[16], uint32_t (&a1)[1][16], const uint2 *tw0, int g,
+                                                 uint32_t q, uint32_t q2) {
+    using Gm = NttGeom<4096>;
+    constexpr int T = Gm::T, R = 16;
+    constexpr int t = 1 << S, NB = R >> (S + 1), OFF = R - (R >> S);
+    const uint4 *t4 = reinterpret_cast<const uint4 *>(tw0) + g;
+    uint2 w[NB];
+    if constexpr (NB >= 2) {
+#pragma unroll
+        for (int b = 0; b < NB / 2; b++) {
+            const uint4 x = t4[(OFF / 2 + b) * T];
+            w[2 * b] = make_uint2(x.x, x.y);
+            w[2 * b + 1] = make_uint2(x.z, x.w);
+        }
+    } else {
+        w[0] = reinterpret_cast<const uint2 *>(t4 + (OFF / 2) * T)[OFF % 2];
+    }
+#pragma unroll
+    for (int b = 0; b < NB; b++) {
+#pragma unroll
+        for (int kk = 0; kk < t; kk++) gs_bfly(a1[0][b * 2 * t + kk], a1[0][b * 2 * t + kk + t], w[b].x, w[b].y, q, q2);
+        const uint32_t X = a0[b * 2 * t + t - 1], Y = a0[b * 2 * t + 2 * t - 1];
+        a0[b * 2 * t + 2 * t - 1] = shoup_mul(X - Y + q2, w[b].x, w[b].y, q);
+    }
+}
+
 template <int L, int J>
 struct LimbLoopPR {
     static constexpr int N = 4096;
@@ -1109,26 +1138,40 @@ struct LimbLoopPR {
         }
         // c0: pass 0 keeping the last Y output of each block -> one value per thread
         const uint2 *twJ = cx.tw + (size_t)J * Gm::TW_LIMB;
-        // c0's pass 0 (Y outputs only), then c1's pass 0 stage by stage with
-        // c0's shuffle stages 4..7 interleaved: the shuffle chain is latency
-        // bound, c1's register-local butterflies fill the gaps
-        C0Pass0<N, 0, true>::run(a0, twJ, g, q, q2);
+        // pass 0 of both components (twiddles loaded once; c0 keeps only the Y
+        // output of each block's last butterfly), c1's first (intra-warp)
+        // exchange, then c1's pass 1 stage by stage with c0's shuffle stages
+        // interleaved (the shuffle chain is latency bound, c1's butterflies fill
+        // the gaps), c1's second exchange and pass 2.  The exchange buffer
+        // alternates with the limb parity (no write-after-read barrier).
+        pass0_stage_both<0>(a0, st.a, twJ, g, q, q2);
+        pass0_stage_both<1>(a0, st.a, twJ, g, q, q2);
+        pass0_stage_both<2>(a0, st.a, twJ, g, q, q2);
+        pass0_stage_both<3>(a0, st.a, twJ, g, q, q2);
+        uint32_t *buf = cx.bufA + par * Gm::SMEM_WORDS;
+        static_assert(Gm::A_IN_WARP, "v6 assumes the first exchange stays inside a warp");
+        smem_store<N, Gm::TB0, Gm::R0, 1, 0>(buf, st.a, g);
+        __syncwarp();
+        smem_load<N, Gm::TB1, Gm::R1, 1, 0>(buf, st.a, g);
         const uint2 *mrgJ = s_mrg + J * 256;
+        const uint2 *tw1 = twJ + Gm::TW1;
         uint32_t y = a0[15];
-        ntt_stage<N, Gm::TB0, Gm::R0, 0, true, 1, true>(st.a, twJ, g, q, q2);
+        ntt_stage<N, Gm::TB1, Gm::R1, 0, true, 1, true>(st.a, tw1, g, q, q2);
         y = c0_mid_stage<N, 4>(y, g, mu, mrgJ, q, q2);
-        ntt_stage<N, Gm::TB0, Gm::R0, 1, true, 1, true>(st.a, twJ, g, q, q2);
+        ntt_stage<N, Gm::TB1, Gm::R1, 1, true, 1, true>(st.a, tw1, g, q, q2);
         y = c0_mid_stage<N, 5>(y, g, mu, mrgJ, q, q2);
-        ntt_stage<N, Gm::TB0, Gm::R0, 2, true, 1, true>(st.a, twJ, g, q, q2);
+        ntt_stage<N, Gm::TB1, Gm::R1, 2, true, 1, true>(st.a, tw1, g, q, q2);
         y = c0_mid_stage<N, 6>(y, g, mu, mrgJ, q, q2);
-        ntt_stage<N, Gm::TB0, Gm::R0, 3, true, 1, true>(st.a, twJ, g, q, q2);
+        ntt_stage<N, Gm::TB1, Gm::R1, 3, true, 1, true>(st.a, tw1, g, q, q2);
         y = c0_mid_stage<N, 7>(y, g, mu, mrgJ, q, q2);
         y = c0_mid_stage<N, 8>(y, g, mu, mrgJ, q, q2);
         uint32_t *z = ybuf + par * Gm::T;
         z[g] = y;
-        // the rest of c1's transform (its group barrier also publishes z); the
-        // exchange buffer alternates with the limb parity
-        intt_chain_group_tail<N, 1, true>(st.a, twJ, g, q, q2, cx.bufA + par * Gm::SMEM_WORDS, cx.bar);
+        __syncwarp();
+        smem_store<N, Gm::TB1, Gm::R1, 1, 1>(buf, st.a, g);
+        group_sync(cx.bar, Gm::T);             // also publishes z to warp 0
+        smem_load<N, Gm::TB2, Gm::R2, 1, 1>(buf, st.a, g);
+        ntt_pass<N, Gm::TB2, Gm::R2, true, 1, true>(st.a, twJ + Gm::TW2, g, q, q2);
         if (g < 32) {
             if (mu == 6 || mu == 7) c0_tail_fast<L, J>(z, cst, s_mrg + J * 256, g, mu, ba.kp);
             else c0_tail<N, L, J>(z, cst, s_mrg + J * 256, g, mu, ba.kp);
