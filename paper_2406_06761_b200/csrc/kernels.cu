@@ -1238,7 +1238,6 @@ __device__ __forceinline__ void eval_item_pr(const BatchArgs &ba, const ItemCurs
 #pragma unroll
             for (int v = 0; v < V / 4; v++) cpre[c][v] = ldg_stream(src + (size_t)c * L * N + (size_t)g * V + 4 * v);
     }
-    const int M = 1 << mu;
     for (uint32_t qi = qb; qi < qe; qi++) {
         const uint32_t qn = (qi + 1 < qe) ? ba.perm[qi + 1] : 0xffffffffu;
         uint32_t *out_q = ba.resp + ba.resp_off[qo] + (size_t)k * ba.wpp;
@@ -1380,7 +1379,7 @@ struct LimbLoopP8 {
         z[g] = c0_mid<N>(a[V - 1], g, mu, s_mrg + J * 256, q, q2);
         __syncthreads();
         if (g < 32) {
-            if (mu == 6 || mu == 7) c0_tail_fast<L, J>(z, cst, s_mrg + J * 256, g, mu, ba.kp);
+            if (mu == 9) c0_tail_fast8<L, J>(z, cst, s_mrg + J * 256, g, ba.kp);
             else c0_tail<N, L, J>(z, cst, s_mrg + J * 256, g, mu, ba.kp);
         }
         par ^= 1u;

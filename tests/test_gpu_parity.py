@@ -108,6 +108,8 @@ EDGE = [
     dict(n=4096, L=2, d=4096, sizes=[3, 1], nq=5),
     dict(n=4096, L=2, d=1024, sizes=[9], nq=20),
     dict(n=8192, L=3, d=32, sizes=[300, 5], nq=7),
+    dict(n=8192, L=3, d=64, sizes=[130, 3], nq=6),
+    dict(n=8192, L=2, d=128, sizes=[70], nq=5),
     dict(n=8192, L=2, d=8192, sizes=[2], nq=4),
 ]
 
