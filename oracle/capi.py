@@ -12,15 +12,15 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SRC = os.path.join(_HERE, "wally_oracle.c")
+_SRCS = [os.path.join(_HERE, "wally_oracle.c"), os.path.join(_HERE, "wally_simd_oracle.c")]
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (-O2, OpenMP)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or any(os.path.getmtime(_LIB) < os.path.getmtime(x) for x in _SRCS):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-o", tmp, _SRC, "-lm"])
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-o", tmp, *_SRCS, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -67,6 +67,22 @@ def lib():
         L.or_noise_budget_q0.restype = ctypes.c_double
         L.or_noise_budget_Q.argtypes = [c_u32, c_u32, u32p, c_u32, u32p, i8p]
         L.or_noise_budget_Q.restype = ctypes.c_double
+        # SIMD formulation (wally_simd_oracle.c)
+        L.or_simd_slot_exponent.argtypes = [c_u32, c_u32]
+        L.or_simd_slot_exponent.restype = c_u32
+        L.or_simd_row_slices.argtypes = [c_u32, c_u32]
+        L.or_simd_row_slices.restype = c_u32
+        L.or_simd_encode.argtypes = [c_u32, c_u32, u32p, u32p]
+        L.or_simd_decode.argtypes = [c_u32, c_u32, u32p, u32p]
+        L.or_automorph.argtypes = [c_u32, c_u32, u32p, c_u32, u32p]
+        L.or_simd_keygen.argtypes = [c_u32, c_u32, u32p, i8p, c_u32, u32p, i32p, u32p]
+        L.or_keyswitch.argtypes = [c_u32, c_u32, u32p, u32p, u32p, u32p]
+        L.or_rotate.argtypes = [c_u32, c_u32, u32p, u32p, c_u32, u32p, u32p]
+        L.or_simd_diagonal_slots.argtypes = [c_u32, c_u32, c_u32, c_u32, i8p, c_u32, u32p]
+        L.or_simd_query_slots.argtypes = [c_u32, c_u32, c_u32, i32p, u32p]
+        L.or_simd_server.argtypes = [c_u32, c_u32, u32p, c_u32, c_u32, c_u32, u32p, u32p, u32p, u32p, u32p]
+        L.or_simd_server.restype = ctypes.c_int
+        L.or_simd_response.argtypes = [c_u32, c_u32, u32p, u32p, u32p]
         _lib = L
     return _lib
 
@@ -240,3 +256,116 @@ def noise_budget_Q(moduli, t: int, ct, s) -> float:
 def result_slots(n: int, d: int, count: int) -> np.ndarray:
     """Coefficient positions j*d + d - 1 holding the dot products (reading S1)."""
     return np.arange(count) * d + d - 1
+
+
+# ---------------------------------------------------------------------------
+# SIMD formulation (SURVEY.md 8(f)-3; oracle/wally_simd_oracle.c)
+# ---------------------------------------------------------------------------
+
+def simd_slot_exponent(n: int, s: int) -> int:
+    return int(lib().or_simd_slot_exponent(n, s))
+
+
+def simd_row_slices(n: int, d: int) -> int:
+    return int(lib().or_simd_row_slices(n, d))
+
+
+def simd_encode(slots, t: int) -> np.ndarray:
+    x = _u32(slots)
+    out = np.zeros_like(x)
+    lib().or_simd_encode(x.size, t, _p(x, ctypes.c_uint32), _p(out, ctypes.c_uint32))
+    return out
+
+
+def simd_decode(coef, t: int) -> np.ndarray:
+    x = _u32(coef)
+    out = np.zeros_like(x)
+    lib().or_simd_decode(x.size, t, _p(x, ctypes.c_uint32), _p(out, ctypes.c_uint32))
+    return out
+
+
+def automorph(a, q: int, k: int) -> np.ndarray:
+    x = _u32(a)
+    out = np.zeros_like(x)
+    lib().or_automorph(x.size, q, _p(x, ctypes.c_uint32), k, _p(out, ctypes.c_uint32))
+    return out
+
+
+def simd_keygen(mods, s, k: int, a, e) -> np.ndarray:
+    """Rotation key for sigma_k: uint32 [2][L][L+1][n] (mods = L ciphertext moduli + special prime)."""
+    m = _u32(mods)
+    L = m.size - 1
+    s = np.ascontiguousarray(s, dtype=np.int8)
+    n = s.size
+    a = _u32(a).reshape(L, L + 1, n)
+    e = np.ascontiguousarray(e, dtype=np.int32).reshape(L, n)
+    key = np.zeros((2, L, L + 1, n), dtype=np.uint32)
+    lib().or_simd_keygen(n, L, _p(m, ctypes.c_uint32), _p(s, ctypes.c_int8), k, _p(a, ctypes.c_uint32),
+                         _p(e, ctypes.c_int32), _p(key, ctypes.c_uint32))
+    return key
+
+
+def keyswitch(mods, c, key) -> np.ndarray:
+    m = _u32(mods)
+    L = m.size - 1
+    c = _u32(c)
+    n = c.size // L
+    key = _u32(key)
+    out = np.zeros((2, L, n), dtype=np.uint32)
+    lib().or_keyswitch(n, L, _p(m, ctypes.c_uint32), _p(c, ctypes.c_uint32), _p(key, ctypes.c_uint32),
+                       _p(out, ctypes.c_uint32))
+    return out
+
+
+def rotate(mods, ct, k: int, key) -> np.ndarray:
+    m = _u32(mods)
+    L = m.size - 1
+    ct = _u32(ct)
+    n = ct.size // (2 * L)
+    key = _u32(key)
+    out = np.zeros((2, L, n), dtype=np.uint32)
+    lib().or_rotate(n, L, _p(m, ctypes.c_uint32), _p(ct, ctypes.c_uint32), k, _p(key, ctypes.c_uint32),
+                    _p(out, ctypes.c_uint32))
+    return out
+
+
+def simd_diagonal_slots(entries, n: int, t: int, d: int, g: int) -> np.ndarray:
+    e = np.ascontiguousarray(entries, dtype=np.int8).reshape(-1, d)
+    out = np.zeros((d, n), dtype=np.uint32)
+    lib().or_simd_diagonal_slots(n, t, d, g, _p(e, ctypes.c_int8), e.shape[0], _p(out, ctypes.c_uint32))
+    return out
+
+
+def simd_query_slots(q, n: int, t: int) -> np.ndarray:
+    q = np.ascontiguousarray(q, dtype=np.int32)
+    out = np.zeros(n, dtype=np.uint32)
+    lib().or_simd_query_slots(n, t, q.size, _p(q, ctypes.c_int32), _p(out, ctypes.c_uint32))
+    return out
+
+
+def simd_server(mods, t: int, d: int, g: int, ct, key1, keyg, pt) -> np.ndarray:
+    """BSGS server computation; returns the result ciphertext [2][L][n] over Q."""
+    m = _u32(mods)
+    L = m.size - 1
+    ct = _u32(ct)
+    n = ct.size // (2 * L)
+    key1, keyg, pt = _u32(key1), _u32(keyg), _u32(pt)
+    assert pt.size == d * n
+    out = np.zeros((2, L, n), dtype=np.uint32)
+    rc = lib().or_simd_server(n, L, _p(m, ctypes.c_uint32), t, d, g, _p(ct, ctypes.c_uint32),
+                              _p(key1, ctypes.c_uint32), _p(keyg, ctypes.c_uint32), _p(pt, ctypes.c_uint32),
+                              _p(out, ctypes.c_uint32))
+    if rc != 0:
+        raise ValueError("bad SIMD server arguments")
+    return out
+
+
+def simd_response(mods, res) -> np.ndarray:
+    """Switch a result ciphertext over Q (mods = the L ciphertext moduli) to q_0: [2][n]."""
+    m = _u32(mods)
+    L = m.size
+    r = _u32(res)
+    n = r.size // (2 * L)
+    out = np.zeros((2, n), dtype=np.uint32)
+    lib().or_simd_response(n, L, _p(m, ctypes.c_uint32), _p(r, ctypes.c_uint32), _p(out, ctypes.c_uint32))
+    return out
