@@ -20,7 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + INCLUDE, "-I" + CSRC]
 
-SOURCES = ["kernels.cu", "capi.cpp"]
+SOURCES = ["kernels.cu", "capi.cpp", "simd.cu"]
 
 
 def _deps():

@@ -1,0 +1,143 @@
+"""GPU parity of the SIMD formulation (csrc/simd.cu, include/wally_simd.h;
+SURVEY.md §8(f)-3) against the oracle (oracle/wally_simd_oracle.c), through
+the C ABI.  Responses are compared word for word; one case also decrypts
+the GPU responses with real keys and checks the dot products."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import capi  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+T = 65537
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_2406_06761_b200 import build
+    build.build()
+    from paper_2406_06761_b200 import simd
+    return simd
+
+
+def _uniform(rng, mods, shape_prefix, n):
+    """uniform residues: last-but-one axis runs over mods"""
+    out = np.empty((*shape_prefix, len(mods), n), dtype=np.uint32)
+    for i, q in enumerate(mods):
+        out[..., i, :] = rng.integers(0, int(q), size=(*shape_prefix, n))
+    return out
+
+
+def _oracle_responses(srv, clusters, ids, cts, keys):
+    n, L, d, g = srv.n, srv.L, srv.d, srv.baby
+    mods = np.array(srv.moduli, dtype=np.uint32)
+    per = srv.block_entries
+    pts = {}
+    out = []
+    for q, c in enumerate(ids):
+        c = int(c)
+        nb = -(-clusters[c].shape[0] // per)
+        for b in range(nb):
+            if (c, b) not in pts:
+                blk = clusters[c][b * per:(b + 1) * per]
+                pts[(c, b)] = np.stack([capi.simd_encode(x, T) for x in capi.simd_diagonal_slots(blk, n, T, d, g)])
+            res = capi.simd_server(mods, T, d, g, cts[q], keys[q, 0], keys[q, 1], pts[(c, b)])
+            out.append(capi.simd_response(mods[:L], res))
+    return out
+
+
+def _run(srv, ids, cts, keys):
+    dev = torch.device("cuda:0")
+    cts_d = torch.from_numpy(cts.view(np.int32)).to(dev)
+    keys_d = torch.from_numpy(keys.view(np.int32)).to(dev)
+    resp = torch.zeros(max(1, srv.response_words(ids)), dtype=torch.int32, device=dev)
+    off = srv.eval_batch(ids, cts_d, keys_d, resp)
+    torch.cuda.synchronize()
+    return resp.cpu().numpy().view(np.uint32), off
+
+
+CASES = [
+    dict(n=1024, L=2, d=32, g=0, sizes=[1025, 100, 7], nq=5),      # d | n/2, a two-block cluster
+    dict(n=4096, L=3, d=48, g=7, sizes=[3000, 40], nq=3),          # d does not divide n/2, g does not divide d
+    dict(n=2048, L=1, d=24, g=24, sizes=[50], nq=2),               # one limb, one giant step (no giant rotation)
+    dict(n=8192, L=4, d=32, g=5, sizes=[300], nq=2),
+]
+
+
+@pytest.mark.parametrize("cfg", CASES, ids=[f"n{c['n']}_L{c['L']}_d{c['d']}_g{c['g']}" for c in CASES])
+def test_simd_bit_exact_with_oracle(S, cfg):
+    n, L, d = cfg["n"], cfg["L"], cfg["d"]
+    rng = np.random.default_rng(n + L + d)
+    srv = S.SimdServer(n, L, d, baby=cfg["g"])
+    clusters = [rng.integers(-15, 16, size=(s, d)).astype(np.int8) for s in cfg["sizes"]]
+    srv.load_clusters(clusters)
+    ids = rng.integers(0, len(clusters), size=cfg["nq"]).astype(np.uint32)
+    ids[0] = 0
+    mods = srv.moduli
+    cts = _uniform(rng, mods[:L], (cfg["nq"], 2), n)
+    keys = _uniform(rng, mods, (cfg["nq"], 2, 2, L), n)
+    got, off = _run(srv, ids, cts, keys)
+    want = _oracle_responses(srv, clusters, ids, cts, keys)
+    assert off[-1] == len(want) * 2 * n
+    for i, w in enumerate(want):
+        g = got[i * 2 * n:(i + 1) * 2 * n].reshape(2, n)
+        assert np.array_equal(g, w), f"response {i}: {np.count_nonzero(g != w)} words differ"
+
+
+def test_simd_gpu_responses_decrypt_to_dot_products(S):
+    n, L, d = 1024, 2, 32
+    rng = np.random.default_rng(11)
+    srv = S.SimdServer(n, L, d)
+    mods = np.array(srv.moduli, dtype=np.uint32)
+    s = rng.integers(-1, 2, size=n).astype(np.int8)
+
+    def key(k):
+        a = _uniform(rng, mods, (L,), n)
+        e = np.clip(np.rint(rng.normal(0, 3.2, size=(L, n))), -19, 19).astype(np.int32)
+        return capi.simd_keygen(mods, s, k, a, e)
+    clusters = [rng.integers(-15, 16, size=(sz, d)).astype(np.int8) for sz in (1024, 300)]
+    srv.load_clusters(clusters)
+    ids = np.array([0, 1], np.uint32)
+    qs = rng.integers(-15, 16, size=(2, d)).astype(np.int32)
+    cts = np.stack([capi.encrypt(mods[:L], T, capi.simd_encode(capi.simd_query_slots(q, n, T), T).astype(np.int32),
+                                 s, _uniform(rng, mods[:L], (), n),
+                                 np.clip(np.rint(rng.normal(0, 3.2, size=n)), -19, 19).astype(np.int32))
+                    for q in qs])
+    keys = np.stack([np.stack([key(srv.galois[0]), key(srv.galois[1])]) for _ in range(2)])
+    got, off = _run(srv, ids, cts, keys)
+    R = srv.row_slices
+    for qi in range(2):
+        resp = got[int(off[qi]):int(off[qi]) + 2 * n]
+        assert capi.noise_budget_q0(int(mods[0]), T, resp, s) > 2
+        slots = capi.simd_decode(capi.decrypt_q0(int(mods[0]), T, resp, s), T)
+        ent = clusters[ids[qi]]
+        want = (ent.astype(np.int64) @ qs[qi].astype(np.int64)) % T
+        for e in range(ent.shape[0]):
+            sl, col = divmod(e, d)
+            r, u = divmod(sl, R)
+            assert slots[r * (n // 2) + u * d + col] == want[e], (qi, e)
+
+
+def test_simd_errors(S):
+    n, L, d = 1024, 2, 16
+    srv = S.SimdServer(n, L, d)
+    rng = np.random.default_rng(3)
+    srv.load_clusters([rng.integers(-15, 16, size=(40, d)).astype(np.int8)])
+    mods = srv.moduli
+    cts = _uniform(rng, mods[:L], (1, 2), n)
+    keys = _uniform(rng, mods, (1, 2, 2, L), n)
+    with pytest.raises(S.WallyError) as e:
+        _run(srv, np.array([1], np.uint32), cts, keys)
+    assert e.value.code == -3
+    bad = cts.copy()
+    bad[0, 1, 1, 5] = mods[1]
+    with pytest.raises(S.WallyError) as e:
+        _run(srv, np.array([0], np.uint32), bad, keys)
+    assert e.value.code == -4
+    with pytest.raises(S.WallyError):
+        S.SimdServer(n, L, n)                     # d > n/2
+    m = list(mods)
+    with pytest.raises(S.WallyError):
+        S.SimdServer(n, L, d, moduli=m[:L] + [m[-1] + 2 * n * 1000])   # special prime not below q_0 / not prime
+    assert srv.modmuls_per_query(1) > 0 and srv.launch_count() > 0
