@@ -66,6 +66,9 @@ def parse():
                     help="response format (SURVEY 8(f)-1): compact = c0 only at the E result coefficients + c1; "
                          "compact_drop = compact with c1's 6 LSBs dropped (24-bit, n = 4096); auto = compact_drop "
                          "where allowed, else compact")
+    ap.add_argument("--path", default="coeff", choices=["coeff", "simd"],
+                    help="coeff: the coefficient-packed path (north star); simd: the paper's SIMD formulation "
+                         "(diagonals + BSGS rotations with hybrid key switching, SURVEY 8(f)-3)")
     ap.add_argument("--queries", type=int, default=0,
                     help="profiling only: evaluate just the first Q queries of the batch (not a bench line)")
     return ap.parse_args()
@@ -456,6 +459,133 @@ def run_e2e(args, srv, ids, cts, off, world, rank, local_rank, dots_local):
 
 
 # ---------------------------------------------------------------------------
+# the SIMD formulation: a second bench line, not the default
+# ---------------------------------------------------------------------------
+
+def run_simd(args, rank, world, local_rank):
+    """One step = wally_simd_eval_batch over the configuration's query batch:
+    NTT of every query ciphertext and both rotation keys, g - 1 baby-step
+    rotations per query, the diagonal inner products, m - 1 giant-step
+    rotations and the switch to q_0 per (query, block).  Ranks > 1 run
+    independent replicas on disjoint query shares (no collective: the SIMD
+    path shards by query like the coefficient path)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2406_06761_b200.simd import SimdServer
+
+    torch.cuda.set_device(local_rank)
+    dev = f"cuda:{local_rank}"
+    w = synth.WORKLOADS[args.config]
+    t_setup = time.time()
+    ents = synth.cluster_entries(w)
+    ids_all = synth.query_clusters(w)
+    srv = SimdServer(w.n, w.num_limbs, w.d, w.t, device=local_rank)
+    te = time.time()
+    srv.load_clusters([ents[c] for c in range(w.num_clusters)])
+    torch.cuda.synchronize()
+    encode_s = time.time() - te
+    nsel = args.queries if args.queries > 0 else ids_all.size
+    share = np.arange(nsel)[rank::world]
+    ids = np.ascontiguousarray(ids_all[share])
+    nq = int(ids.size)
+    cts = synth.uniform_ciphertexts_torch(w, srv.moduli[:w.num_limbs], device=dev)[:nsel]
+    keys = synth.uniform_keys_torch(w, srv.moduli, num_queries=nsel, device=dev)
+    if world > 1:
+        sel = torch.from_numpy(share).to(dev)
+        cts, keys = cts[sel].contiguous(), keys[sel].contiguous()
+    cts = cts.contiguous()
+    words = srv.response_words(ids)
+    resp = torch.empty(max(1, words), dtype=torch.int32, device=dev)
+    blocks = np.array([srv.blocks(int(c)) for c in ids])
+    dots = nq * w.cluster_size
+    torch.cuda.synchronize()
+    setup_s = time.time() - t_setup
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        srv.eval_batch(ids, cts, keys, resp)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = srv.launch_count()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        clk.wait_first()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t_clk0 = clk.mark()
+        start.record(stream)
+        for _ in range(args.steps):
+            srv.eval_batch(ids, cts, keys, resp)
+        end.record(stream)
+        torch.cuda.synchronize()
+        t_clk1 = clk.mark()
+    ms = start.elapsed_time(end)
+    launches = srv.launch_count() - launches0
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    wk = torch.tensor([dots, nq], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(wk, op=dist.ReduceOp.SUM)
+    ms_per_step = float(t[0]) / args.steps
+    tot_dots, tot_nq = (int(x) for x in wk.tolist())
+    value = tot_dots / (ms_per_step / 1e3)
+    peaks = measured_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    clocks = clk.summary(t_clk0, t_clk1)
+    mm = sum(srv.modmuls_per_query(int(b)) for b in blocks)
+    achieved = mm / (ms / args.steps / 1e3) / 1e12
+    peak = SM_COUNT * MODMUL_PER_CLK_PER_SM * sm_max * 1e6 / 1e12
+    roofline = {"bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 4), "unit": "Tmodmul/s",
+                "frac": round(achieved / peak, 4), "traffic": None,
+                "kernel": "the whole SIMD step (simd_ntt, simd_modup/moddown key switching, simd_ptmac, "
+                          "simd_switch; every kernel is bound by the same integer multiply pipe)",
+                "per_launch": f"{mm} modmul per step (wally_simd_modmuls_per_query summed over the batch)",
+                "peak_basis": f"{SM_COUNT} SMs x {MODMUL_PER_CLK_PER_SM:.0f} Shoup modmul/clk/SM x {sm_max:.0f} MHz"}
+    out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+           "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "u32",
+           "data": "synthetic (seeded; query ciphertexts and rotation keys are uniform RNS residues)",
+           "path": "simd (SURVEY.md 8(f)-3: diagonal packing + BSGS rotations, hybrid key switching)",
+           "config": {"workload": w.name + "-simd", "description": w.description, "n": w.n, "limbs": w.num_limbs,
+                      "special_prime": srv.moduli[-1], "d": w.d, "t": w.t, "baby": srv.baby, "giant": srv.giant,
+                      "row_slices": srv.row_slices, "block_entries": srv.block_entries,
+                      "queries": int(tot_nq), "blocks_per_step": int(blocks.sum()), "dots_per_step": int(tot_dots),
+                      "key_bytes_per_query": int(srv.key_words * 4),
+                      "l2": "inputs larger than L2 (plaintexts, keys and ciphertexts >> 126 MB)"},
+           "roofline": roofline, "gpu_launches": int(launches), "clocks": clocks,
+           "setup_s": round(setup_s, 1), "encode_s": round(encode_s, 3)}
+    if args.queries > 0:
+        out["profiling_subset"] = f"first {args.queries} queries only -- not a bench line"
+    if not args.no_e2e and args.e2e_steps > 0:
+        # end to end: pinned host ciphertexts + keys -> device, eval, responses -> pinned host
+        qh = torch.empty(cts.shape, dtype=torch.int32, pin_memory=True)
+        qh.copy_(cts)
+        kh = torch.empty(keys.shape, dtype=torch.int32, pin_memory=True)
+        kh.copy_(keys)
+        rh = torch.empty(resp.numel(), dtype=torch.int32, pin_memory=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            cts.copy_(qh, non_blocking=True)
+            keys.copy_(kh, non_blocking=True)
+            srv.eval_batch(ids, cts, keys, resp)
+            rh.copy_(resp, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / args.e2e_steps
+        out["e2e"] = {"value": round(dots / (ems / 1e3), 1), "unit": UNIT,
+                      "h2d_bytes_per_step": int((cts.numel() + keys.numel()) * 4), "d2h_bytes_per_step": int(words * 4),
+                      "ms_per_step": round(ems, 3), "steps": args.e2e_steps,
+                      "api": "wally_simd_eval_batch with pinned host ciphertexts and keys copied in and responses "
+                             "copied out inside the timed region"}
+        del qh, kh, rh
+    srv.close()
+    return out
+
+
+# ---------------------------------------------------------------------------
 # the reference arm: the CPU oracle as it stands
 # ---------------------------------------------------------------------------
 
@@ -516,7 +646,7 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
-    out = run_wally(args, rank, world, local_rank)
+    out = run_simd(args, rank, world, local_rank) if args.path == "simd" else run_wally(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -250,3 +250,25 @@ def uniform_ciphertexts_torch(w: Workload, moduli, num_queries: int | None = Non
     for l, q in enumerate(moduli):
         out[:, :, l, :] = torch.randint(0, int(q), (nq, 2, w.n), generator=g, device=device, dtype=torch.int32)
     return out
+
+
+def uniform_keys_torch(w: Workload, moduli, num_queries: int | None = None, device="cuda", seed_offset: int = 0,
+                       chunk: int = 1024):
+    """Stand-ins for the two per-query rotation keys of the SIMD formulation
+    (SURVEY.md 8(f)-3): int32 [nq][2 keys][2][L][L+1][n] uniform residues,
+    residue m (last-but-one axis) below moduli[m] (the L ciphertext limbs and
+    the special prime).  A key is (b, a) with a uniform and b = -a s + e + ...
+    an RLWE sample, so uniform residues have its distribution; the server
+    path is data-oblivious."""
+    import torch
+    nq = w.num_queries if num_queries is None else num_queries
+    L, M = len(moduli) - 1, len(moduli)
+    g = torch.Generator(device=device)
+    g.manual_seed(w.seed * 1000033 + seed_offset)
+    out = torch.empty((nq, 2, 2, L, M, w.n), dtype=torch.int32, device=device)
+    for q0 in range(0, nq, chunk):
+        q1 = min(nq, q0 + chunk)
+        for m, q in enumerate(moduli):
+            out[q0:q1, :, :, :, m, :] = torch.randint(0, int(q), (q1 - q0, 2, 2, L, w.n), generator=g,
+                                                      device=device, dtype=torch.int32)
+    return out
