@@ -75,14 +75,16 @@ __device__ __forceinline__ uint32_t canon4(uint32_t x, uint32_t q, uint32_t q2) 
 
 // ---------------------------------------------------------------------------
 // Forward NTT of polynomials p = 0..count-1 (a2'): modulus index p % period;
-// input polynomial p at in + (p / grp) * in_stride + (p % grp) * N (the same
-// for out); residues >= q set err.
+// input polynomial p at in + sel[p / grp] * in_stride + (p % grp) * N (sel ==
+// nullptr: p / grp), output at out + (p / grp) * out_stride + (p % grp) * N;
+// residues >= q set err.
 // ---------------------------------------------------------------------------
 template <int N>
 __global__ void __launch_bounds__(NttGeom<N>::T) simd_ntt_kernel(Mods md, const uint2 *__restrict__ tw, uint32_t period,
                                                                 uint32_t grp, const uint32_t *__restrict__ in,
-                                                                size_t in_stride, uint32_t *__restrict__ out,
-                                                                size_t out_stride, uint32_t *err) {
+                                                                size_t in_stride, const uint32_t *__restrict__ sel,
+                                                                uint32_t *__restrict__ out, size_t out_stride,
+                                                                uint32_t *err) {
     using Gm = NttGeom<N>;
     constexpr int V = Gm::V;
     extern __shared__ uint32_t smem[];
@@ -90,7 +92,8 @@ __global__ void __launch_bounds__(NttGeom<N>::T) simd_ntt_kernel(Mods md, const 
     const size_t p = blockIdx.x;
     const uint32_t m = (uint32_t)(p % period);
     const uint32_t q = md.q[m], q2 = md.q2[m];
-    const uint32_t *src = in + (p / grp) * in_stride + (p % grp) * N;
+    const size_t gi = sel ? (size_t)sel[p / grp] : p / grp;    // input group (query) of this polynomial
+    const uint32_t *src = in + gi * in_stride + (p % grp) * N;
     uint32_t a[1][V];
     bool bad = false;
 #pragma unroll
@@ -266,6 +269,187 @@ __global__ void __launch_bounds__(256) simd_ptmac_kernel(Mods md, uint32_t N, ui
         }
         *reinterpret_cast<uint2 *>(Iu + (size_t)j * CT + w) = make_uint2(csub(a0x, q), csub(a0y, q));
         *reinterpret_cast<uint2 *>(Iu + (size_t)j * CT + (size_t)L * N + w) = make_uint2(csub(a1x, q), csub(a1y, q));
+    }
+}
+
+// The same with the baby step outermost and the m accumulators of a thread
+// in registers (MAXM >= m): every baby ciphertext and plaintext word is read
+// once.  Units are ordered by cluster, so the CTAs sharing a plaintext
+// chunk run together and the plaintexts are served from L2.
+template <int MAXM>
+__global__ void __launch_bounds__(256) simd_ptmac_reg_kernel(Mods md, uint32_t N, uint32_t d, uint32_t g, uint32_t m,
+                                                             const uint32_t *__restrict__ baby,
+                                                             const uint32_t *__restrict__ uq,
+                                                             const uint32_t *__restrict__ ublk,
+                                                             const uint32_t *__restrict__ ptv,
+                                                             const uint32_t *__restrict__ ptc,
+                                                             uint32_t *__restrict__ I) {
+    const uint32_t L = md.L;
+    const uint32_t u = blockIdx.x;
+    const uint32_t w = (blockIdx.y * blockDim.x + threadIdx.x) * 2;
+    if (w >= L * N) return;
+    const uint32_t l = w / N;
+    const uint32_t q = md.q[l], q2 = md.q2[l];
+    const size_t CT = (size_t)2 * L * N, LN = (size_t)L * N;
+    const uint32_t *bq = baby + (size_t)uq[u] * g * CT + w;
+    const uint32_t *pv0 = ptv + (size_t)ublk[u] * d * LN + w, *pc0 = ptc + (size_t)ublk[u] * d * LN + w;
+    uint32_t acc[MAXM][4];
+#pragma unroll
+    for (int j = 0; j < MAXM; j++) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0;
+    for (uint32_t b = 0; b < g; b++) {
+        const uint2 x0 = __ldg(reinterpret_cast<const uint2 *>(bq + (size_t)b * CT));
+        const uint2 x1 = __ldg(reinterpret_cast<const uint2 *>(bq + (size_t)b * CT + LN));
+#pragma unroll
+        for (int j = 0; j < MAXM; j++) {
+            const uint32_t i = (uint32_t)j * g + b;
+            if ((uint32_t)j < m && i < d) {
+                const uint2 pv = __ldg(reinterpret_cast<const uint2 *>(pv0 + (size_t)i * LN));
+                const uint2 pc = __ldg(reinterpret_cast<const uint2 *>(pc0 + (size_t)i * LN));
+                acc[j][0] = csub(acc[j][0] + shoup_mul(x0.x, pv.x, pc.x, q), q2);
+                acc[j][1] = csub(acc[j][1] + shoup_mul(x0.y, pv.y, pc.y, q), q2);
+                acc[j][2] = csub(acc[j][2] + shoup_mul(x1.x, pv.x, pc.x, q), q2);
+                acc[j][3] = csub(acc[j][3] + shoup_mul(x1.y, pv.y, pc.y, q), q2);
+            }
+        }
+    }
+    uint32_t *Iu = I + (size_t)u * m * CT + w;
+#pragma unroll
+    for (int j = 0; j < MAXM; j++) {
+        if ((uint32_t)j < m) {
+            *reinterpret_cast<uint2 *>(Iu + (size_t)j * CT) = make_uint2(csub(acc[j][0], q), csub(acc[j][1], q));
+            *reinterpret_cast<uint2 *>(Iu + (size_t)j * CT + LN) = make_uint2(csub(acc[j][2], q), csub(acc[j][3], q));
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// A chain of rotations in one CTA per unit (n <= 4096): step s = 1..steps
+// computes X_s = rot(X_{s-1}) (+ addend_s) -- the whole key switch of one
+// rotation (ModUp, key products, ModDown) without materialising the
+// extended digits, and the unit's key is re-read from L2 by every step.
+//   X_0   = X0 + u * x0s
+//   X_s   = outs[s & 1] + u * out_us + (s - 1) * out_ss
+//   add_s = add + u * add_us + (s - 1) * add_ss        (add == nullptr: none)
+// Shared memory: the L digits D_j (coefficient form; each thread reads back
+// only the elements it wrote) and the two exchange buffers.  Step outputs
+// are read back with L1-bypassing loads (another thread wrote them).
+// ---------------------------------------------------------------------------
+template <int N>
+__global__ void __launch_bounds__(NttGeom<N>::T, 2) simd_rot_chain_kernel(
+    Mods md, const uint2 *__restrict__ twf, const uint2 *__restrict__ twi, const uint32_t *__restrict__ perm,
+    const uint32_t *__restrict__ keys, size_t key_stride, const uint32_t *__restrict__ uq, const uint32_t *X0,
+    size_t x0s, uint32_t *out_even, uint32_t *out_odd, size_t out_us, ptrdiff_t out_ss, const uint32_t *add,
+    size_t add_us, ptrdiff_t add_ss, uint32_t steps) {
+    using Gm = NttGeom<N>;
+    constexpr int V = Gm::V;
+    extern __shared__ uint32_t smem[];
+    uint32_t *bufA = smem, *bufB = smem + Gm::SMEM_WORDS, *D = smem + 2 * Gm::SMEM_WORDS;
+    const int g = threadIdx.x;
+    const uint32_t u = blockIdx.x, L = md.L, M = md.M;
+    const uint32_t P = md.q[L], P2 = md.q2[L];
+    const uint32_t *ku = keys + (size_t)(uq ? uq[u] : u) * key_stride;
+    const size_t KC = (size_t)L * M * N;                // one key component
+    uint32_t pm[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) pm[v] = __ldg(perm + g * V + v);
+    const uint32_t *X = X0 + (size_t)u * x0s;
+    for (uint32_t st = 1; st <= steps; st++) {
+        uint32_t *Y = ((st & 1) ? out_odd : out_even) + (size_t)u * out_us + (ptrdiff_t)(st - 1) * out_ss;
+        const uint32_t *ad = add ? add + (size_t)u * add_us + (ptrdiff_t)(st - 1) * add_ss : nullptr;
+        uint32_t a[1][V];
+        // ModUp, part 1: digits D_j = INTT_j(sigma(c1)_j)
+        for (uint32_t j = 0; j < L; j++) {
+            const uint32_t qj = md.q[j], qj2 = md.q2[j];
+            const uint32_t *c1 = X + ((size_t)L + j) * N;
+#pragma unroll
+            for (int v = 0; v < V; v++) a[0][v] = shoup_mul(__ldcg(c1 + pm[v]), md.ninv[j], md.ninvp[j], qj);
+            __syncthreads();
+            intt_chain<N, 1>(a, twi + (size_t)j * Gm::TW_LIMB, g, qj, qj2, bufA, bufB);
+#pragma unroll
+            for (int jj = 0; jj < V / Gm::R2; jj++)
+#pragma unroll
+                for (int k = 0; k < Gm::R2; k++)
+                    D[(size_t)j * N + pass_index<N, Gm::TB2, Gm::R2>(g, jj, k)] = csub(a[0][jj * Gm::R2 + k], qj);
+        }
+        // key products at modulus m: s_c = sum_j ext_j * key[c][j][m]
+        auto mac_at = [&](uint32_t m, uint64_t (&s0)[V], uint64_t (&s1)[V]) {
+            const uint32_t q = md.q[m], q2 = md.q2[m];
+#pragma unroll
+            for (int v = 0; v < V; v++) s0[v] = s1[v] = 0;
+            for (uint32_t j = 0; j < L; j++) {
+                if (j == m) {
+                    const uint32_t *c1 = X + ((size_t)L + j) * N;
+#pragma unroll
+                    for (int v = 0; v < V; v++) a[0][v] = __ldcg(c1 + pm[v]);
+                } else {
+#pragma unroll
+                    for (int jj = 0; jj < V / Gm::R2; jj++)
+#pragma unroll
+                        for (int k = 0; k < Gm::R2; k++)
+                            a[0][jj * Gm::R2 + k] =
+                                csub(D[(size_t)j * N + pass_index<N, Gm::TB2, Gm::R2>(g, jj, k)], q);
+                    __syncthreads();
+                    ntt_chain<N, 1>(a, twf + (size_t)m * Gm::TW_LIMB, g, q, q2, bufA, bufB);
+#pragma unroll
+                    for (int v = 0; v < V; v++) a[0][v] = canon4(a[0][v], q, q2);
+                }
+                uint32_t k0[V], k1[V];
+                load_contig<N>(ku + ((size_t)j * M + m) * N, k0, g);
+                load_contig<N>(ku + KC + ((size_t)j * M + m) * N, k1, g);
+#pragma unroll
+                for (int v = 0; v < V; v++) {
+                    s0[v] += (uint64_t)a[0][v] * k0[v];
+                    s1[v] += (uint64_t)a[0][v] * k1[v];
+                }
+            }
+        };
+        uint64_t s0[V], s1[V];
+        // ModDown, part 1: z_c = INTT_P([acc_c]_P)
+        mac_at(L, s0, s1);
+        uint32_t z0[V], z1[V];
+#pragma unroll
+        for (int v = 0; v < V; v++) a[0][v] = shoup_mul(red64(s0[v], P, md.mu[L]), md.ninv[L], md.ninvp[L], P);
+        __syncthreads();
+        intt_chain<N, 1>(a, twi + (size_t)L * Gm::TW_LIMB, g, P, P2, bufA, bufB);
+#pragma unroll
+        for (int v = 0; v < V; v++) z0[v] = csub(a[0][v], P);
+#pragma unroll
+        for (int v = 0; v < V; v++) a[0][v] = shoup_mul(red64(s1[v], P, md.mu[L]), md.ninv[L], md.ninvp[L], P);
+        __syncthreads();
+        intt_chain<N, 1>(a, twi + (size_t)L * Gm::TW_LIMB, g, P, P2, bufA, bufB);
+#pragma unroll
+        for (int v = 0; v < V; v++) z1[v] = csub(a[0][v], P);
+        // ModDown, part 2, per limb i: out_c,i = (acc_c,i - NTT_i(z_c)) P^{-1} (+ sigma(c0)_i) (+ add)
+        for (uint32_t i = 0; i < L; i++) {
+            const uint32_t q = md.q[i], q2 = md.q2[i];
+            mac_at(i, s0, s1);
+            for (int c = 0; c < 2; c++) {
+#pragma unroll
+                for (int v = 0; v < V; v++) a[0][v] = c ? z1[v] : z0[v];     // z < P < q_i
+                __syncthreads();
+                ntt_chain<N, 1>(a, twf + (size_t)i * Gm::TW_LIMB, g, q, q2, bufA, bufB);
+                uint32_t r[1][V];
+#pragma unroll
+                for (int v = 0; v < V; v++) {
+                    const uint32_t acc = red64(c ? s1[v] : s0[v], q, md.mu[i]);
+                    r[0][v] = csub(shoup_mul(acc + q - canon4(a[0][v], q, q2), md.pinv[i], md.pinvp[i], q), q);
+                }
+                if (c == 0) {
+                    const uint32_t *c0 = X + (size_t)i * N;
+#pragma unroll
+                    for (int v = 0; v < V; v++) r[0][v] = csub(r[0][v] + __ldcg(c0 + pm[v]), q);
+                }
+                if (ad) {
+                    uint32_t w2[V];
+                    load_contig<N>(ad + ((size_t)c * L + i) * N, w2, g);
+#pragma unroll
+                    for (int v = 0; v < V; v++) r[0][v] = csub(r[0][v] + w2[v], q);
+                }
+                store_contig<N>(Y + ((size_t)c * L + i) * N, r, g);
+            }
+        }
+        __syncthreads();                 // Y complete before the next step gathers from it
+        X = Y;
     }
 }
 
@@ -705,12 +889,13 @@ extern "C" uint64_t wally_simd_modmuls_per_query(const wally_simd_ctx *c, uint32
 // ---------------------------------------------------------------------------
 template <int N>
 static cudaError_t launch_ntt(wally_simd_ctx *c, uint32_t period, uint32_t grp, const uint32_t *in, size_t in_stride,
-                              uint32_t *out, size_t out_stride, size_t count, uint32_t *err, cudaStream_t s) {
+                              const uint32_t *sel, uint32_t *out, size_t out_stride, size_t count, uint32_t *err,
+                              cudaStream_t s) {
     static bool cfg = false;
     if (!cfg) { cudaError_t e = allow(simd_ntt_kernel<N>, chain_smem<N>()); if (e) return e; cfg = true; }
     if (!count) return cudaSuccess;
     simd_ntt_kernel<N><<<(unsigned)count, NttGeom<N>::T, chain_smem<N>(), s>>>(c->md, c->d_twf, period, grp, in,
-                                                                              in_stride, out, out_stride, err);
+                                                                              in_stride, sel, out, out_stride, err);
     c->launches++;
     return cudaGetLastError();
 }
@@ -733,6 +918,53 @@ static cudaError_t launch_rotate(wally_simd_ctx *c, uint32_t units, const uint32
     simd_moddown_kernel<N><<<dim3(units, 2), NttGeom<N>::T, chain_smem<N>(), s>>>(
         c->md, c->d_twf, c->d_twi, ext, keys, key_stride, uq, X, xs, perm, add, as, out, os);
     c->launches += 2;
+    return cudaGetLastError();
+}
+
+template <int N>
+static size_t chain_kernel_smem(uint32_t L) { return chain_smem<N>() + (size_t)L * N * sizeof(uint32_t); }
+
+template <int N>
+static cudaError_t launch_chain(wally_simd_ctx *c, uint32_t units, bool giant, const uint32_t *keys, size_t key_stride,
+                                const uint32_t *uq, const uint32_t *X0, size_t x0s, uint32_t *out_even,
+                                uint32_t *out_odd, size_t out_us, ptrdiff_t out_ss, const uint32_t *add, size_t add_us,
+                                ptrdiff_t add_ss, uint32_t steps, cudaStream_t s) {
+    if constexpr (N > 4096) {
+        return cudaErrorNotSupported;
+    } else {
+        static bool cfg = false;
+        if (!cfg) {
+            cudaError_t e = allow(simd_rot_chain_kernel<N>, chain_kernel_smem<N>(WALLY_MAX_LIMBS));
+            if (e) return e;
+            cfg = true;
+        }
+        if (!units || !steps) return cudaSuccess;
+        simd_rot_chain_kernel<N><<<units, NttGeom<N>::T, chain_kernel_smem<N>(c->L), s>>>(
+            c->md, c->d_twf, c->d_twi, giant ? c->d_permg : c->d_perm1, keys, key_stride, uq, X0, x0s, out_even,
+            out_odd, out_us, out_ss, add, add_us, add_ss, steps);
+        c->launches++;
+        return cudaGetLastError();
+    }
+}
+
+static cudaError_t launch_ptmac(wally_simd_ctx *c, uint32_t U, const uint32_t *baby, const uint32_t *uq,
+                                const uint32_t *ublk, uint32_t *I, cudaStream_t s) {
+    const uint32_t n = c->p.n, thr = 256, words = c->L * n / 2;
+    const dim3 grid(U, (words + thr - 1) / thr);
+#ifndef WALLY_SIMD_PTMAC_REG
+#define WALLY_SIMD_PTMAC_REG 0
+#endif
+    if (!WALLY_SIMD_PTMAC_REG)
+        simd_ptmac_kernel<<<grid, thr, 0, s>>>(c->md, n, c->p.d, c->g, c->m, baby, uq, ublk, c->d_ptv, c->d_ptc, I);
+    else if (c->m <= 16)
+        simd_ptmac_reg_kernel<16><<<grid, thr, 0, s>>>(c->md, n, c->p.d, c->g, c->m, baby, uq, ublk, c->d_ptv,
+                                                        c->d_ptc, I);
+    else if (c->m <= 32)
+        simd_ptmac_reg_kernel<32><<<grid, thr, 0, s>>>(c->md, n, c->p.d, c->g, c->m, baby, uq, ublk, c->d_ptv,
+                                                        c->d_ptc, I);
+    else
+        simd_ptmac_kernel<<<grid, thr, 0, s>>>(c->md, n, c->p.d, c->g, c->m, baby, uq, ublk, c->d_ptv, c->d_ptc, I);
+    c->launches++;
     return cudaGetLastError();
 }
 
@@ -843,15 +1075,27 @@ extern "C" int wally_simd_eval_batch(wally_simd_ctx *c, uint32_t nq, const uint3
     SCUDA(c, cudaSetDevice(c->device));
     cudaStream_t s = (cudaStream_t)stream;
     const size_t CT = (size_t)2 * L * n, KW = (size_t)2 * 2 * L * M * n, EXT = (size_t)L * M * n;
+    // queries are processed in cluster order (stable), so the units sharing a
+    // block's plaintexts are adjacent; responses stay in input order
+    std::vector<uint32_t> order(nq);
+    for (uint32_t q = 0; q < nq; q++) order[q] = q;
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return ids[a] < ids[b]; });
     // chunk: at most Qc queries and Uc units (query-blocks)
     uint32_t max_blk = 1;
     for (uint32_t q = 0; q < nq; q++) max_blk = std::max(max_blk, c->blk_num[ids[q]]);
     const uint32_t Qc = std::min<uint32_t>(nq, std::max<uint32_t>(1, (uint32_t)((2048ull * 4096) / n)));
     const uint32_t Uc = Qc * max_blk;
-    // workspace: baby [Qc][g][CT], keys [Qc][KW], ext [max(Qc,Uc)][EXT], I [Uc][m][CT], acc 2 x [Uc][CT], err
-    const size_t w_baby = (size_t)Qc * g * CT, w_key = (size_t)Qc * KW, w_ext = (size_t)std::max(Qc, Uc) * EXT;
+#ifndef WALLY_SIMD_CHAIN
+#define WALLY_SIMD_CHAIN 1
+#endif
+    const bool fused = WALLY_SIMD_CHAIN && n <= 4096;
+    // workspace: baby [Qc][g][CT], keys [Qc][KW], ext [max(Qc,Uc)][EXT] (n = 8192 only), I [Uc][m][CT],
+    // acc 2 x [Uc][CT], unit tables, err
+    const size_t w_baby = (size_t)Qc * g * CT, w_key = (size_t)Qc * KW;
+    const size_t w_ext = fused ? 0 : (size_t)std::max(Qc, Uc) * EXT;
     const size_t w_I = (size_t)Uc * m * CT, w_acc = (size_t)Uc * CT;
-    const size_t need = 4 * (w_baby + w_key + w_ext + w_I + 2 * w_acc + 3 * (size_t)Uc + 64);
+    const size_t w_tab = 3 * (size_t)Uc + Qc;
+    const size_t need = 4 * (w_baby + w_key + w_ext + w_I + 2 * w_acc + w_tab + 64);
     if (c->ws_bytes < need) {
         cudaFree(c->ws);
         c->ws = nullptr;
@@ -859,67 +1103,73 @@ extern "C" int wally_simd_eval_batch(wally_simd_ctx *c, uint32_t nq, const uint3
         if (cudaMalloc(&c->ws, need) != cudaSuccess) return sfail(c, WALLY_E_OOM, "workspace (%zu bytes)", need);
         c->ws_bytes = need;
     }
-    if (c->h_units_cap < 3 * (size_t)Uc) {
+    if (c->h_units_cap < w_tab) {
         cudaFreeHost(c->h_units);
         c->h_units = nullptr;
-        SCUDA(c, cudaMallocHost(&c->h_units, 4 * 3 * (size_t)Uc));
-        c->h_units_cap = 3 * (size_t)Uc;
+        SCUDA(c, cudaMallocHost(&c->h_units, 4 * w_tab));
+        c->h_units_cap = w_tab;
     }
     uint32_t *w = (uint32_t *)c->ws;
     uint32_t *baby = w, *keyN = baby + w_baby, *ext = keyN + w_key, *I = ext + w_ext, *accA = I + w_I,
              *accB = accA + w_acc, *d_uq = accB + w_acc, *d_ublk = d_uq + Uc, *d_uoff = d_ublk + Uc,
-             *d_err = d_uoff + Uc;
+             *d_sel = d_uoff + Uc, *d_err = d_sel + Qc;
     SCUDA(c, cudaMemsetAsync(d_err, 0, 4, s));
     cudaError_t e = cudaSuccess;
     for (uint32_t q0 = 0; q0 < nq; q0 += Qc) {
         const uint32_t nc = std::min(Qc, nq - q0);
         // unit tables of this chunk (pinned, uploaded in stream order)
         uint32_t U = 0;
-        uint32_t *hq = c->h_units, *hb = hq + Uc, *ho = hb + Uc;
+        uint32_t *hq = c->h_units, *hb = hq + Uc, *ho = hb + Uc, *hs = ho + Uc;
         SCUDA(c, cudaStreamSynchronize(s));     // the pinned tables of the previous chunk are consumed
         for (uint32_t q = 0; q < nc; q++) {
-            const uint32_t cl = ids[q0 + q];
+            const uint32_t qi = order[q0 + q], cl = ids[qi];
+            hs[q] = qi;
             for (uint32_t b = 0; b < c->blk_num[cl]; b++, U++) {
                 hq[U] = q;
                 hb[U] = c->blk_first[cl] + b;
-                const uint64_t o = off[q0 + q] + (uint64_t)b * 2 * n;
+                const uint64_t o = off[qi] + (uint64_t)b * 2 * n;
                 if (o > 0xffffffffull) return sfail(c, WALLY_E_ARG, "response offset beyond 2^32 words: batch too large");
                 ho[U] = (uint32_t)o;
             }
         }
-        SCUDA(c, cudaMemcpyAsync(d_uq, hq, 4ull * 3 * Uc, cudaMemcpyHostToDevice, s));
+        SCUDA(c, cudaMemcpyAsync(d_uq, hq, 4 * w_tab, cudaMemcpyHostToDevice, s));
         const size_t gCT = (size_t)g * CT;
         // a2': NTT of the chunk's ciphertexts (-> baby_0) and keys
-        SIMD_DISPATCH(n, e = launch_ntt<N>(c, L, 2 * L, query_ct + (size_t)q0 * CT, CT, baby, gCT, (size_t)nc * 2 * L,
-                                           d_err, s));
+        SIMD_DISPATCH(n, e = launch_ntt<N>(c, L, 2 * L, query_ct, CT, d_sel, baby, gCT, (size_t)nc * 2 * L, d_err, s));
         if (e) break;
-        SIMD_DISPATCH(n, e = launch_ntt<N>(c, M, 1, keys + (size_t)q0 * KW, n, keyN, n, (size_t)nc * 2 * 2 * L * M,
-                                           d_err, s));
+        SIMD_DISPATCH(n, e = launch_ntt<N>(c, M, 2 * 2 * L * M, keys, KW, d_sel, keyN, KW,
+                                           (size_t)nc * 2 * 2 * L * M, d_err, s));
         if (e) break;
         // baby steps: baby_b = rot_1(baby_{b-1})
-        for (uint32_t b = 1; b < g && !e; b++)
-            SIMD_DISPATCH(n, e = launch_rotate<N>(c, nc, baby + (size_t)(b - 1) * CT, gCT, false, ext, keyN, KW,
-                                                  nullptr, nullptr, 0, baby + (size_t)b * CT, gCT, s));
+        if (fused) {
+            SIMD_DISPATCH(n, e = launch_chain<N>(c, nc, false, keyN, KW, nullptr, baby, gCT, baby + CT, baby + CT, gCT,
+                                                 (ptrdiff_t)CT, nullptr, 0, 0, g - 1, s));
+        } else {
+            for (uint32_t b = 1; b < g && !e; b++)
+                SIMD_DISPATCH(n, e = launch_rotate<N>(c, nc, baby + (size_t)(b - 1) * CT, gCT, false, ext, keyN, KW,
+                                                      nullptr, nullptr, 0, baby + (size_t)b * CT, gCT, s));
+        }
         if (e) break;
         // inner products I_j per unit
-        {
-            const uint32_t thr = 256, words = L * n / 2;
-            simd_ptmac_kernel<<<dim3(U, (words + thr - 1) / thr), thr, 0, s>>>(c->md, n, c->p.d, g, m, baby, d_uq,
-                                                                             d_ublk, c->d_ptv, c->d_ptc, I);
-            c->launches++;
-            e = cudaGetLastError();
-            if (e) break;
-        }
-        // giant steps (Horner): acc = I_{m-1}; acc = rot_g(acc) + I_j
+        e = launch_ptmac(c, U, baby, d_uq, d_ublk, I, s);
+        if (e) break;
+        // giant steps (Horner): acc = I_{m-1}; acc = rot_g(acc) + I_j, j = m-2 .. 0
         const uint32_t *X = I + (size_t)(m - 1) * CT;
         size_t xs = (size_t)m * CT;
-        uint32_t *Y = accA;
-        for (int j = (int)m - 2; j >= 0 && !e; j--) {
-            SIMD_DISPATCH(n, e = launch_rotate<N>(c, U, X, xs, true, ext, keyN + KW / 2, KW, d_uq,
-                                                  I + (size_t)j * CT, (size_t)m * CT, Y, CT, s));
-            X = Y;
+        if (fused && m > 1) {
+            SIMD_DISPATCH(n, e = launch_chain<N>(c, U, true, keyN + KW / 2, KW, d_uq, X, xs, accB, accA, CT, 0,
+                                                 I + (size_t)(m - 2) * CT, (size_t)m * CT, -(ptrdiff_t)CT, m - 1, s));
+            X = ((m - 1) & 1) ? accA : accB;
             xs = CT;
-            Y = (Y == accA) ? accB : accA;
+        } else {
+            uint32_t *Y = accA;
+            for (int j = (int)m - 2; j >= 0 && !e; j--) {
+                SIMD_DISPATCH(n, e = launch_rotate<N>(c, U, X, xs, true, ext, keyN + KW / 2, KW, d_uq,
+                                                      I + (size_t)j * CT, (size_t)m * CT, Y, CT, s));
+                X = Y;
+                xs = CT;
+                Y = (Y == accA) ? accB : accA;
+            }
         }
         if (e) break;
         SIMD_DISPATCH(n, e = launch_switch<N>(c, U, X, xs, d_uoff, resp, s));
