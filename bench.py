@@ -581,8 +581,35 @@ def run_simd(args, rank, world, local_rank):
                       "api": "wally_simd_eval_batch with pinned host ciphertexts and keys copied in and responses "
                              "copied out inside the timed region"}
         del qh, kh, rh
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = simd_oracle_sample(w, srv, ents, ids, cts, keys)
     srv.close()
     return out
+
+
+def simd_oracle_sample(w, srv, ents, ids, cts, keys, nsample: int = 1):
+    """The SIMD oracle (oracle/wally_simd_oracle.c, single thread) timed on
+    `nsample` queries of the batch: its BSGS server computation and q_0
+    switch; the plaintext encoding (offline ServerInit) is not timed."""
+    from oracle import capi
+    mods = np.array(srv.moduli, dtype=np.uint32)
+    per = srv.block_entries
+    tot_t, tot_dots = 0.0, 0
+    for qi in range(nsample):
+        c = int(ids[qi])
+        ct = cts[qi].cpu().numpy().view(np.uint32)
+        key = keys[qi].cpu().numpy().view(np.uint32)
+        for b in range(-(-w.cluster_size // per)):
+            blk = ents[c][b * per:(b + 1) * per]
+            pt = np.stack([capi.simd_encode(x, w.t) for x in capi.simd_diagonal_slots(blk, w.n, w.t, w.d, srv.baby)])
+            t0 = time.perf_counter()
+            res = capi.simd_server(mods, w.t, w.d, srv.baby, ct, key[0], key[1], pt)
+            capi.simd_response(mods[:w.num_limbs], res)
+            tot_t += time.perf_counter() - t0
+            tot_dots += blk.shape[0]
+    return {"value": round(tot_dots / tot_t, 2), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{nsample} query of {w.name}-simd ({tot_dots} dot products) in {tot_t:.1f} s: the plain C "
+                      "SIMD oracle (BSGS server + q_0 switch, single thread); plaintext encoding not timed"}
 
 
 # ---------------------------------------------------------------------------
