@@ -1387,13 +1387,112 @@ struct LimbLoopP8 {
     }
 };
 
+// c1 of the n = 8192 pruned kernel: one limb of pointwise product, whole-CTA
+// inverse NTT and modulus-switch step, with the switch state (rtop, then the
+// accumulators) in tensor memory instead of registers: NA slots of 32
+// columns per thread (slot l holds acc[l]; slot 0 holds rtop after limb
+// L-1), so two CTAs fit per SM.
+template <int L, int J>
+struct LimbLoopP8C1 {
+    static constexpr int N = 8192;
+    static __device__ __forceinline__ void run(uint32_t (&a)[1][NttGeom<N>::V], const BatchArgs &ba,
+                                               const uint32_t *chat_q, const uint32_t *phat, int g,
+                                               const ChainCtx &cx, uint32_t tcol) {
+        using Gm = NttGeom<N>;
+        constexpr int V = Gm::V;
+        constexpr int NA = (L > 2) ? (L - 2) : 1;
+        const uint32_t q = ba.kp.q[J], q2 = ba.kp.q2[J];
+        const uint32_t *pv = phat + (size_t)J * 2 * N + (size_t)g * V;
+        const uint32_t *cv = chat_q + ((size_t)L + J) * N + (size_t)g * V;
+#pragma unroll
+        for (int v = 0; v < V / 4; v++) {
+            const uint4 p = ldg_stream(pv + 4 * v), pp = ldg_stream(pv + N + 4 * v), x = ldg_stream(cv + 4 * v);
+            a[0][4 * v + 0] = shoup_mul(x.x, p.x, pp.x, q);
+            a[0][4 * v + 1] = shoup_mul(x.y, p.y, pp.y, q);
+            a[0][4 * v + 2] = shoup_mul(x.z, p.z, pp.z, q);
+            a[0][4 * v + 3] = shoup_mul(x.w, p.w, pp.w, q);
+        }
+        intt_chain<N, 1>(a, cx.tw + (size_t)J * Gm::TW_LIMB, g, q, q2, cx.bufA, cx.bufB);
+        if constexpr (L > 1 && J < L - 1) tmem_wait_st_all();
+#pragma unroll
+        for (int c8 = 0; c8 < V / 8; c8++) {
+            uint32_t rt[8], ac[NA][8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                rt[k] = 0;
+#pragma unroll
+                for (int l = 0; l < NA; l++) ac[l][k] = 0;
+            }
+            if constexpr (L > 1 && J == L - 2) {
+                tmem_ld<8>(tcol + 8 * c8, rt);
+                tmem_wait_ld<8>(rt);
+            }
+            if constexpr (L > 2 && J < L - 2) {
+#pragma unroll
+                for (int l = 0; l <= J; l++) {
+                    tmem_ld<8>(tcol + 32 * l + 8 * c8, ac[l]);
+                    tmem_wait_ld<8>(ac[l]);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                uint32_t acc[NA];
+#pragma unroll
+                for (int l = 0; l < NA; l++) acc[l] = ac[l][k];
+                ms_elem<L, J, NA>(a[0][8 * c8 + k], rt[k], acc, ba.kp);
+#pragma unroll
+                for (int l = 0; l < NA; l++) ac[l][k] = acc[l];
+            }
+            if constexpr (L > 1 && J == L - 1) tmem_st<8>(tcol + 8 * c8, rt);
+            if constexpr (L > 2 && J > 0 && J <= L - 2) {
+#pragma unroll
+                for (int l = 0; l < J; l++) tmem_st<8>(tcol + 32 * l + 8 * c8, ac[l]);
+            }
+        }
+        if constexpr (J > 0) LimbLoopP8C1<L, J - 1>::run(a, ba, chat_q, phat, g, cx, tcol);
+    }
+};
+
+template <int L>
+__device__ __noinline__ uint32_t p8_c0_phase(const BatchArgs &ba, const uint32_t *chat_q, const uint32_t *phat, int g,
+                                             uint32_t *ybuf, uint32_t par, uint32_t *cst, int mu, const uint2 *s_mrg,
+                                             uint32_t *out_q) {
+    constexpr int N = 8192;
+    uint32_t a[NttGeom<N>::V];
+    LimbLoopP8<L, L - 1>::run(a, ba, chat_q, phat, g, ybuf, par, cst, mu, s_mrg);
+    if (g < 32) c0_write_results<N>(ba, out_q, ybuf + (par ^ 1u) * NttGeom<N>::T, g, mu);
+    return par;
+}
+
 template <int L, int FMT>
-__global__ void __launch_bounds__(NttGeom<8192>::T, 1) eval_kernel_p8(BatchArgs ba) {
+__device__ __noinline__ void p8_c1_phase(const BatchArgs &ba, const uint32_t *chat_q, const uint32_t *phat, int g,
+                                         ChainCtx cx, uint32_t tcol, uint32_t *out_q, const uint32_t *s_rmap) {
+    constexpr int N = 8192;
+    uint32_t a1[1][NttGeom<N>::V];
+    LimbLoopP8C1<L, L - 1>::run(a1, ba, chat_q, phat, g, cx, tcol);
+    write_component<N, FMT>(ba, out_q, a1[0], 1, g, s_rmap);
+}
+
+template <int L, int FMT>
+__global__ void __launch_bounds__(NttGeom<8192>::T, 2) eval_kernel_p8(BatchArgs ba) {
     constexpr int N = 8192;
     using Gm = NttGeom<N>;
     constexpr int NA = (L > 2) ? (L - 2) : 1;
     extern __shared__ uint32_t smem[];
     ChainCtx cx{ba.tw_inv, smem, smem + Gm::SMEM_WORDS, 0};
+    __shared__ BatchArgs s_ba;                         // the phases take it by reference (no local copy)
+    __shared__ uint32_t s_taddr;
+    const int warp = threadIdx.x / 32;
+    if (threadIdx.x == 0) s_ba = ba;
+    if (warp == 0) {   // 128 columns: NA x 32 per thread, warps w and w + 4 share a lane quadrant
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&s_taddr);
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(dst) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tcol = s_taddr + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 64);
     __shared__ uint32_t s_item[2];
     __shared__ uint32_t s_rmap[ResultMap<N>::WORDS];
     __shared__ uint32_t s_ybuf[2 * Gm::T];
@@ -1422,16 +1521,15 @@ __global__ void __launch_bounds__(NttGeom<8192>::T, 1) eval_kernel_p8(BatchArgs 
             const uint32_t qo = ba.perm[qi];
             uint32_t *out_q = ba.resp + ba.resp_off[qo] + (size_t)k * ba.wpp;
             const uint32_t *chat_q = ba.chat + (size_t)qo * 2 * L * N;
-            {
-                uint32_t a[Gm::V];
-                LimbLoopP8<L, L - 1>::run(a, ba, chat_q, phat, g, s_ybuf, par, s_cst, mu, s_mrg);
-                if (g < 32) c0_write_results<N>(ba, out_q, s_ybuf + (par ^ 1u) * Gm::T, g, mu);
-            }
-            EvalState<N, L, 1> st;
-            LimbLoop<N, L, 1, L - 1, false>::run(st, ba, chat_q, 1, phat, g, cx);
-            write_component<N, FMT>(ba, out_q, st.a[0], 1, g, s_rmap);
+            // two separately register-allocated phases (inlined together they spilled)
+            par = p8_c0_phase<L>(s_ba, chat_q, phat, g, s_ybuf, par, s_cst, mu, s_mrg, out_q);
+            p8_c1_phase<L, FMT>(s_ba, chat_q, phat, g, cx, tcol, out_q, s_rmap);
         }
     }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(s_taddr) : "memory");
 }
 
 template <int L, int FMT>
@@ -1443,7 +1541,7 @@ static cudaError_t launch_eval_p8(const BatchArgs &a, cudaStream_t s, int num_sm
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    eval_kernel_p8<L, FMT><<<num_sms, NttGeom<8192>::T, smem, s>>>(a);
+    eval_kernel_p8<L, FMT><<<num_sms * 2, NttGeom<8192>::T, smem, s>>>(a);
     return cudaGetLastError();
 }
 
