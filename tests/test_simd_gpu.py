@@ -141,3 +141,33 @@ def test_simd_errors(S):
     with pytest.raises(S.WallyError):
         S.SimdServer(n, L, d, moduli=m[:L] + [m[-1] + 2 * n * 1000])   # special prime not below q_0 / not prime
     assert srv.modmuls_per_query(1) > 0 and srv.launch_count() > 0
+
+
+def test_simd_edge_cases(S):
+    """empty batch, an empty cluster (no response blocks), a cluster of exactly one block, reload"""
+    n, L, d = 1024, 2, 16
+    rng = np.random.default_rng(8)
+    srv = S.SimdServer(n, L, d, baby=3)
+    per = srv.block_entries
+    clusters = [np.zeros((0, d), np.int8), rng.integers(-15, 16, size=(per, d)).astype(np.int8),
+                rng.integers(-15, 16, size=(per + 1, d)).astype(np.int8)]
+    srv.load_clusters(clusters)
+    assert [srv.blocks(c) for c in range(3)] == [0, 1, 2] and srv.blocks(3) == 0
+    mods = srv.moduli
+    # empty batch
+    got, off = _run(srv, np.zeros(0, np.uint32), _uniform(rng, mods[:L], (0, 2), n),
+                    _uniform(rng, mods, (0, 2, 2, L), n))
+    assert off.tolist() == [0]
+    ids = np.array([0, 2, 1, 0], np.uint32)
+    cts = _uniform(rng, mods[:L], (4, 2), n)
+    keys = _uniform(rng, mods, (4, 2, 2, L), n)
+    got, off = _run(srv, ids, cts, keys)
+    assert off.tolist() == [0, 0, 4 * n, 6 * n, 6 * n]
+    want = _oracle_responses(srv, clusters, ids, cts, keys)
+    assert len(want) == 3
+    for i, w in enumerate(want):
+        assert np.array_equal(got[i * 2 * n:(i + 1) * 2 * n].reshape(2, n), w), i
+    # reload a different database into the same context
+    srv.load_clusters(clusters[1:2])
+    got2, off2 = _run(srv, np.array([0], np.uint32), cts[2:3], keys[2:3])
+    assert np.array_equal(got2[:2 * n], got[4 * n:6 * n])
