@@ -1374,13 +1374,6 @@ struct LimbLoopP8 {
             a[4 * v + 2] = shoup_mul(x.z, p.z, pp.z, q);
             a[4 * v + 3] = shoup_mul(x.w, p.w, pp.w, q);
         }
-        {   // pull the next limb's operands toward L2 (after limb 0: c1's first limb)
-            const uint32_t *np = phat + (size_t)(J > 0 ? J - 1 : L - 1) * 2 * N + (size_t)g * V;
-            const uint32_t *nc = chat0 + (J > 0 ? (size_t)(J - 1) * N : (size_t)(2 * L - 1) * N) + (size_t)g * V;
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(np));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(np + N));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(nc));
-        }
         C0Pass0<N, 0, false>::run(a, ba.tw_inv + (size_t)J * Gm::TW_LIMB, g, q, q2);
         uint32_t *z = ybuf + par * Gm::T;
         z[g] = c0_mid<N>(a[V - 1], g, mu, s_mrg + J * 256, q, q2);
@@ -1418,12 +1411,6 @@ struct LimbLoopP8C1 {
             a[0][4 * v + 1] = shoup_mul(x.y, p.y, pp.y, q);
             a[0][4 * v + 2] = shoup_mul(x.z, p.z, pp.z, q);
             a[0][4 * v + 3] = shoup_mul(x.w, p.w, pp.w, q);
-        }
-        if constexpr (J > 0) {   // pull the next limb's operands toward L2
-            const uint32_t *np = phat + (size_t)(J - 1) * 2 * N + (size_t)g * V;
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(np));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(np + N));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(chat_q + ((size_t)L + J - 1) * N + (size_t)g * V));
         }
         intt_chain<N, 1>(a, cx.tw + (size_t)J * Gm::TW_LIMB, g, q, q2, cx.bufA, cx.bufB);
         if constexpr (L > 1 && J < L - 1) tmem_wait_st_all();
@@ -1554,7 +1541,7 @@ static cudaError_t launch_eval_p8(const BatchArgs &a, cudaStream_t s, int num_sm
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    eval_kernel_p8<L, FMT><<<num_sms * 2, NttGeom<8192>::T, smem, s>>>(a);
+    eval_kernel_p8<L, FMT><<<num_sms * 2, NttGeom<8192>::T, smem, s>>>(a);   // two CTAs per SM
     return cudaGetLastError();
 }
 
