@@ -544,7 +544,7 @@ def run_simd(args, rank, world, local_rank):
                 "peak_basis": f"{SM_COUNT} SMs x {MODMUL_PER_CLK_PER_SM:.0f} Shoup modmul/clk/SM x {sm_max:.0f} MHz"}
     out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-           "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "u32",
+           "scaling": "strong", "vs_baseline": None, "dtype": "u32",
            "data": "synthetic (seeded; query ciphertexts and rotation keys are uniform RNS residues)",
            "path": "simd (SURVEY.md 8(f)-3: diagonal packing + BSGS rotations, hybrid key switching)",
            "config": {"workload": w.name + "-simd", "description": w.description, "n": w.n, "limbs": w.num_limbs,
