@@ -1355,64 +1355,67 @@ __device__ __forceinline__ void c0_tail_fast8(uint32_t *z, uint32_t *cst, const 
     __syncwarp();
 }
 
+// One limb of both components, merged (n = 8192): the operands are streamed
+// in chunks of four values, so the plaintext is loaded once for c0 and c1;
+// c0's pass 0 (Y outputs only) runs as a reduction tree over the chunks
+// (stage s block b combines the last elements of its two halves, exactly
+// as C0Pass0), leaving one value per thread for the shuffle stages; c1 goes
+// through the whole-CTA inverse NTT and the switch step (state in TMEM);
+// c0's tail runs on warp 0 after c1's transform (whose barriers publish z).
 template <int L, int J>
-struct LimbLoopP8 {
+struct LimbLoopP8M {
     static constexpr int N = 8192;
-    static __device__ __forceinline__ void run(uint32_t (&a)[NttGeom<N>::V], const BatchArgs &ba,
-                                               const uint32_t *chat0, const uint32_t *phat, int g, uint32_t *ybuf,
-                                               uint32_t &par, uint32_t *cst, int mu, const uint2 *s_mrg) {
+    static __device__ __forceinline__ void run(uint32_t (&a)[1][NttGeom<N>::V], const BatchArgs &ba,
+                                               const uint32_t *chat_q, const uint32_t *phat, int g,
+                                               const ChainCtx &cx, uint32_t tcol, uint32_t *ybuf, uint32_t &par,
+                                               uint32_t *cst, int mu, const uint2 *s_mrg) {
         using Gm = NttGeom<N>;
-        constexpr int V = Gm::V;
+        constexpr int V = Gm::V, T = Gm::T;
+        static_assert(V == 32, "the c0 tree assumes 32 values per thread");
+        constexpr int NA = (L > 2) ? (L - 2) : 1;
         const uint32_t q = ba.kp.q[J], q2 = ba.kp.q2[J];
-        const uint32_t *pv = phat + (size_t)J * 2 * N + (size_t)g * V;
-        const uint32_t *cv = chat0 + (size_t)J * N + (size_t)g * V;
+        const uint4 *pv = reinterpret_cast<const uint4 *>(phat + (size_t)J * 2 * N + (size_t)g * V);
+        const uint4 *ppv = reinterpret_cast<const uint4 *>(phat + (size_t)J * 2 * N + N + (size_t)g * V);
+        const uint4 *c0v = reinterpret_cast<const uint4 *>(chat_q + (size_t)J * N + (size_t)g * V);
+        const uint4 *c1v = reinterpret_cast<const uint4 *>(chat_q + ((size_t)L + J) * N + (size_t)g * V);
+        const uint4 *t4 = reinterpret_cast<const uint4 *>(ba.tw_inv + (size_t)J * Gm::TW_LIMB) + g;
+        auto tw = [&](int slot) -> uint2 { return __ldg(reinterpret_cast<const uint2 *>(t4 + (slot / 2) * T) + (slot % 2)); };
+        auto yo = [&](uint32_t X, uint32_t Y, uint2 w) { return shoup_mul(X - Y + q2, w.x, w.y, q); };
+        uint32_t l2 = 0, l3 = 0, l4 = 0, y = 0;
 #pragma unroll
-        for (int v = 0; v < V / 4; v++) {
-            const uint4 p = ldg_stream(pv + 4 * v), pp = ldg_stream(pv + N + 4 * v), x = ldg_stream(cv + 4 * v);
-            a[4 * v + 0] = shoup_mul(x.x, p.x, pp.x, q);
-            a[4 * v + 1] = shoup_mul(x.y, p.y, pp.y, q);
-            a[4 * v + 2] = shoup_mul(x.z, p.z, pp.z, q);
-            a[4 * v + 3] = shoup_mul(x.w, p.w, pp.w, q);
+        for (int c = 0; c < 8; c++) {
+            const uint4 p = ldg_stream(pv + c), pp = ldg_stream(ppv + c), x0 = ldg_stream(c0v + c),
+                        x1 = ldg_stream(c1v + c);
+            a[0][4 * c + 0] = shoup_mul(x1.x, p.x, pp.x, q);
+            a[0][4 * c + 1] = shoup_mul(x1.y, p.y, pp.y, q);
+            a[0][4 * c + 2] = shoup_mul(x1.z, p.z, pp.z, q);
+            a[0][4 * c + 3] = shoup_mul(x1.w, p.w, pp.w, q);
+            const uint32_t y0 = shoup_mul(x0.x, p.x, pp.x, q), y1 = shoup_mul(x0.y, p.y, pp.y, q);
+            const uint32_t y2 = shoup_mul(x0.z, p.z, pp.z, q), y3 = shoup_mul(x0.w, p.w, pp.w, q);
+            const uint4 w0 = __ldg(t4 + c * T);                       // stage 0, blocks 2c, 2c + 1
+            const uint32_t u0 = yo(y0, y1, make_uint2(w0.x, w0.y)), u1 = yo(y2, y3, make_uint2(w0.z, w0.w));
+            const uint32_t v = yo(u0, u1, tw(16 + c));                // stage 1, block c
+            if (c % 2 == 0) {
+                l2 = v;
+            } else {
+                const uint32_t v2 = yo(l2, v, tw(24 + c / 2));         // stage 2, block c / 2
+                if ((c / 2) % 2 == 0) {
+                    l3 = v2;
+                } else {
+                    const uint32_t v3 = yo(l3, v2, tw(28 + c / 4));    // stage 3, block c / 4
+                    if (c / 4 == 0) l4 = v3;
+                    else y = yo(l4, v3, tw(30));                       // stage 4
+                }
+            }
         }
-        C0Pass0<N, 0, false>::run(a, ba.tw_inv + (size_t)J * Gm::TW_LIMB, g, q, q2);
-        uint32_t *z = ybuf + par * Gm::T;
-        z[g] = c0_mid<N>(a[V - 1], g, mu, s_mrg + J * 256, q, q2);
-        __syncthreads();
+        uint32_t *z = ybuf + par * T;
+        z[g] = c0_mid<N>(y, g, mu, s_mrg + J * 256, q, q2);
+        intt_chain<N, 1>(a, cx.tw + (size_t)J * Gm::TW_LIMB, g, q, q2, cx.bufA, cx.bufB);
         if (g < 32) {
             if (mu == 9) c0_tail_fast8<L, J>(z, cst, s_mrg + J * 256, g, ba.kp);
             else c0_tail<N, L, J>(z, cst, s_mrg + J * 256, g, mu, ba.kp);
         }
         par ^= 1u;
-        if constexpr (J > 0) LimbLoopP8<L, J - 1>::run(a, ba, chat0, phat, g, ybuf, par, cst, mu, s_mrg);
-    }
-};
-
-// c1 of the n = 8192 pruned kernel: one limb of pointwise product, whole-CTA
-// inverse NTT and modulus-switch step, with the switch state (rtop, then the
-// accumulators) in tensor memory instead of registers: NA slots of 32
-// columns per thread (slot l holds acc[l]; slot 0 holds rtop after limb
-// L-1), so two CTAs fit per SM.
-template <int L, int J>
-struct LimbLoopP8C1 {
-    static constexpr int N = 8192;
-    static __device__ __forceinline__ void run(uint32_t (&a)[1][NttGeom<N>::V], const BatchArgs &ba,
-                                               const uint32_t *chat_q, const uint32_t *phat, int g,
-                                               const ChainCtx &cx, uint32_t tcol) {
-        using Gm = NttGeom<N>;
-        constexpr int V = Gm::V;
-        constexpr int NA = (L > 2) ? (L - 2) : 1;
-        const uint32_t q = ba.kp.q[J], q2 = ba.kp.q2[J];
-        const uint32_t *pv = phat + (size_t)J * 2 * N + (size_t)g * V;
-        const uint32_t *cv = chat_q + ((size_t)L + J) * N + (size_t)g * V;
-#pragma unroll
-        for (int v = 0; v < V / 4; v++) {
-            const uint4 p = ldg_stream(pv + 4 * v), pp = ldg_stream(pv + N + 4 * v), x = ldg_stream(cv + 4 * v);
-            a[0][4 * v + 0] = shoup_mul(x.x, p.x, pp.x, q);
-            a[0][4 * v + 1] = shoup_mul(x.y, p.y, pp.y, q);
-            a[0][4 * v + 2] = shoup_mul(x.z, p.z, pp.z, q);
-            a[0][4 * v + 3] = shoup_mul(x.w, p.w, pp.w, q);
-        }
-        intt_chain<N, 1>(a, cx.tw + (size_t)J * Gm::TW_LIMB, g, q, q2, cx.bufA, cx.bufB);
         if constexpr (L > 1 && J < L - 1) tmem_wait_st_all();
 #pragma unroll
         for (int c8 = 0; c8 < V / 8; c8++) {
@@ -1449,29 +1452,10 @@ struct LimbLoopP8C1 {
                 for (int l = 0; l < J; l++) tmem_st<8>(tcol + 32 * l + 8 * c8, ac[l]);
             }
         }
-        if constexpr (J > 0) LimbLoopP8C1<L, J - 1>::run(a, ba, chat_q, phat, g, cx, tcol);
+        if constexpr (J > 0)
+            LimbLoopP8M<L, J - 1>::run(a, ba, chat_q, phat, g, cx, tcol, ybuf, par, cst, mu, s_mrg);
     }
 };
-
-template <int L>
-__device__ __noinline__ uint32_t p8_c0_phase(const BatchArgs &ba, const uint32_t *chat_q, const uint32_t *phat, int g,
-                                             uint32_t *ybuf, uint32_t par, uint32_t *cst, int mu, const uint2 *s_mrg,
-                                             uint32_t *out_q) {
-    constexpr int N = 8192;
-    uint32_t a[NttGeom<N>::V];
-    LimbLoopP8<L, L - 1>::run(a, ba, chat_q, phat, g, ybuf, par, cst, mu, s_mrg);
-    if (g < 32) c0_write_results<N>(ba, out_q, ybuf + (par ^ 1u) * NttGeom<N>::T, g, mu);
-    return par;
-}
-
-template <int L, int FMT>
-__device__ __noinline__ void p8_c1_phase(const BatchArgs &ba, const uint32_t *chat_q, const uint32_t *phat, int g,
-                                         ChainCtx cx, uint32_t tcol, uint32_t *out_q, const uint32_t *s_rmap) {
-    constexpr int N = 8192;
-    uint32_t a1[1][NttGeom<N>::V];
-    LimbLoopP8C1<L, L - 1>::run(a1, ba, chat_q, phat, g, cx, tcol);
-    write_component<N, FMT>(ba, out_q, a1[0], 1, g, s_rmap);
-}
 
 template <int L, int FMT>
 __global__ void __launch_bounds__(NttGeom<8192>::T, 2) eval_kernel_p8(BatchArgs ba) {
@@ -1480,7 +1464,7 @@ __global__ void __launch_bounds__(NttGeom<8192>::T, 2) eval_kernel_p8(BatchArgs 
     constexpr int NA = (L > 2) ? (L - 2) : 1;
     extern __shared__ uint32_t smem[];
     ChainCtx cx{ba.tw_inv, smem, smem + Gm::SMEM_WORDS, 0};
-    __shared__ BatchArgs s_ba;                         // the phases take it by reference (no local copy)
+    __shared__ BatchArgs s_ba;     // the limb loop reads the arguments from here (fewer spills than param space)
     __shared__ uint32_t s_taddr;
     const int warp = threadIdx.x / 32;
     if (threadIdx.x == 0) s_ba = ba;
@@ -1521,9 +1505,10 @@ __global__ void __launch_bounds__(NttGeom<8192>::T, 2) eval_kernel_p8(BatchArgs 
             const uint32_t qo = ba.perm[qi];
             uint32_t *out_q = ba.resp + ba.resp_off[qo] + (size_t)k * ba.wpp;
             const uint32_t *chat_q = ba.chat + (size_t)qo * 2 * L * N;
-            // two separately register-allocated phases (inlined together they spilled)
-            par = p8_c0_phase<L>(s_ba, chat_q, phat, g, s_ybuf, par, s_cst, mu, s_mrg, out_q);
-            p8_c1_phase<L, FMT>(s_ba, chat_q, phat, g, cx, tcol, out_q, s_rmap);
+            uint32_t a1[1][Gm::V];
+            LimbLoopP8M<L, L - 1>::run(a1, s_ba, chat_q, phat, g, cx, tcol, s_ybuf, par, s_cst, mu, s_mrg);
+            if (g < 32) c0_write_results<N>(s_ba, out_q, s_ybuf + (par ^ 1u) * Gm::T, g, mu);
+            write_component<N, FMT>(s_ba, out_q, a1[0], 1, g, s_rmap);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
