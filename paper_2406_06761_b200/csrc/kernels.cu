@@ -1382,10 +1382,16 @@ struct LimbLoopP8M {
         auto tw = [&](int slot) -> uint2 { return __ldg(reinterpret_cast<const uint2 *>(t4 + (slot / 2) * T) + (slot % 2)); };
         auto yo = [&](uint32_t X, uint32_t Y, uint2 w) { return shoup_mul(X - Y + q2, w.x, w.y, q); };
         uint32_t l2 = 0, l3 = 0, l4 = 0, y = 0;
+        uint4 np = ldg_stream(pv), npp = ldg_stream(ppv), nx0 = ldg_stream(c0v), nx1 = ldg_stream(c1v);
 #pragma unroll
         for (int c = 0; c < 8; c++) {
-            const uint4 p = ldg_stream(pv + c), pp = ldg_stream(ppv + c), x0 = ldg_stream(c0v + c),
-                        x1 = ldg_stream(c1v + c);
+            const uint4 p = np, pp = npp, x0 = nx0, x1 = nx1;
+            if (c + 1 < 8) {     // the next chunk's loads fly while this chunk computes
+                np = ldg_stream(pv + c + 1);
+                npp = ldg_stream(ppv + c + 1);
+                nx0 = ldg_stream(c0v + c + 1);
+                nx1 = ldg_stream(c1v + c + 1);
+            }
             a[0][4 * c + 0] = shoup_mul(x1.x, p.x, pp.x, q);
             a[0][4 * c + 1] = shoup_mul(x1.y, p.y, pp.y, q);
             a[0][4 * c + 2] = shoup_mul(x1.z, p.z, pp.z, q);
