@@ -1368,7 +1368,7 @@ struct LimbLoopP8M {
     static __device__ __forceinline__ void run(uint32_t (&a)[1][NttGeom<N>::V], const BatchArgs &ba,
                                                const uint32_t *chat_q, const uint32_t *phat, int g,
                                                const ChainCtx &cx, uint32_t tcol, uint32_t *ybuf, uint32_t &par,
-                                               uint32_t *cst, int mu, const uint2 *s_mrg) {
+                                               uint32_t *cst, int mu, const uint2 *s_mrg, uint4 (&pre)[4]) {
         using Gm = NttGeom<N>;
         constexpr int V = Gm::V, T = Gm::T;
         static_assert(V == 32, "the c0 tree assumes 32 values per thread");
@@ -1382,7 +1382,7 @@ struct LimbLoopP8M {
         auto tw = [&](int slot) -> uint2 { return __ldg(reinterpret_cast<const uint2 *>(t4 + (slot / 2) * T) + (slot % 2)); };
         auto yo = [&](uint32_t X, uint32_t Y, uint2 w) { return shoup_mul(X - Y + q2, w.x, w.y, q); };
         uint32_t l2 = 0, l3 = 0, l4 = 0, y = 0;
-        uint4 np = ldg_stream(pv), npp = ldg_stream(ppv), nx0 = ldg_stream(c0v), nx1 = ldg_stream(c1v);
+        uint4 np = pre[0], npp = pre[1], nx0 = pre[2], nx1 = pre[3];
 #pragma unroll
         for (int c = 0; c < 8; c++) {
             const uint4 p = np, pp = npp, x0 = nx0, x1 = nx1;
@@ -1416,6 +1416,13 @@ struct LimbLoopP8M {
         }
         uint32_t *z = ybuf + par * T;
         z[g] = c0_mid<N>(y, g, mu, s_mrg + J * 256, q, q2);
+        if constexpr (J > 0) {   // the next limb's first chunk flies during this limb's transform
+            const uint32_t *pn = phat + (size_t)(J - 1) * 2 * N + (size_t)g * V;
+            pre[0] = ldg_stream(pn);
+            pre[1] = ldg_stream(pn + N);
+            pre[2] = ldg_stream(chat_q + (size_t)(J - 1) * N + (size_t)g * V);
+            pre[3] = ldg_stream(chat_q + ((size_t)L + J - 1) * N + (size_t)g * V);
+        }
         intt_chain<N, 1>(a, cx.tw + (size_t)J * Gm::TW_LIMB, g, q, q2, cx.bufA, cx.bufB);
         if (g < 32) {
             if (mu == 9) c0_tail_fast8<L, J>(z, cst, s_mrg + J * 256, g, ba.kp);
@@ -1459,7 +1466,7 @@ struct LimbLoopP8M {
             }
         }
         if constexpr (J > 0)
-            LimbLoopP8M<L, J - 1>::run(a, ba, chat_q, phat, g, cx, tcol, ybuf, par, cst, mu, s_mrg);
+            LimbLoopP8M<L, J - 1>::run(a, ba, chat_q, phat, g, cx, tcol, ybuf, par, cst, mu, s_mrg, pre);
     }
 };
 
@@ -1512,7 +1519,15 @@ __global__ void __launch_bounds__(NttGeom<8192>::T, 2) eval_kernel_p8(BatchArgs 
             uint32_t *out_q = ba.resp + ba.resp_off[qo] + (size_t)k * ba.wpp;
             const uint32_t *chat_q = ba.chat + (size_t)qo * 2 * L * N;
             uint32_t a1[1][Gm::V];
-            LimbLoopP8M<L, L - 1>::run(a1, s_ba, chat_q, phat, g, cx, tcol, s_ybuf, par, s_cst, mu, s_mrg);
+            uint4 pre[4];
+            {
+                const uint32_t *pn = phat + (size_t)(L - 1) * 2 * N + (size_t)g * Gm::V;
+                pre[0] = ldg_stream(pn);
+                pre[1] = ldg_stream(pn + N);
+                pre[2] = ldg_stream(chat_q + (size_t)(L - 1) * N + (size_t)g * Gm::V);
+                pre[3] = ldg_stream(chat_q + (2 * (size_t)L - 1) * N + (size_t)g * Gm::V);
+            }
+            LimbLoopP8M<L, L - 1>::run(a1, s_ba, chat_q, phat, g, cx, tcol, s_ybuf, par, s_cst, mu, s_mrg, pre);
             if (g < 32) c0_write_results<N>(s_ba, out_q, s_ybuf + (par ^ 1u) * Gm::T, g, mu);
             write_component<N, FMT>(s_ba, out_q, a1[0], 1, g, s_rmap);
         }
