@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(NttGeom<N>::T) simd_modup_kernel(Mods md, cons
 // [2 comps][L digits][M][N].
 // ---------------------------------------------------------------------------
 template <int N>
-__global__ void __launch_bounds__(NttGeom<N>::T) simd_moddown_kernel(
+__global__ void __launch_bounds__(NttGeom<N>::T, 2) simd_moddown_kernel(
     Mods md, const uint2 *__restrict__ twf, const uint2 *__restrict__ twi, const uint32_t *__restrict__ ext,
     const uint32_t *__restrict__ keys, size_t key_stride, const uint32_t *__restrict__ uq,
     const uint32_t *__restrict__ X, size_t xs, const uint32_t *__restrict__ perm, const uint32_t *__restrict__ add,
