@@ -104,6 +104,18 @@ int wally_simd_eval_batch(wally_simd_ctx *ctx, uint32_t nq, const uint32_t *clus
                           const uint32_t *keys, uint32_t *resp, uint64_t resp_words, uint64_t *resp_off,
                           void *stream);
 
+/* The same computation end to end from host memory (the serving call):
+ * query_ct, keys and resp are HOST buffers (pinned for overlap) with the
+ * layouts above.  The batch runs in sub-batches of `sub_batch` queries
+ * through double-buffered device staging: the inputs of sub-batch i+1 are
+ * copied in, and the responses of sub-batch i-1 copied out, on two copy
+ * streams while sub-batch i computes on `stream`.  Within a sub-batch the
+ * queries are evaluated in cluster order.  Returns after the last response
+ * has arrived in `resp`.  Errors as wally_simd_eval_batch. */
+int wally_simd_eval_batch_host(wally_simd_ctx *ctx, uint32_t nq, const uint32_t *cluster_ids,
+                               const uint32_t *query_ct, const uint32_t *keys, uint32_t *resp, uint64_t resp_words,
+                               uint64_t *resp_off, uint32_t sub_batch, void *stream);
+
 /* Algorithmic modular multiplications of one query with `blocks` response
  * blocks (the roofline unit): NTT butterflies, pointwise and
  * key-switch products, scalings and the final switch. */

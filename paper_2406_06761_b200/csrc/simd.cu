@@ -603,8 +603,15 @@ struct wally_simd_ctx {
     // workspace
     void *ws = nullptr;
     size_t ws_bytes = 0;
-    uint32_t *h_units = nullptr;                   // pinned unit tables
+    uint32_t *h_units = nullptr;                   // pinned unit tables, two slots
     size_t h_units_cap = 0;
+    cudaEvent_t tab_ev[2] = {nullptr, nullptr};    // upload of a slot completed
+    int tab_slot = 0;
+    // host-buffer path: staging, copy streams, events
+    void *stage = nullptr;
+    size_t stage_bytes = 0;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
     uint64_t launches = 0;
     std::string err;
 };
@@ -736,8 +743,18 @@ extern "C" void wally_simd_destroy(wally_simd_ctx *c) {
     cudaFree(c->d_slot_of);
     cudaFree(c->d_ptv);
     cudaFree(c->d_ptc);
+    cudaDeviceSynchronize();
     cudaFree(c->ws);
+    cudaFree(c->stage);
     cudaFreeHost(c->h_units);
+    for (int k = 0; k < 2; k++) {
+        if (c->tab_ev[k]) cudaEventDestroy(c->tab_ev[k]);
+        if (c->ev_in[k]) cudaEventDestroy(c->ev_in[k]);
+        if (c->ev_done[k]) cudaEventDestroy(c->ev_done[k]);
+        if (c->ev_out[k]) cudaEventDestroy(c->ev_out[k]);
+    }
+    if (c->h2d) cudaStreamDestroy(c->h2d);
+    if (c->d2h) cudaStreamDestroy(c->d2h);
     delete c;
 }
 
@@ -1053,49 +1070,45 @@ extern "C" int wally_simd_load_clusters(wally_simd_ctx *c, uint32_t n_clusters, 
     return WALLY_OK;
 }
 
-extern "C" int wally_simd_eval_batch(wally_simd_ctx *c, uint32_t nq, const uint32_t *ids, const uint32_t *query_ct,
-                                     const uint32_t *keys, uint32_t *resp, uint64_t resp_words, uint64_t *resp_off,
-                                     void *stream) {
-    if (!c) return WALLY_E_ARG;
-    if (nq && (!ids || !query_ct || !keys || !resp)) return sfail(c, WALLY_E_ARG, "eval_batch: null argument");
-    const uint32_t n = c->p.n, L = c->L, M = c->M, g = c->g, m = c->m;
-    std::vector<uint64_t> off(nq + 1, 0);
+#ifndef WALLY_SIMD_CHAIN
+#define WALLY_SIMD_CHAIN 1
+#endif
+
+// Response offsets (words) of a batch in input order; validates the ids.
+static int simd_offsets(wally_simd_ctx *c, uint32_t nq, const uint32_t *ids, std::vector<uint64_t> &off) {
+    off.assign(nq + 1, 0);
     uint64_t total_blocks = 0;
     for (uint32_t q = 0; q < nq; q++) {
         if (ids[q] >= c->n_clusters)
             return sfail(c, WALLY_E_UNKNOWN_CLUSTER, "query %u names cluster %u (loaded: %u)", q, ids[q], c->n_clusters);
-        off[q] = total_blocks * 2 * n;
+        off[q] = total_blocks * 2 * c->p.n;
         total_blocks += c->blk_num[ids[q]];
     }
-    off[nq] = total_blocks * 2 * n;
-    if (resp_off) std::copy(off.begin(), off.end(), resp_off);
-    if (resp_words < off[nq]) return sfail(c, WALLY_E_ARG, "resp_words %llu < %llu", (unsigned long long)resp_words,
-                                           (unsigned long long)off[nq]);
-    if (!nq) return WALLY_OK;
-    SCUDA(c, cudaSetDevice(c->device));
-    cudaStream_t s = (cudaStream_t)stream;
+    off[nq] = total_blocks * 2 * c->p.n;
+    return WALLY_OK;
+}
+
+// Workspace of the computation for batches of up to Qc queries / Uc units:
+// err word first, then baby [Qc][g][CT], keys [Qc][KW], ext [max(Qc,Uc)][EXT]
+// (n = 8192), I [Uc][m][CT], acc 2 x [Uc][CT], device unit tables.  Pinned
+// unit tables: two slots, each reused once its upload has completed.
+struct SimdWs {
+    uint32_t Qc, Uc;
+    uint32_t *err, *baby, *keyN, *ext, *I, *accA, *accB, *uq, *ublk, *uoff, *sel;
+    size_t w_tab;
+};
+
+static int simd_workspace(wally_simd_ctx *c, uint32_t nq, uint32_t max_blk, SimdWs &W) {
+    const uint32_t n = c->p.n, L = c->L, M = c->M, g = c->g, m = c->m;
     const size_t CT = (size_t)2 * L * n, KW = (size_t)2 * 2 * L * M * n, EXT = (size_t)L * M * n;
-    // queries are processed in cluster order (stable), so the units sharing a
-    // block's plaintexts are adjacent; responses stay in input order
-    std::vector<uint32_t> order(nq);
-    for (uint32_t q = 0; q < nq; q++) order[q] = q;
-    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return ids[a] < ids[b]; });
-    // chunk: at most Qc queries and Uc units (query-blocks)
-    uint32_t max_blk = 1;
-    for (uint32_t q = 0; q < nq; q++) max_blk = std::max(max_blk, c->blk_num[ids[q]]);
-    const uint32_t Qc = std::min<uint32_t>(nq, std::max<uint32_t>(1, (uint32_t)((2048ull * 4096) / n)));
-    const uint32_t Uc = Qc * max_blk;
-#ifndef WALLY_SIMD_CHAIN
-#define WALLY_SIMD_CHAIN 1
-#endif
+    W.Qc = std::min<uint32_t>(std::max<uint32_t>(nq, 1), std::max<uint32_t>(1, (uint32_t)((2048ull * 4096) / n)));
+    W.Uc = W.Qc * max_blk;
     const bool fused = WALLY_SIMD_CHAIN && n <= 4096;
-    // workspace: baby [Qc][g][CT], keys [Qc][KW], ext [max(Qc,Uc)][EXT] (n = 8192 only), I [Uc][m][CT],
-    // acc 2 x [Uc][CT], unit tables, err
-    const size_t w_baby = (size_t)Qc * g * CT, w_key = (size_t)Qc * KW;
-    const size_t w_ext = fused ? 0 : (size_t)std::max(Qc, Uc) * EXT;
-    const size_t w_I = (size_t)Uc * m * CT, w_acc = (size_t)Uc * CT;
-    const size_t w_tab = 3 * (size_t)Uc + Qc;
-    const size_t need = 4 * (w_baby + w_key + w_ext + w_I + 2 * w_acc + w_tab + 64);
+    const size_t w_baby = (size_t)W.Qc * g * CT, w_key = (size_t)W.Qc * KW;
+    const size_t w_ext = fused ? 0 : (size_t)std::max(W.Qc, W.Uc) * EXT;
+    const size_t w_I = (size_t)W.Uc * m * CT, w_acc = (size_t)W.Uc * CT;
+    W.w_tab = 3 * (size_t)W.Uc + W.Qc;
+    const size_t need = 4 * (64 + w_baby + w_key + w_ext + w_I + 2 * w_acc + W.w_tab);
     if (c->ws_bytes < need) {
         cudaFree(c->ws);
         c->ws = nullptr;
@@ -1103,24 +1116,57 @@ extern "C" int wally_simd_eval_batch(wally_simd_ctx *c, uint32_t nq, const uint3
         if (cudaMalloc(&c->ws, need) != cudaSuccess) return sfail(c, WALLY_E_OOM, "workspace (%zu bytes)", need);
         c->ws_bytes = need;
     }
-    if (c->h_units_cap < w_tab) {
+    if (c->h_units_cap < W.w_tab) {
+        for (auto &ev : c->tab_ev)
+            if (ev) cudaEventSynchronize(ev);
         cudaFreeHost(c->h_units);
         c->h_units = nullptr;
-        SCUDA(c, cudaMallocHost(&c->h_units, 4 * w_tab));
-        c->h_units_cap = w_tab;
+        SCUDA(c, cudaMallocHost(&c->h_units, 2 * 4 * W.w_tab));
+        c->h_units_cap = W.w_tab;
     }
+    for (auto &ev : c->tab_ev)
+        if (!ev) SCUDA(c, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     uint32_t *w = (uint32_t *)c->ws;
-    uint32_t *baby = w, *keyN = baby + w_baby, *ext = keyN + w_key, *I = ext + w_ext, *accA = I + w_I,
-             *accB = accA + w_acc, *d_uq = accB + w_acc, *d_ublk = d_uq + Uc, *d_uoff = d_ublk + Uc,
-             *d_sel = d_uoff + Uc, *d_err = d_sel + Qc;
-    SCUDA(c, cudaMemsetAsync(d_err, 0, 4, s));
+    W.err = w;
+    W.baby = w + 64;
+    W.keyN = W.baby + w_baby;
+    W.ext = W.keyN + w_key;
+    W.I = W.ext + w_ext;
+    W.accA = W.I + w_I;
+    W.accB = W.accA + w_acc;
+    W.uq = W.accB + w_acc;
+    W.ublk = W.uq + W.Uc;
+    W.uoff = W.ublk + W.Uc;
+    W.sel = W.uoff + W.Uc;
+    return WALLY_OK;
+}
+
+// The server computation of nq queries whose inputs are on the device;
+// off: response offsets (words, input order) relative to resp.  Everything
+// is stream-ordered on s; no host synchronisation except the reuse of a
+// pinned table slot.
+static int simd_eval_core(wally_simd_ctx *c, const SimdWs &W, uint32_t nq, const uint32_t *ids,
+                          const uint32_t *query_ct, const uint32_t *keys, uint32_t *resp, const uint64_t *off,
+                          cudaStream_t s) {
+    const uint32_t n = c->p.n, L = c->L, M = c->M, g = c->g, m = c->m;
+    const size_t CT = (size_t)2 * L * n, KW = (size_t)2 * 2 * L * M * n;
+    const bool fused = WALLY_SIMD_CHAIN && n <= 4096;
+    const uint32_t Qc = W.Qc, Uc = W.Uc;
+    // queries are processed in cluster order (stable), so the units sharing a
+    // block's plaintexts are adjacent; responses stay in input order
+    std::vector<uint32_t> order(nq);
+    for (uint32_t q = 0; q < nq; q++) order[q] = q;
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return ids[a] < ids[b]; });
+    uint32_t *baby = W.baby, *keyN = W.keyN, *ext = W.ext, *I = W.I, *accA = W.accA, *accB = W.accB;
     cudaError_t e = cudaSuccess;
     for (uint32_t q0 = 0; q0 < nq; q0 += Qc) {
         const uint32_t nc = std::min(Qc, nq - q0);
-        // unit tables of this chunk (pinned, uploaded in stream order)
+        // unit tables of this chunk: a pinned slot whose previous upload has completed
+        const int slot = c->tab_slot;
+        c->tab_slot ^= 1;
+        SCUDA(c, cudaEventSynchronize(c->tab_ev[slot]));
         uint32_t U = 0;
-        uint32_t *hq = c->h_units, *hb = hq + Uc, *ho = hb + Uc, *hs = ho + Uc;
-        SCUDA(c, cudaStreamSynchronize(s));     // the pinned tables of the previous chunk are consumed
+        uint32_t *hq = c->h_units + slot * W.w_tab, *hb = hq + Uc, *ho = hb + Uc, *hs = ho + Uc;
         for (uint32_t q = 0; q < nc; q++) {
             const uint32_t qi = order[q0 + q], cl = ids[qi];
             hs[q] = qi;
@@ -1132,13 +1178,14 @@ extern "C" int wally_simd_eval_batch(wally_simd_ctx *c, uint32_t nq, const uint3
                 ho[U] = (uint32_t)o;
             }
         }
-        SCUDA(c, cudaMemcpyAsync(d_uq, hq, 4 * w_tab, cudaMemcpyHostToDevice, s));
+        SCUDA(c, cudaMemcpyAsync(W.uq, hq, 4 * W.w_tab, cudaMemcpyHostToDevice, s));
+        SCUDA(c, cudaEventRecord(c->tab_ev[slot], s));
         const size_t gCT = (size_t)g * CT;
         // a2': NTT of the chunk's ciphertexts (-> baby_0) and keys
-        SIMD_DISPATCH(n, e = launch_ntt<N>(c, L, 2 * L, query_ct, CT, d_sel, baby, gCT, (size_t)nc * 2 * L, d_err, s));
+        SIMD_DISPATCH(n, e = launch_ntt<N>(c, L, 2 * L, query_ct, CT, W.sel, baby, gCT, (size_t)nc * 2 * L, W.err, s));
         if (e) break;
-        SIMD_DISPATCH(n, e = launch_ntt<N>(c, M, 2 * 2 * L * M, keys, KW, d_sel, keyN, KW,
-                                           (size_t)nc * 2 * 2 * L * M, d_err, s));
+        SIMD_DISPATCH(n, e = launch_ntt<N>(c, M, 2 * 2 * L * M, keys, KW, W.sel, keyN, KW,
+                                           (size_t)nc * 2 * 2 * L * M, W.err, s));
         if (e) break;
         // baby steps: baby_b = rot_1(baby_{b-1})
         if (fused) {
@@ -1151,20 +1198,20 @@ extern "C" int wally_simd_eval_batch(wally_simd_ctx *c, uint32_t nq, const uint3
         }
         if (e) break;
         // inner products I_j per unit
-        e = launch_ptmac(c, U, baby, d_uq, d_ublk, I, s);
+        e = launch_ptmac(c, U, baby, W.uq, W.ublk, I, s);
         if (e) break;
         // giant steps (Horner): acc = I_{m-1}; acc = rot_g(acc) + I_j, j = m-2 .. 0
         const uint32_t *X = I + (size_t)(m - 1) * CT;
         size_t xs = (size_t)m * CT;
         if (fused && m > 1) {
-            SIMD_DISPATCH(n, e = launch_chain<N>(c, U, true, keyN + KW / 2, KW, d_uq, X, xs, accB, accA, CT, 0,
+            SIMD_DISPATCH(n, e = launch_chain<N>(c, U, true, keyN + KW / 2, KW, W.uq, X, xs, accB, accA, CT, 0,
                                                  I + (size_t)(m - 2) * CT, (size_t)m * CT, -(ptrdiff_t)CT, m - 1, s));
             X = ((m - 1) & 1) ? accA : accB;
             xs = CT;
         } else {
             uint32_t *Y = accA;
             for (int j = (int)m - 2; j >= 0 && !e; j--) {
-                SIMD_DISPATCH(n, e = launch_rotate<N>(c, U, X, xs, true, ext, keyN + KW / 2, KW, d_uq,
+                SIMD_DISPATCH(n, e = launch_rotate<N>(c, U, X, xs, true, ext, keyN + KW / 2, KW, W.uq,
                                                       I + (size_t)j * CT, (size_t)m * CT, Y, CT, s));
                 X = Y;
                 xs = CT;
@@ -1172,12 +1219,119 @@ extern "C" int wally_simd_eval_batch(wally_simd_ctx *c, uint32_t nq, const uint3
             }
         }
         if (e) break;
-        SIMD_DISPATCH(n, e = launch_switch<N>(c, U, X, xs, d_uoff, resp, s));
+        SIMD_DISPATCH(n, e = launch_switch<N>(c, U, X, xs, W.uoff, resp, s));
         if (e) break;
     }
     if (e) return sfail(c, WALLY_E_CUDA, "eval launch: %s", cudaGetErrorString(e));
+    return WALLY_OK;
+}
+
+static uint32_t simd_max_blocks(const wally_simd_ctx *c, uint32_t nq, const uint32_t *ids) {
+    uint32_t mb = 1;
+    for (uint32_t q = 0; q < nq; q++) mb = std::max(mb, c->blk_num[ids[q]]);
+    return mb;
+}
+
+extern "C" int wally_simd_eval_batch(wally_simd_ctx *c, uint32_t nq, const uint32_t *ids, const uint32_t *query_ct,
+                                     const uint32_t *keys, uint32_t *resp, uint64_t resp_words, uint64_t *resp_off,
+                                     void *stream) {
+    if (!c) return WALLY_E_ARG;
+    if (nq && (!ids || !query_ct || !keys || !resp)) return sfail(c, WALLY_E_ARG, "eval_batch: null argument");
+    std::vector<uint64_t> off;
+    int rc = simd_offsets(c, nq, ids, off);
+    if (rc) return rc;
+    if (resp_off) std::copy(off.begin(), off.end(), resp_off);
+    if (resp_words < off[nq]) return sfail(c, WALLY_E_ARG, "resp_words %llu < %llu", (unsigned long long)resp_words,
+                                           (unsigned long long)off[nq]);
+    if (!nq) return WALLY_OK;
+    SCUDA(c, cudaSetDevice(c->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    SimdWs W;
+    rc = simd_workspace(c, nq, simd_max_blocks(c, nq, ids), W);
+    if (rc) return rc;
+    SCUDA(c, cudaMemsetAsync(W.err, 0, 4, s));
+    rc = simd_eval_core(c, W, nq, ids, query_ct, keys, resp, off.data(), s);
+    if (rc) return rc;
     uint32_t herr = 0;
-    SCUDA(c, cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, s));
+    SCUDA(c, cudaMemcpyAsync(&herr, W.err, 4, cudaMemcpyDeviceToHost, s));
+    SCUDA(c, cudaStreamSynchronize(s));
+    if (herr) return sfail(c, WALLY_E_RESIDUE, "an input residue is >= its modulus");
+    return WALLY_OK;
+}
+
+extern "C" int wally_simd_eval_batch_host(wally_simd_ctx *c, uint32_t nq, const uint32_t *ids,
+                                          const uint32_t *query_ct, const uint32_t *keys, uint32_t *resp,
+                                          uint64_t resp_words, uint64_t *resp_off, uint32_t sub_batch, void *stream) {
+    if (!c) return WALLY_E_ARG;
+    if (nq && (!ids || !query_ct || !keys || !resp)) return sfail(c, WALLY_E_ARG, "eval_batch_host: null argument");
+    if (!sub_batch) return sfail(c, WALLY_E_ARG, "eval_batch_host: sub_batch must be > 0");
+    std::vector<uint64_t> off;
+    int rc = simd_offsets(c, nq, ids, off);
+    if (rc) return rc;
+    if (resp_off) std::copy(off.begin(), off.end(), resp_off);
+    if (resp_words < off[nq]) return sfail(c, WALLY_E_ARG, "resp_words %llu < %llu", (unsigned long long)resp_words,
+                                           (unsigned long long)off[nq]);
+    if (!nq) return WALLY_OK;
+    SCUDA(c, cudaSetDevice(c->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint32_t n = c->p.n, L = c->L, M = c->M;
+    const size_t CT = (size_t)2 * L * n, KW = (size_t)2 * 2 * L * M * n;
+    const uint32_t sb = std::min(sub_batch, nq), max_blk = simd_max_blocks(c, nq, ids);
+    SimdWs W;
+    rc = simd_workspace(c, sb, max_blk, W);
+    if (rc) return rc;
+    // double-buffered device staging: inputs and responses of two sub-batches
+    const size_t in_words = (size_t)sb * (CT + KW), out_words = (size_t)sb * max_blk * 2 * n;
+    const size_t need = 2 * 4 * (in_words + out_words);
+    if (c->stage_bytes < need) {
+        SCUDA(c, cudaStreamSynchronize(s));
+        cudaFree(c->stage);
+        c->stage = nullptr;
+        c->stage_bytes = 0;
+        if (cudaMalloc(&c->stage, need) != cudaSuccess) return sfail(c, WALLY_E_OOM, "host-path staging (%zu bytes)", need);
+        c->stage_bytes = need;
+    }
+    if (!c->h2d) {
+        SCUDA(c, cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+        SCUDA(c, cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+        for (int k = 0; k < 2; k++) {
+            SCUDA(c, cudaEventCreateWithFlags(&c->ev_in[k], cudaEventDisableTiming));
+            SCUDA(c, cudaEventCreateWithFlags(&c->ev_done[k], cudaEventDisableTiming));
+            SCUDA(c, cudaEventCreateWithFlags(&c->ev_out[k], cudaEventDisableTiming));
+        }
+    }
+    uint32_t *stage = (uint32_t *)c->stage;
+    SCUDA(c, cudaMemsetAsync(W.err, 0, 4, s));
+    // the first sub-batches must not overtake work already queued on s
+    SCUDA(c, cudaEventRecord(c->ev_done[0], s));
+    SCUDA(c, cudaEventRecord(c->ev_done[1], s));
+    SCUDA(c, cudaEventRecord(c->ev_out[0], s));
+    SCUDA(c, cudaEventRecord(c->ev_out[1], s));
+    for (uint32_t q0 = 0, it = 0; q0 < nq; q0 += sb, it++) {
+        const uint32_t nc = std::min(sb, nq - q0), k = it & 1;
+        uint32_t *ict = stage + k * (in_words + out_words), *ikey = ict + (size_t)sb * CT, *iout = ikey + (size_t)sb * KW;
+        // inputs of this sub-batch (copy stream), once the computation that read this slot is done
+        SCUDA(c, cudaStreamWaitEvent(c->h2d, c->ev_done[k], 0));
+        SCUDA(c, cudaMemcpyAsync(ict, query_ct + (size_t)q0 * CT, 4 * (size_t)nc * CT, cudaMemcpyHostToDevice, c->h2d));
+        SCUDA(c, cudaMemcpyAsync(ikey, keys + (size_t)q0 * KW, 4 * (size_t)nc * KW, cudaMemcpyHostToDevice, c->h2d));
+        SCUDA(c, cudaEventRecord(c->ev_in[k], c->h2d));
+        // computation (main stream), once the inputs arrived and this slot's responses left
+        SCUDA(c, cudaStreamWaitEvent(s, c->ev_in[k], 0));
+        SCUDA(c, cudaStreamWaitEvent(s, c->ev_out[k], 0));
+        std::vector<uint64_t> loc(nc + 1);
+        for (uint32_t q = 0; q <= nc; q++) loc[q] = off[q0 + q] - off[q0];
+        rc = simd_eval_core(c, W, nc, ids + q0, ict, ikey, iout, loc.data(), s);
+        if (rc) return rc;
+        SCUDA(c, cudaEventRecord(c->ev_done[k], s));
+        // responses (copy-out stream)
+        SCUDA(c, cudaStreamWaitEvent(c->d2h, c->ev_done[k], 0));
+        SCUDA(c, cudaMemcpyAsync(resp + off[q0], iout, 4 * (size_t)loc[nc], cudaMemcpyDeviceToHost, c->d2h));
+        SCUDA(c, cudaEventRecord(c->ev_out[k], c->d2h));
+    }
+    SCUDA(c, cudaStreamWaitEvent(s, c->ev_out[0], 0));
+    SCUDA(c, cudaStreamWaitEvent(s, c->ev_out[1], 0));
+    uint32_t herr = 0;
+    SCUDA(c, cudaMemcpyAsync(&herr, W.err, 4, cudaMemcpyDeviceToHost, s));
     SCUDA(c, cudaStreamSynchronize(s));
     if (herr) return sfail(c, WALLY_E_RESIDUE, "an input residue is >= its modulus");
     return WALLY_OK;

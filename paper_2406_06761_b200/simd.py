@@ -11,7 +11,7 @@ import numpy as np
 from .wally import WALLY_MAX_LIMBS, WallyError, _stream, lib
 
 EXPORTED = ["wally_simd_default_moduli", "wally_simd_create", "wally_simd_destroy", "wally_simd_last_error", "wally_simd_get_info",
-            "wally_simd_load_clusters", "wally_simd_blocks", "wally_simd_eval_batch",
+            "wally_simd_load_clusters", "wally_simd_blocks", "wally_simd_eval_batch", "wally_simd_eval_batch_host",
             "wally_simd_modmuls_per_query", "wally_simd_launch_count"]
 
 
@@ -38,6 +38,7 @@ def _sig():
         "wally_simd_load_clusters": ([vp, u32, P(u32), P(ctypes.c_int8), vp], ctypes.c_int),
         "wally_simd_blocks": ([vp, u32], u32),
         "wally_simd_eval_batch": ([vp, u32, P(u32), vp, vp, vp, u64, P(u64), vp], ctypes.c_int),
+        "wally_simd_eval_batch_host": ([vp, u32, P(u32), vp, vp, vp, u64, P(u64), u32, vp], ctypes.c_int),
         "wally_simd_modmuls_per_query": ([vp, u32], u64),
         "wally_simd_launch_count": ([vp], u64),
     }
@@ -124,6 +125,17 @@ class SimdServer:
                                          cts_dev.data_ptr(), keys_dev.data_ptr(), resp_dev.data_ptr(),
                                          resp_dev.numel(), off.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
                                          _stream(stream)), self.ctx)
+        return off
+
+    def eval_batch_host(self, ids, cts_host, keys_host, resp_host, sub_batch: int = 1024, stream=None) -> np.ndarray:
+        """The same from host buffers (torch CPU tensors, pinned for overlap); sub-batches are pipelined
+        through device staging.  Returns the response offsets [nq+1] (words)."""
+        ids = np.ascontiguousarray(ids, dtype=np.uint32)
+        off = np.zeros(ids.size + 1, dtype=np.uint64)
+        _check(lib.wally_simd_eval_batch_host(self.ctx, ids.size, ids.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
+                                              cts_host.data_ptr(), keys_host.data_ptr(), resp_host.data_ptr(),
+                                              resp_host.numel(), off.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                              sub_batch, _stream(stream)), self.ctx)
         return off
 
     def modmuls_per_query(self, blocks: int) -> int:

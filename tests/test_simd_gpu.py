@@ -171,3 +171,26 @@ def test_simd_edge_cases(S):
     srv.load_clusters(clusters[1:2])
     got2, off2 = _run(srv, np.array([0], np.uint32), cts[2:3], keys[2:3])
     assert np.array_equal(got2[:2 * n], got[4 * n:6 * n])
+
+
+def test_simd_host_path_matches_device_path(S):
+    """wally_simd_eval_batch_host (pipelined sub-batches from pinned host memory) gives the device path's bytes"""
+    n, L, d = 1024, 2, 16
+    rng = np.random.default_rng(21)
+    srv = S.SimdServer(n, L, d, baby=4)
+    clusters = [rng.integers(-15, 16, size=(s_, d)).astype(np.int8) for s_ in (40, 600, 300, 1)]
+    srv.load_clusters(clusters)
+    nq = 11
+    ids = rng.integers(0, len(clusters), size=nq).astype(np.uint32)
+    mods = srv.moduli
+    cts = _uniform(rng, mods[:L], (nq, 2), n)
+    keys = _uniform(rng, mods, (nq, 2, 2, L), n)
+    want, off = _run(srv, ids, cts, keys)
+    words = srv.response_words(ids)
+    for sub in (3, 4, 11, 64):
+        ch = torch.from_numpy(cts.view(np.int32)).pin_memory()
+        kh = torch.from_numpy(keys.view(np.int32)).pin_memory()
+        rh = torch.zeros(words, dtype=torch.int32).pin_memory()
+        off2 = srv.eval_batch_host(ids, ch, kh, rh, sub_batch=sub)
+        assert np.array_equal(off2, off)
+        assert np.array_equal(rh.numpy().view(np.uint32), want[:words]), sub
