@@ -194,3 +194,62 @@ def test_simd_host_path_matches_device_path(S):
         off2 = srv.eval_batch_host(ids, ch, kh, rh, sub_batch=sub)
         assert np.array_equal(off2, off)
         assert np.array_equal(rh.numpy().view(np.uint32), want[:words]), sub
+
+
+@pytest.mark.parametrize("name", ["c3", "c5"])
+def test_simd_full_config_sampled_bit_exact(S, name):
+    """The bench's launch configuration at full size (every cluster loaded, the whole query batch in one
+    call, uniform stand-in ciphertexts and keys as in bench.py): sampled queries -- the first, the last and
+    some in between, i.e. in different chunks -- are compared word for word with the oracle, and one query
+    is a real encryption under real rotation keys whose response must decrypt to its dot products."""
+    import synth
+    w = synth.WORKLOADS[name]
+    ents = synth.cluster_entries(w)
+    ids = synth.query_clusters(w)
+    srv = S.SimdServer(w.n, w.num_limbs, w.d, w.t)
+    srv.load_clusters([ents[c] for c in range(w.num_clusters)])
+    L, n = w.num_limbs, w.n
+    mods = np.array(srv.moduli, dtype=np.uint32)
+    cts = synth.uniform_ciphertexts_torch(w, srv.moduli[:L], device="cuda")
+    keys = synth.uniform_keys_torch(w, srv.moduli, device="cuda")
+    # one real query with real keys
+    rng = np.random.default_rng(5)
+    qreal = w.num_queries // 2
+    s = rng.integers(-1, 2, size=n).astype(np.int8)
+    qvec = rng.integers(-15, 16, size=w.d).astype(np.int32)
+
+    def key(k):
+        a = _uniform(rng, mods, (L,), n)
+        e = np.clip(np.rint(rng.normal(0, 3.2, size=(L, n))), -19, 19).astype(np.int32)
+        return capi.simd_keygen(mods, s, k, a, e)
+    ct_real = capi.encrypt(mods[:L], w.t, capi.simd_encode(capi.simd_query_slots(qvec, n, w.t), w.t).astype(np.int32),
+                           s, _uniform(rng, mods[:L], (), n),
+                           np.clip(np.rint(rng.normal(0, 3.2, size=n)), -19, 19).astype(np.int32))
+    key_real = np.stack([key(srv.galois[0]), key(srv.galois[1])])
+    cts[qreal] = torch.from_numpy(ct_real.view(np.int32)).cuda()
+    keys[qreal] = torch.from_numpy(key_real.view(np.int32)).cuda()
+    resp = torch.empty(srv.response_words(ids), dtype=torch.int32, device="cuda")
+    off = srv.eval_batch(ids, cts, keys, resp)
+    torch.cuda.synchronize()
+    per = srv.block_entries
+    sample = [0, qreal, w.num_queries - 1, int(rng.integers(1, w.num_queries - 1))]
+    for q in sample:
+        c = int(ids[q])
+        ct = cts[q].cpu().numpy().view(np.uint32)
+        kq = keys[q].cpu().numpy().view(np.uint32)
+        for b in range(srv.blocks(c)):
+            blk = ents[c][b * per:(b + 1) * per]
+            pt = np.stack([capi.simd_encode(x, w.t) for x in capi.simd_diagonal_slots(blk, n, w.t, w.d, srv.baby)])
+            want = capi.simd_response(mods[:L], capi.simd_server(mods, w.t, w.d, srv.baby, ct, kq[0], kq[1], pt))
+            o = int(off[q]) + b * 2 * n
+            got = resp[o:o + 2 * n].cpu().numpy().view(np.uint32).reshape(2, n)
+            assert np.array_equal(got, want), (name, q, b)
+            if q == qreal:
+                slots = capi.simd_decode(capi.decrypt_q0(int(mods[0]), w.t, got, s), w.t)
+                dots = (blk.astype(np.int64) @ qvec.astype(np.int64)) % w.t
+                R = srv.row_slices
+                for e in range(blk.shape[0]):
+                    sl, col = divmod(e, w.d)
+                    r, u = divmod(sl, R)
+                    assert slots[r * (n // 2) + u * w.d + col] == dots[e], (name, e)
+    srv.close()
