@@ -70,6 +70,12 @@ __device__ __forceinline__ void load_contig(const uint32_t *src, uint32_t (&a)[N
     }
 }
 
+__device__ __forceinline__ uint2 ldg_stream2(const void *p) {
+    uint2 r;
+    asm("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+    return r;
+}
+
 // [0, 4q) -> [0, q)
 __device__ __forceinline__ uint32_t canon4(uint32_t x, uint32_t q, uint32_t q2) { return csub(csub(x, q2), q); }
 
@@ -258,8 +264,8 @@ __global__ void __launch_bounds__(256) simd_ptmac_kernel(Mods md, uint32_t N, ui
         uint32_t a0x = 0, a0y = 0, a1x = 0, a1y = 0;   // lazy in [0, 2q)
         for (uint32_t b = 0; b < g && j * g + b < d; b++) {
             const size_t pi = pbase + (size_t)(j * g + b) * L * N;
-            const uint2 pv = *reinterpret_cast<const uint2 *>(ptv + pi);
-            const uint2 pc = *reinterpret_cast<const uint2 *>(ptc + pi);
+            const uint2 pv = ldg_stream2(ptv + pi);       // plaintexts stream through (L2-shared, not L1)
+            const uint2 pc = ldg_stream2(ptc + pi);
             const uint2 x0 = *reinterpret_cast<const uint2 *>(bq + (size_t)b * CT + w);
             const uint2 x1 = *reinterpret_cast<const uint2 *>(bq + (size_t)b * CT + (size_t)L * N + w);
             a0x = csub(a0x + shoup_mul(x0.x, pv.x, pc.x, q), q2);
