@@ -62,6 +62,9 @@ CASES = [
     dict(n=4096, L=3, d=48, g=7, sizes=[3000, 40], nq=3),          # d does not divide n/2, g does not divide d
     dict(n=2048, L=1, d=24, g=24, sizes=[50], nq=2),               # one limb, one giant step (no giant rotation)
     dict(n=8192, L=4, d=32, g=5, sizes=[300], nq=2),
+    dict(n=1024, L=3, d=512, g=1, sizes=[1024, 3], nq=2),          # d = n/2 (one slice per row), no baby steps
+    dict(n=1024, L=2, d=7, g=3, sizes=[1100], nq=3),               # odd d: R = 72 slices per row, two blocks
+    dict(n=2048, L=4, d=100, g=10, sizes=[1500], nq=2),            # L = 4 through the fused chain, g | d
 ]
 
 
