@@ -563,6 +563,9 @@ static int eval_impl(wally_ctx *c, uint32_t nq, const uint32_t *ids, const uint3
     a.compact = c->p.resp_format != WALLY_RESP_FULL;
     a.drop = c->p.resp_format == WALLY_RESP_COMPACT_DROP;
     a.nq = nq;
+    // a small batch would leave most thread groups idle with 8 queries per
+    // work item (c1: 32 items for 296 groups): one query per item instead
+    a.chunk = (nq < 4u * (uint32_t)c->num_sms) ? 1u : kQueryChunk;
     a.n_local = c->n_local;
     a.total_clusters = c->total_clusters;
     a.tw_fwd = c->d_tw_fwd;

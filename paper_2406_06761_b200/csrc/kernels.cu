@@ -142,10 +142,10 @@ __global__ void batch_count_kernel(const uint32_t *__restrict__ ids, uint32_t nq
 
 // One CTA of 1024 threads: exclusive scans of query counts (segment starts)
 // and of work items  P_c * ceil(count_c / chunk)  (item starts).
-__global__ void __launch_bounds__(1024) batch_scan_kernel(const uint32_t *__restrict__ counts, uint32_t n_local,
-                                                          const uint32_t *__restrict__ n_pt, uint32_t chunk,
-                                                          uint32_t *__restrict__ seg, uint32_t *__restrict__ item_start,
-                                                          uint32_t *__restrict__ misc) {
+__device__ __forceinline__ void batch_scan_block(const uint32_t *__restrict__ counts, uint32_t n_local,
+                                                 const uint32_t *__restrict__ n_pt, uint32_t chunk,
+                                                 uint32_t *__restrict__ seg, uint32_t *__restrict__ item_start,
+                                                 uint32_t *__restrict__ misc) {
     __shared__ uint32_t wsum_q[32], wsum_i[32];
     const uint32_t tid = threadIdx.x, per = (n_local + 1023) / 1024;
     const uint32_t b = tid * per, e = min(n_local, b + per);
@@ -187,6 +187,37 @@ __global__ void __launch_bounds__(1024) batch_scan_kernel(const uint32_t *__rest
     if (tid == 1023) {
         item_start[n_local] = oi;
         misc[kMiscTotalItems] = oi;
+    }
+}
+
+__global__ void __launch_bounds__(1024) batch_scan_kernel(const uint32_t *__restrict__ counts, uint32_t n_local,
+                                                          const uint32_t *__restrict__ n_pt, uint32_t chunk,
+                                                          uint32_t *__restrict__ seg, uint32_t *__restrict__ item_start,
+                                                          uint32_t *__restrict__ misc) {
+    batch_scan_block(counts, n_local, n_pt, chunk, seg, item_start, misc);
+}
+
+// The whole batcher in one CTA for small batches (one launch instead of
+// three): count, scan, scatter, separated by block barriers.
+__global__ void __launch_bounds__(1024) batch_small_kernel(const uint32_t *__restrict__ ids, uint32_t nq,
+                                                           const int32_t *__restrict__ local_of_cluster,
+                                                           uint32_t total_clusters, uint32_t *__restrict__ counts,
+                                                           uint32_t n_local, const uint32_t *__restrict__ n_pt,
+                                                           uint32_t chunk, uint32_t *__restrict__ seg,
+                                                           uint32_t *__restrict__ item_start, uint32_t *__restrict__ misc,
+                                                           uint32_t *__restrict__ fill, uint32_t *__restrict__ perm) {
+    for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
+        const uint32_t c = ids[q];
+        const int32_t li = c < total_clusters ? local_of_cluster[c] : -1;
+        if (li >= 0) atomicAdd(&counts[li], 1u);
+    }
+    __syncthreads();
+    batch_scan_block(counts, n_local, n_pt, chunk, seg, item_start, misc);
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
+        const uint32_t c = ids[q];
+        const int32_t li = c < total_clusters ? local_of_cluster[c] : -1;
+        if (li >= 0) perm[seg[li] + atomicAdd(&fill[li], 1u)] = q;
     }
 }
 
@@ -473,8 +504,8 @@ __device__ __forceinline__ void eval_item(const BatchArgs &ba, const ItemCursor 
     // (a hot cluster's queries can exceed L2; its plaintexts never do)
     const uint32_t P = ba.n_pt[li];
     const uint32_t ch = local / P, k = local % P;
-    const uint32_t qb = ba.seg[li] + ch * kQueryChunk;
-    const uint32_t qe = min(qb + kQueryChunk, ba.seg[li] + cnt);
+    const uint32_t qb = ba.seg[li] + ch * ba.chunk;
+    const uint32_t qe = min(qb + ba.chunk, ba.seg[li] + cnt);
     const uint32_t *phat = ba.store + (size_t)(ba.pt_base[li] + k) * L * 2 * N;
     for (uint32_t qi = qb; qi < qe; qi++) {
         const uint32_t qo = ba.perm[qi];
@@ -666,8 +697,8 @@ __device__ __forceinline__ void eval_item_tm(const BatchArgs &ba, const ItemCurs
     // (a hot cluster's queries can exceed L2; its plaintexts never do)
     const uint32_t P = ba.n_pt[li];
     const uint32_t ch = local / P, k = local % P;
-    const uint32_t qb = ba.seg[li] + ch * kQueryChunk;
-    const uint32_t qe = min(qb + kQueryChunk, ba.seg[li] + cnt);
+    const uint32_t qb = ba.seg[li] + ch * ba.chunk;
+    const uint32_t qe = min(qb + ba.chunk, ba.seg[li] + cnt);
     const uint32_t *phat = ba.store + (size_t)(ba.pt_base[li] + k) * L * 2 * N;
     // the item's plaintext slice -> TMEM (previous item's reads were waited on)
 #pragma unroll
@@ -1212,8 +1243,8 @@ __device__ __forceinline__ void eval_item_pr(const BatchArgs &ba, const ItemCurs
     const uint32_t local = item - cur.b;
     const uint32_t P = ba.n_pt[li];
     const uint32_t ch = local / P, k = local % P;
-    const uint32_t qb = ba.seg[li] + ch * kQueryChunk;
-    const uint32_t qe = min(qb + kQueryChunk, ba.seg[li] + cnt);
+    const uint32_t qb = ba.seg[li] + ch * ba.chunk;
+    const uint32_t qe = min(qb + ba.chunk, ba.seg[li] + cnt);
     const uint32_t *phat = ba.store + (size_t)(ba.pt_base[li] + k) * L * 2 * N;
 #pragma unroll
     for (int J = 0; J < L; J++) {
@@ -1511,8 +1542,8 @@ __global__ void __launch_bounds__(NttGeom<8192>::T, 2) eval_kernel_p8(BatchArgs 
         const uint32_t cnt = ba.counts[li];
         const uint32_t P = ba.n_pt[li];
         const uint32_t ch = (item - cur.b) / P, k = (item - cur.b) % P;
-        const uint32_t qb = ba.seg[li] + ch * kQueryChunk;
-        const uint32_t qe = min(qb + kQueryChunk, ba.seg[li] + cnt);
+        const uint32_t qb = ba.seg[li] + ch * ba.chunk;
+        const uint32_t qe = min(qb + ba.chunk, ba.seg[li] + cnt);
         const uint32_t *phat = ba.store + (size_t)(ba.pt_base[li] + k) * L * 2 * N;
         for (uint32_t qi = qb; qi < qe; qi++) {
             const uint32_t qo = ba.perm[qi];
@@ -1658,10 +1689,16 @@ cudaError_t launch_pack_rows(const uint32_t *index, const uint32_t *src, uint32_
 
 cudaError_t launch_batcher(const BatchArgs &a, cudaStream_t s, uint64_t *launches) {
     if (a.nq == 0) return cudaSuccess;
+    if (a.nq <= 4096) {
+        batch_small_kernel<<<1, 1024, 0, s>>>(a.ids, a.nq, a.local_of_cluster, a.total_clusters, a.counts, a.n_local,
+                                              a.n_pt, a.chunk, a.seg, a.item_start, a.misc, a.fill, a.perm);
+        *launches += 1;
+        return cudaGetLastError();
+    }
     const unsigned threads = 256;
     const unsigned blocks = (a.nq + threads - 1) / threads;
     batch_count_kernel<<<blocks, threads, 0, s>>>(a.ids, a.nq, a.local_of_cluster, a.total_clusters, a.counts);
-    batch_scan_kernel<<<1, 1024, 0, s>>>(a.counts, a.n_local, a.n_pt, kQueryChunk, a.seg, a.item_start, a.misc);
+    batch_scan_kernel<<<1, 1024, 0, s>>>(a.counts, a.n_local, a.n_pt, a.chunk, a.seg, a.item_start, a.misc);
     batch_scatter_kernel<<<blocks, threads, 0, s>>>(a.ids, a.nq, a.local_of_cluster, a.total_clusters, a.seg, a.fill,
                                                     a.perm);
     *launches += 3;

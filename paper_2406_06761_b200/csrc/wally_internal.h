@@ -51,6 +51,7 @@ struct BatchArgs {
     uint32_t compact;             // WALLY_RESP_COMPACT or _COMPACT_DROP (c0 at the result coefficients only)
     uint32_t drop;                // WALLY_RESP_COMPACT_DROP (c1 rounded to 2^6, 24-bit planes)
     uint32_t nq;
+    uint32_t chunk;               // queries per work item (kQueryChunk, or 1 for small batches)
     uint32_t n_local;
     uint32_t total_clusters;
     const uint2 *tw_fwd;          // [L][n] (w, w') psi^{brev(i)}
