@@ -121,6 +121,13 @@ int wally_simd_eval_batch_host(wally_simd_ctx *ctx, uint32_t nq, const uint32_t 
  * key-switch products, scalings and the final switch. */
 uint64_t wally_simd_modmuls_per_query(const wally_simd_ctx *ctx, uint32_t blocks);
 
+/* Rotation kernels: at n <= 4096 a chunk of at least `min_queries` queries
+ * (default: 2 per SM) runs each unit's whole chain of rotations in one CTA
+ * (simd_rot_chain_kernel); smaller chunks use the separate ModUp / ModDown
+ * kernels, which spread one rotation over L + 2 CTAs.  0 = always the
+ * chain, UINT32_MAX = never.  Results are identical either way. */
+int wally_simd_set_chain_threshold(wally_simd_ctx *ctx, uint32_t min_queries);
+
 /* Kernel launches issued by this context so far. */
 uint64_t wally_simd_launch_count(const wally_simd_ctx *ctx);
 

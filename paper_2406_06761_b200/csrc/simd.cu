@@ -597,6 +597,8 @@ using namespace wally::simd;
 struct wally_simd_ctx {
     wally_simd_params p{};
     int device = 0;
+    int num_sms = 148;
+    uint32_t chain_min_queries = 0;                // fused rotation chain from this many queries per chunk
     uint32_t L = 0, M = 0, g = 0, m = 0, R = 0, logn = 0;
     Mods md{};
     uint2 *d_twf = nullptr, *d_twi = nullptr;      // [M + 1][TW_LIMB] (index M: t)
@@ -790,6 +792,8 @@ extern "C" int wally_simd_create(const wally_simd_params *params, int device, wa
     wally_simd_ctx *c = new wally_simd_ctx();
     c->p = p;
     c->device = device;
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    c->chain_min_queries = 2u * (uint32_t)c->num_sms;
     c->L = L;
     c->M = L + 1;
     c->g = g;
@@ -891,6 +895,12 @@ extern "C" uint32_t wally_simd_blocks(const wally_simd_ctx *c, uint32_t cluster)
 }
 
 extern "C" uint64_t wally_simd_launch_count(const wally_simd_ctx *c) { return c ? c->launches : 0; }
+
+extern "C" int wally_simd_set_chain_threshold(wally_simd_ctx *c, uint32_t min_queries) {
+    if (!c) return WALLY_E_ARG;
+    c->chain_min_queries = min_queries;
+    return WALLY_OK;
+}
 
 // Algorithmic modmuls of one NTT of length n: (n/2) log2 n butterflies.
 static uint64_t s_ntt_mm(const wally_simd_ctx *c) { return (uint64_t)(c->p.n / 2) * c->logn; }
@@ -1080,6 +1090,13 @@ extern "C" int wally_simd_load_clusters(wally_simd_ctx *c, uint32_t n_clusters, 
 #define WALLY_SIMD_CHAIN 1
 #endif
 
+// The fused rotation chain runs one CTA per query (per block in the giant
+// steps); a batch with fewer queries than two per SM would leave most SMs
+// idle, so it uses the separate ModUp (L CTAs) / ModDown (2 CTAs) kernels.
+static bool simd_fused(const wally_simd_ctx *c, uint32_t nq) {
+    return WALLY_SIMD_CHAIN && c->p.n <= 4096 && nq >= c->chain_min_queries;
+}
+
 // Response offsets (words) of a batch in input order; validates the ids.
 static int simd_offsets(wally_simd_ctx *c, uint32_t nq, const uint32_t *ids, std::vector<uint64_t> &off) {
     off.assign(nq + 1, 0);
@@ -1109,7 +1126,7 @@ static int simd_workspace(wally_simd_ctx *c, uint32_t nq, uint32_t max_blk, Simd
     const size_t CT = (size_t)2 * L * n, KW = (size_t)2 * 2 * L * M * n, EXT = (size_t)L * M * n;
     W.Qc = std::min<uint32_t>(std::max<uint32_t>(nq, 1), std::max<uint32_t>(1, (uint32_t)((2048ull * 4096) / n)));
     W.Uc = W.Qc * max_blk;
-    const bool fused = WALLY_SIMD_CHAIN && n <= 4096;
+    const bool fused = simd_fused(c, W.Qc);
     const size_t w_baby = (size_t)W.Qc * g * CT, w_key = (size_t)W.Qc * KW;
     const size_t w_ext = fused ? 0 : (size_t)std::max(W.Qc, W.Uc) * EXT;
     const size_t w_I = (size_t)W.Uc * m * CT, w_acc = (size_t)W.Uc * CT;
@@ -1156,7 +1173,7 @@ static int simd_eval_core(wally_simd_ctx *c, const SimdWs &W, uint32_t nq, const
                           cudaStream_t s) {
     const uint32_t n = c->p.n, L = c->L, M = c->M, g = c->g, m = c->m;
     const size_t CT = (size_t)2 * L * n, KW = (size_t)2 * 2 * L * M * n;
-    const bool fused = WALLY_SIMD_CHAIN && n <= 4096;
+    const bool fused = simd_fused(c, W.Qc);
     const uint32_t Qc = W.Qc, Uc = W.Uc;
     // queries are processed in cluster order (stable), so the units sharing a
     // block's plaintexts are adjacent; responses stay in input order

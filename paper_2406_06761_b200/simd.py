@@ -12,7 +12,7 @@ from .wally import WALLY_MAX_LIMBS, WallyError, _stream, lib
 
 EXPORTED = ["wally_simd_default_moduli", "wally_simd_create", "wally_simd_destroy", "wally_simd_last_error", "wally_simd_get_info",
             "wally_simd_load_clusters", "wally_simd_blocks", "wally_simd_eval_batch", "wally_simd_eval_batch_host",
-            "wally_simd_modmuls_per_query", "wally_simd_launch_count"]
+            "wally_simd_modmuls_per_query", "wally_simd_launch_count", "wally_simd_set_chain_threshold"]
 
 
 class wally_simd_params(ctypes.Structure):
@@ -41,6 +41,7 @@ def _sig():
         "wally_simd_eval_batch_host": ([vp, u32, P(u32), vp, vp, vp, u64, P(u64), u32, vp], ctypes.c_int),
         "wally_simd_modmuls_per_query": ([vp, u32], u64),
         "wally_simd_launch_count": ([vp], u64),
+        "wally_simd_set_chain_threshold": ([vp, u32], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -140,6 +141,10 @@ class SimdServer:
 
     def modmuls_per_query(self, blocks: int) -> int:
         return int(lib.wally_simd_modmuls_per_query(self.ctx, blocks))
+
+    def set_chain_threshold(self, min_queries: int):
+        """0: always the fused rotation chain; 2**32-1: never (see include/wally_simd.h)."""
+        _check(lib.wally_simd_set_chain_threshold(self.ctx, min_queries), self.ctx)
 
     def launch_count(self) -> int:
         return int(lib.wally_simd_launch_count(self.ctx))

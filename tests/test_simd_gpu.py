@@ -68,11 +68,13 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("chain", [True, False], ids=["chain", "modup_moddown"])
 @pytest.mark.parametrize("cfg", CASES, ids=[f"n{c['n']}_L{c['L']}_d{c['d']}_g{c['g']}" for c in CASES])
-def test_simd_bit_exact_with_oracle(S, cfg):
+def test_simd_bit_exact_with_oracle(S, cfg, chain):
     n, L, d = cfg["n"], cfg["L"], cfg["d"]
     rng = np.random.default_rng(n + L + d)
     srv = S.SimdServer(n, L, d, baby=cfg["g"])
+    srv.set_chain_threshold(0 if chain else 2**32 - 1)
     clusters = [rng.integers(-15, 16, size=(s, d)).astype(np.int8) for s in cfg["sizes"]]
     srv.load_clusters(clusters)
     ids = rng.integers(0, len(clusters), size=cfg["nq"]).astype(np.uint32)
