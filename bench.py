@@ -197,7 +197,7 @@ def oracle_sample(w, moduli, ents, ids, cts_host_fn, seconds: float, seed: int =
     rng = np.random.default_rng(seed)
     cores = len(os.sched_getaffinity(0))
 
-    def run(npairs):
+    def run(npairs, threads=None):
         qsel = rng.integers(0, ids.size, size=npairs)
         ksel = rng.integers(0, P, size=npairs)
         uq, inv = np.unique(qsel, return_inverse=True)
@@ -208,7 +208,7 @@ def oracle_sample(w, moduli, ents, ids, cts_host_fn, seconds: float, seed: int =
         pp = np.array([pidx[(int(ids[q]), int(k))] for q, k in zip(qsel, ksel)], dtype=np.uint32)
         dots = int(sum(min(E, w.cluster_size - int(k) * E) for k in ksel))
         t0 = time.perf_counter()
-        _, used = capi.server_pairs(moduli, cts, pcs, inv.astype(np.uint32), pp, threads=cores)
+        _, used = capi.server_pairs(moduli, cts, pcs, inv.astype(np.uint32), pp, threads=threads or cores)
         dt = time.perf_counter() - t0
         return npairs, dots, dt, used
 
@@ -216,9 +216,13 @@ def oracle_sample(w, moduli, ents, ids, cts_host_fn, seconds: float, seed: int =
     rate = n0 / t0
     npairs = max(cores, int(rate * seconds))
     n1, d1, t1, used = run(npairs)
+    # the same oracle on one core, a sample of about 3 s
+    n2, d2, t2, _ = run(max(4, int(rate / max(used, 1) * 3.0)), threads=1)
     return {"value": d1 / t1, "unit": UNIT, "cores": int(used), "kind": "oracle",
+            "value_1core": round(d2 / t2, 2),
             "sample": f"{n1} random (query, plaintext) pairs of {w.name} ({d1} dot products) in {t1:.1f} s "
-                      f"with {used} OpenMP threads; plain C oracle, uint64 % arithmetic"}
+                      f"with {used} OpenMP threads; plain C oracle, uint64 % arithmetic; value_1core: {n2} pairs "
+                      f"in {t2:.1f} s on one thread"}
 
 
 # ---------------------------------------------------------------------------
