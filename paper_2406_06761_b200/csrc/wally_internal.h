@@ -16,7 +16,10 @@ namespace wally {
 constexpr int kMaxLimbs = WALLY_MAX_LIMBS;
 // Queries per work item of the fused kernel (a query chunk of one cluster
 // shares every staged plaintext).
-constexpr uint32_t kQueryChunk = 8;
+#ifndef WALLY_QUERY_CHUNK
+#define WALLY_QUERY_CHUNK 32
+#endif
+constexpr uint32_t kQueryChunk = WALLY_QUERY_CHUNK;
 
 // Per-limb constants, passed by value to every kernel (kernel parameter
 // space -> constant bank, uniform across the grid).
