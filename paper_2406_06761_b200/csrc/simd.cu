@@ -1089,6 +1089,9 @@ extern "C" int wally_simd_load_clusters(wally_simd_ctx *c, uint32_t n_clusters, 
 #ifndef WALLY_SIMD_CHAIN
 #define WALLY_SIMD_CHAIN 1
 #endif
+#ifndef WALLY_SIMD_CHUNK
+#define WALLY_SIMD_CHUNK 2048   // queries per chunk at n = 4096 (scaled by 4096 / n)
+#endif
 
 // The fused rotation chain runs one CTA per query (per block in the giant
 // steps); a batch with fewer queries than two per SM would leave most SMs
@@ -1124,7 +1127,7 @@ struct SimdWs {
 static int simd_workspace(wally_simd_ctx *c, uint32_t nq, uint32_t max_blk, SimdWs &W) {
     const uint32_t n = c->p.n, L = c->L, M = c->M, g = c->g, m = c->m;
     const size_t CT = (size_t)2 * L * n, KW = (size_t)2 * 2 * L * M * n, EXT = (size_t)L * M * n;
-    W.Qc = std::min<uint32_t>(std::max<uint32_t>(nq, 1), std::max<uint32_t>(1, (uint32_t)((2048ull * 4096) / n)));
+    W.Qc = std::min<uint32_t>(std::max<uint32_t>(nq, 1), std::max<uint32_t>(1, (uint32_t)((WALLY_SIMD_CHUNK * 4096ull) / n)));
     W.Uc = W.Qc * max_blk;
     const bool fused = simd_fused(c, W.Qc);
     const size_t w_baby = (size_t)W.Qc * g * CT, w_key = (size_t)W.Qc * KW;
