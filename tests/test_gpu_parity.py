@@ -114,6 +114,34 @@ EDGE = [
 ]
 
 
+@pytest.mark.parametrize("fmt", [0, 2], ids=["full", "compact_drop"])
+def test_multi_chunk_batch_bit_exact(fmt):
+    """A batch large enough for 32-query work items (>= 4 queries per SM) with one cluster
+    split over several chunks, including a ragged last chunk: every response word of a
+    sample of queries (first, last, chunk boundaries) against the oracle."""
+    n, L, d = 4096, 3, 128
+    rng = np.random.default_rng(77)
+    sizes = [130, 40, 300]
+    clusters = [rng.integers(-15, 16, size=(s_, d)).astype(np.int8) for s_ in sizes]
+    srv = H.make_server_ragged(n, L, d, clusters, resp_format=fmt)
+    qs = srv.moduli
+    nq = 700
+    ids = np.concatenate([np.zeros(101, np.uint32), rng.integers(1, 3, size=nq - 101).astype(np.uint32)])
+    rng.shuffle(ids)
+    cts = np.stack([np.stack([np.stack([rng.integers(0, q, size=n) for q in qs]) for _ in range(2)])
+                    for _ in range(nq)]).astype(np.uint32)
+    resp, off = H.run_batch(srv, ids, cts)
+    zeros = np.flatnonzero(ids == 0)
+    sample = sorted(set([0, nq - 1] + zeros[[0, 31, 32, 63, 64, 95, 96, 100]].tolist()))
+    pcs_by_c = [capi.encode_cluster(c, d, n) for c in clusters]
+    for q in sample:
+        c = int(ids[q])
+        P = pcs_by_c[c].shape[0]
+        want = H.oracle_pairs(qs, cts[q:q + 1], pcs_by_c[c], np.zeros(P), np.arange(P))
+        for k in range(P):
+            assert H.matches_oracle(H.response_of(resp, off, q, k, n, d, fmt), want[k], n, d, fmt), (q, k)
+
+
 @pytest.mark.parametrize("fmt", [0, 1, 2], ids=["full", "compact", "compact_drop"])
 @pytest.mark.parametrize("cfg", EDGE, ids=[f"n{c['n']}_L{c['L']}_d{c['d']}" for c in EDGE])
 def test_edge_cases_bit_exact(cfg, fmt):
