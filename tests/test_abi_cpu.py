@@ -78,3 +78,33 @@ def test_create_validates_params_before_touching_the_device(wl):
     if not has_gpu:
         assert wl.lib.wally_create(ctypes.byref(p), 0, ctypes.byref(h)) == -6
         assert b"CUDA" in wl.lib.wally_last_error(None) or b"device" in wl.lib.wally_last_error(None)
+
+
+def test_simd_default_moduli_and_param_validation(wl):
+    """Host-only parts of include/wally_simd.h: the default moduli (reading S25: the coefficient path's L
+    limbs, then the next NTT-friendly prime below them) and parameter validation before any device work."""
+    from paper_2406_06761_b200 import simd
+    for n, L in [(4096, 3), (4096, 2), (8192, 4), (1024, 1)]:
+        m = simd.simd_moduli(n, L)
+        assert m[:L] == wl.wally_find_moduli(n, L)
+        allp = capi.find_primes(n, L + 1)
+        assert m[L] == allp[0] and m[L] < m[0]
+    bad = [
+        dict(n=3000, L=2, d=16),                      # n not supported
+        dict(n=4096, L=2, d=4096),                    # d > n/2
+        dict(n=4096, L=2, d=16, t=65539),             # t not = 1 mod 2n (and not prime)
+        dict(n=4096, L=2, d=16, swap=True),           # special prime above q_0
+        dict(n=4096, L=2, d=16, baby=17),             # g > d
+    ]
+    for b in bad:
+        n, L = b["n"], b["L"]
+        p = simd.wally_simd_params(n=n, num_limbs=L, t=b.get("t", 65537), d=b["d"], baby=b.get("baby", 0))
+        mods = simd.simd_moduli(4096, L) if n == 3000 else simd.simd_moduli(n, L)
+        if b.get("swap"):
+            mods = [mods[L]] + mods[1:L] + [mods[0]]
+        for i, q in enumerate(mods):
+            p.moduli[i] = q
+        h = ctypes.c_void_p()
+        rc = wl.lib.wally_simd_create(ctypes.byref(p), 0, ctypes.byref(h))
+        assert rc == -2, (b, rc)
+        assert wl.lib.wally_simd_last_error(None)
