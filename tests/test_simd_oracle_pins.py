@@ -185,3 +185,31 @@ def test_bsgs_equals_naive_diagonal_method():
     R = capi.simd_row_slices(n, d)
     used = [r * (n // 2) + k for r in range(2) for k in range(R * d)]
     assert np.array_equal(a[used], b[used])
+
+
+def _is_prime_trial(x: int) -> bool:
+    if x < 2:
+        return False
+    f = 2
+    while f * f <= x:
+        if x % f == 0:
+            return False
+        f += 1
+    return True
+
+
+def test_special_primes_golden():
+    """Reading S25: P is the (L+1)-th largest NTT-friendly prime below 2^30 (golden file), re-derived by
+    trial division and by the oracle's own search."""
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "simd_special_primes.txt")
+    rows = [l.split() for l in open(path) if l.strip() and not l.startswith("#")]
+    for n, L, P in ((int(a), int(b), int(c)) for a, b, c in rows):
+        found = []
+        q = (2 ** 30 - 2) // (2 * n) * (2 * n) + 1
+        while len(found) < L + 1:
+            if q < 2 ** 30 and _is_prime_trial(q):
+                found.append(q)
+            q -= 2 * n
+        assert found[L] == P
+        assert capi.find_primes(n, L + 1)[0] == P
