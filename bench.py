@@ -10,9 +10,16 @@ every single-limb response ciphertext, for the configuration's full query
 batch (default: configs[2] "c3", the paper-scale 3.2M-entry workload the
 north star names; all inputs resident in HBM when the timed region starts).
 
-Multi-GPU (torchrun, one process per GPU): clusters are owned by ranks
-(cluster c -> rank c mod N); every rank evaluates the queries of the clusters
-it owns; value = all ranks' dot products / max-over-ranks device time.
+Multi-GPU (one process per GPU; `--gpus N` without WORLD_SIZE re-launches
+itself under torch.distributed.run with N ranks): clusters are owned by ranks
+(greedy LPT on expected work, hot clusters replicated --
+wally_assign_owners_replicated); the batch is resident on the ingress rank
+0, whose cluster ids go to every rank over the gloo control group, and every
+timed step scatters each owner's queries with the C ABI's NCCL data plane
+(wally_scatter_queries: pack kernel + grouped ncclSend/ncclRecv) before the
+owners evaluate them; value = all ranks' dot products / max-over-ranks
+device time.  `--dry-run` runs the same routing and a gloo scatter on host
+tensors without a GPU (the CPU test of the launch path).
 
 `--impl reference` times the CPU oracle (oracle/, plain C) on this host's
 cores on a bounded sample of the same workload (the reference arm).
@@ -71,7 +78,37 @@ def parse():
                          "(diagonals + BSGS rotations with hybrid key switching, SURVEY 8(f)-3)")
     ap.add_argument("--queries", type=int, default=0,
                     help="profiling only: evaluate just the first Q queries of the batch (not a bench line)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="no GPU: ranks over gloo run the routing plan and the query scatter on host tensors "
+                         "(checks the multi-rank launch path; prints a JSON line with value null)")
     return ap.parse_args()
+
+
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_if_needed(args):
+    """`--gpus N` must run N ranks.  Without WORLD_SIZE (a plain `python bench.py
+    --gpus N`), re-execute under torch.distributed.run with N local ranks and
+    exit with its status; under a launcher, WORLD_SIZE must equal --gpus."""
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None:
+        if args.gpus > 1:
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+                   "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+                   *sys.argv[1:]]
+            log("launching", args.gpus, "ranks:", " ".join(cmd))
+            sys.exit(subprocess.run(cmd).returncode)
+        return
+    if int(env_world) != args.gpus:
+        print(f"bench.py: WORLD_SIZE={env_world} but --gpus {args.gpus}: the two must agree", file=sys.stderr)
+        sys.exit(2)
 
 
 def log(*a):
@@ -266,15 +303,30 @@ def run_wally(args, rank, world, local_rank):
     nsel = args.queries if args.queries > 0 else ids_all.size
     ids_in = np.ascontiguousarray(ids_all[:nsel])
     router = None
+    comm = None
     if world > 1:
         # queries arrive on the ingress rank 0 (resident in its HBM); every step
-        # broadcasts their cluster ids, routes (wally_route_plan, same on every
-        # rank) and scatters each owner's share with NCCL P2P (dist.Router)
+        # broadcasts their cluster ids over the gloo control plane (host tensors,
+        # no device sync), routes (wally_route_plan, same on every rank) and
+        # scatters each owner's share with the C ABI's NCCL data plane
         from paper_2406_06761_b200.dist import Router
-        router = Router(sizes, owner, w.n, w.d, w.num_limbs, srv=srv, device=dev)
-        cts_in = synth.uniform_ciphertexts_torch(w, moduli, device=dev)[:nsel] if rank == 0 else None
+        router = Router(sizes, owner, w.n, w.d, w.num_limbs, srv=srv, device=dev, transport="wally")
+        comm = {"nranks": srv.comm_world, "rank": srv.comm_rank,
+                "transport": "NCCL communicator inside libwally.so (wally_comm_init / wally_scatter_queries / "
+                             "wally_gather_responses); control plane (cluster ids, unique id) over gloo"}
+        log(f"rank {rank}: wally NCCL communicator nranks={srv.comm_world}")
+        cts_in = synth.uniform_ciphertexts_torch(w, moduli, device=dev)[:nsel].contiguous() if rank == 0 else None
         plan = router.plan(ids_in)
         ids = np.ascontiguousarray(ids_in[plan.share(rank)])
+        share_buf = torch.empty((max(1, int(plan.counts[rank])), 2, w.num_limbs, w.n), dtype=torch.int32,
+                                device=dev)
+        pack_buf = torch.empty_like(cts_in) if rank == 0 else None
+        # the route order goes to the device through two pinned buffers (async copies, no stream sync)
+        order_pin = [torch.empty(nsel, dtype=torch.int32).pin_memory() for _ in range(2)]
+        order_dev = torch.empty(nsel, dtype=torch.int32, device=dev) if rank == 0 else None
+        order_ev = [torch.cuda.Event(), torch.cuda.Event()]
+        order_ev[1].record()
+        step_no = [0]
     else:
         cts_in = synth.uniform_ciphertexts_torch(w, moduli, device=dev)
         if nsel < ids_all.size:
@@ -296,7 +348,14 @@ def run_wally(args, rank, world, local_rank):
             return cts_in
         ids_r = router.broadcast_ids(ids_in if rank == 0 else None, nsel)
         pl = router.plan(ids_r)
-        mine = router.scatter(pl, cts_in)
+        if rank == 0:
+            k = step_no[0] & 1
+            order_ev[k].synchronize()          # the copy out of this buffer two steps ago is done
+            order_pin[k].numpy()[:] = pl.order.view(np.int32)
+            order_dev.copy_(order_pin[k], non_blocking=True)
+            order_ev[k].record()
+            step_no[0] += 1
+        mine = router.scatter(pl, cts_in, out=share_buf, pack_buf=pack_buf, order_dev=order_dev)
         srv.eval_batch(ids_r[pl.share(rank)], mine, resp, ws)
         return mine
 
@@ -309,26 +368,29 @@ def run_wally(args, rank, world, local_rank):
     srv.enable_stage_timing(True)
     srv.stage_times()
     launches0 = srv.kernel_launches()
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(local_rank) as clk:
         clk.wait_first()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t_clk0 = clk.mark()
-        start.record(stream)
-        for _ in range(args.steps):
+        evs[0].record(stream)
+        for i in range(args.steps):
             cts = step()
-        end.record(stream)
+            evs[i + 1].record(stream)
         torch.cuda.synchronize()
         t_clk1 = clk.mark()
     if world > 1:
         dist.barrier()
-    ms = start.elapsed_time(end)
+    step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    ms = evs[0].elapsed_time(evs[-1])
     launches = srv.kernel_launches() - launches0
     st_batcher, st_fwd, st_fused, nb = srv.stage_times()
     srv.enable_stage_timing(False)
     srv.check_batch(ws)
+    if router is not None:
+        srv.comm_check()
     gather_ms = None
     if router is not None:
         # optional response gather to the ingress, timed separately
@@ -342,13 +404,14 @@ def run_wally(args, rank, world, local_rank):
         gather_ms = ge0.elapsed_time(ge1)
         del gathered
 
-    # max over ranks (time) and sums (work)
-    t = torch.tensor([ms, st_fused / max(nb, 1), gather_ms or 0.0], dtype=torch.float64, device=dev)
+    # max over ranks (time, per step too) and sums (work)
+    t = torch.tensor([ms, st_fused / max(nb, 1), gather_ms or 0.0, *step_ms], dtype=torch.float64, device=dev)
     wk = torch.tensor([dots, pairs, nq], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(wk, op=dist.ReduceOp.SUM)
     ms_max, fused_ms_max, gather_ms_max = float(t[0]), float(t[1]), float(t[2])
+    step_ms_max = [float(x) for x in t[3:]]
     tot_dots, tot_pairs, tot_nq = (int(x) for x in wk.tolist())
     ms_per_step = ms_max / args.steps
     value = tot_dots / (ms_per_step / 1e3)
@@ -364,7 +427,9 @@ def run_wally(args, rank, world, local_rank):
     achieved = modmul_per_launch / (fused_ms / 1e3) / 1e12
     peak = SM_COUNT * MODMUL_PER_CLK_PER_SM * sm_max * 1e6 / 1e12
     sm_now = clocks.get("sm_mhz") or sm_max
-    roofline = {"bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 4), "unit": "Tmodmul/s",
+    roofline = {"bound": "fmaheavy", "bound_class": "alu (integer multiply-add on the FMA-heavy pipe; no "
+                                                    "tensor-core or HBM bound, DESIGN.md section 6)",
+                "achieved": round(achieved, 4), "peak": round(peak, 4), "unit": "Tmodmul/s",
                 "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.config),
                 "frac_at_measured_clock": round(achieved / (peak * sm_now / sm_max), 4),
                 "frac_vs_microbench": round(achieved / (SM_COUNT * MEASURED_MODMUL_PER_CLK_PER_SM * sm_max * 1e6 / 1e12),
@@ -385,7 +450,11 @@ def run_wally(args, rank, world, local_rank):
                 "hbm_peak_GBps": peaks.get("hbm_gbs")}
 
     out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+           "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+           "ms_per_step_best": round(min(step_ms_max), 4),
+           "ms_per_step_median": round(float(np.median(step_ms_max)), 4),
+           "value_best": round(tot_dots / (min(step_ms_max) / 1e3), 1),
+           "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "u32",
            "data": "synthetic (seeded numpy/torch; entries per BASELINE config; query ciphertexts are uniform "
                    "RNS residues, which RLWE makes indistinguishable from fresh encryptions)",
@@ -396,13 +465,14 @@ def run_wally(args, rank, world, local_rank):
                                          "include/wally.h WALLY_RESP_*)",
                       "ownership": ("greedy LPT on expected work with hot-cluster replication "
                                     "(wally_assign_owners_replicated); queries resident on rank 0, scattered by "
-                                    "NCCL P2P inside every step") if world > 1 else "single rank",
+                                    "the C ABI's NCCL data plane inside every step") if world > 1 else "single rank",
                       "l2": "inputs larger than L2 (plaintext store, query NTTs and responses >> 126 MB)"},
            "roofline": roofline,
            "stages_ms_per_step": {"batcher": round(st_batcher / max(nb, 1), 4),
                                   "forward_ntt": round(st_fwd / max(nb, 1), 4),
                                   "fused": round(fused_ms, 4)},
            "gpu_launches": int(launches),
+           "comm": comm,
            "gather_ms_per_batch": round(gather_ms_max, 3) if world > 1 else None,
            "clocks": clocks,
            "setup_s": round(setup_s, 1), "encode_s": round(encode_s, 3)}
@@ -540,7 +610,9 @@ def run_simd(args, rank, world, local_rank):
     mm = sum(srv.modmuls_per_query(int(b)) for b in blocks)
     achieved = mm / (ms / args.steps / 1e3) / 1e12
     peak = SM_COUNT * MODMUL_PER_CLK_PER_SM * sm_max * 1e6 / 1e12
-    roofline = {"bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 4), "unit": "Tmodmul/s",
+    roofline = {"bound": "fmaheavy", "bound_class": "alu (integer multiply-add on the FMA-heavy pipe; no "
+                                                    "tensor-core or HBM bound, DESIGN.md section 6)",
+                "achieved": round(achieved, 4), "peak": round(peak, 4), "unit": "Tmodmul/s",
                 "frac": round(achieved / peak, 4), "traffic": None,
                 "kernel": "the whole SIMD step (simd_ntt, simd_modup/moddown key switching, simd_ptmac, "
                           "simd_switch; every kernel is bound by the same integer multiply pipe)",
@@ -663,25 +735,70 @@ def run_reference(args):
             "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def run_dry(args, rank, world):
+    """The multi-rank launch path without a GPU (gloo, host tensors): the
+    ownership map, the ingress's cluster-id broadcast, the routing plan and
+    the query scatter of a 512-query slice of the configuration, each share
+    checked against the plan.  No CUDA call is made; value is null."""
+    import torch
+    from paper_2406_06761_b200 import wally as W
+    from paper_2406_06761_b200.dist import Router
+    w0 = synth.WORKLOADS[args.config]
+    w = synth.scaled(w0, num_queries=min(w0.num_queries, 512))
+    E = w.n // w.d
+    P = -(-w.cluster_size // E)
+    sizes = np.full(w.num_clusters, w.cluster_size, np.uint32)
+    owner = W.wally_assign_owners_replicated(synth.cluster_popularity(w) * P, world)
+    ids_in = synth.query_clusters(w)
+    moduli = W.wally_find_moduli(w.n, w.num_limbs)
+    cts = torch.from_numpy(synth.uniform_ciphertexts(w, moduli).view(np.int32)) if rank == 0 else None
+    rt = Router(sizes, owner, w.n, w.d, w.num_limbs,
+                pack=lambda idx, c: c[torch.from_numpy(idx.astype(np.int64))].contiguous())
+    t0 = time.perf_counter()
+    counts = None
+    for _ in range(max(1, args.steps)):
+        ids = rt.broadcast_ids(ids_in if rank == 0 else None, ids_in.size)
+        assert np.array_equal(ids, ids_in)
+        plan = rt.plan(ids)
+        share = rt.scatter(plan, cts)
+        assert share.shape[0] == int(plan.counts[rank])
+        counts = plan.counts.tolist()
+    dt = time.perf_counter() - t0
+    return {"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(dt * 1e3 / max(1, args.steps), 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded)",
+            "dry_run": "gloo on host tensors, no GPU: ownership, id broadcast, routing plan and query scatter only",
+            "config": {"workload": w0.name, "queries": int(w.num_queries), "routed_counts": counts}}
+
+
 def main():
     args = parse()
+    if not (args.impl == "reference" and "WORLD_SIZE" not in os.environ):
+        relaunch_if_needed(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
+        # the oracle arm: rank 0 alone runs and prints; the other ranks exit without work
         if rank == 0:
             print(json.dumps(run_reference(args)), flush=True)
         return
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
-    out = run_simd(args, rank, world, local_rank) if args.path == "simd" else run_wally(args, rank, world, local_rank)
+    import torch
+    import torch.distributed as dist
+    if args.dry_run:
+        if world > 1:
+            dist.init_process_group("gloo")
+        out = run_dry(args, rank, world)
+    else:
+        if world > 1:
+            torch.cuda.set_device(local_rank)
+            # host tensors (cluster ids, the NCCL unique id) over gloo, device tensors over NCCL
+            dist.init_process_group("cpu:gloo,cuda:nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        out = run_simd(args, rank, world, local_rank) if args.path == "simd" else run_wally(args, rank, world,
+                                                                                            local_rank)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
-        import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()
 

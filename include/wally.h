@@ -62,6 +62,7 @@ typedef enum {
     WALLY_E_RESIDUE = -4,         /* an input residue >= q_i (reported by wally_check_batch) */
     WALLY_E_STATE = -5,           /* call order: e.g. eval before encode */
     WALLY_E_CUDA = -6,            /* a CUDA runtime call failed */
+    WALLY_E_NCCL = -7,            /* NCCL unavailable, or an NCCL call / communicator failed */
     WALLY_E_OOM = -8              /* internal table allocation failed */
 } wally_status;
 
@@ -117,7 +118,16 @@ typedef struct {
 int wally_find_moduli(uint32_t n, uint32_t num_limbs, uint32_t *moduli_out);
 
 /* Create a context on CUDA device `device`: validates params, builds the
- * NTT twiddle tables and modulus-switch constants and uploads them. */
+ * NTT twiddle tables and modulus-switch constants and uploads them.
+ * One context is one server (one rank) of the paper's setting: it holds the
+ * scheme of P:L244-251 (R_Q = Z_Q[X]/(X^n+1), plaintext modulus t) in the RNS
+ * form of P:L1310-1317 with NTT-friendly limbs q_i = 1 mod 2n, and
+ * the modulus-switch target q_0 of P:L1003 / P:L1323 ("Q' = q_0").
+ *   params   read only during the call (the context keeps a copy)
+ *   ctx_out  receives the context; the caller releases it with wally_destroy
+ * Errors: WALLY_E_PARAMS (unsupported n, L, d, t or moduli), WALLY_E_CUDA (no
+ * such device), WALLY_E_OOM; *ctx_out is NULL on error and the detail is in
+ * wally_last_error(NULL). */
 int wally_create(const wally_params *params, int device, wally_ctx **ctx_out);
 void wally_destroy(wally_ctx *ctx);
 /* Detail of the last error on ctx (or of the last failed wally_create when ctx is NULL). */
@@ -195,8 +205,12 @@ int wally_eval_batch(wally_ctx *ctx, uint32_t nq, const uint32_t *cluster_of_que
  * this workspace: WALLY_E_RESIDUE if any query residue was >= its modulus. */
 int wally_check_batch(wally_ctx *ctx, const void *workspace_dev, void *stream);
 
-/* Copy responses device -> host (stream-ordered, then synchronizes the stream).
- *   responses_dev  uint32 [words] (device);  out_host  uint32 [words] (host, pinned or pageable) */
+/* Copy responses device -> host (stream-ordered, then synchronizes the stream):
+ * the return of the encrypted scores R to the client, Alg 4
+ * ("return r = (R, metadata)"; metadata is out of scope).
+ *   responses_dev  uint32 [words] (device);  out_host  uint32 [words] (host, pinned or pageable)
+ * The caller owns both buffers.  Errors: WALLY_E_ARG (null pointer with
+ * words > 0), WALLY_E_CUDA (copy failed). */
 int wally_fetch_responses(wally_ctx *ctx, const uint32_t *responses_dev, uint64_t words, uint32_t *out_host,
                           void *stream);
 
@@ -207,7 +221,11 @@ int wally_fetch_responses(wally_ctx *ctx, const uint32_t *responses_dev, uint64_
  * sub-batches overlapped on two streams.  Synchronizes before returning.
  *   query_ct_host   uint32 [nq][2][L][n] (pinned for full copy bandwidth)
  *   responses_host  uint32 [responses_words], layout of wally_response_layout
- *   workspace_dev   wally_host_workspace_bytes(sub_batch, max_words) bytes */
+ *   workspace_dev   wally_host_workspace_bytes(sub_batch) bytes (device)
+ * Unlike wally_eval_batch, the device-side residue check is collected here:
+ * after the final synchronisation the call returns WALLY_E_RESIDUE if any
+ * query residue of any sub-batch was >= its modulus (the responses of such a
+ * batch are meaningless). */
 int wally_host_workspace_bytes(const wally_ctx *ctx, uint32_t sub_batch, size_t *bytes_out);
 int wally_eval_batch_host(wally_ctx *ctx, uint32_t nq, const uint32_t *cluster_of_query_host,
                           const uint32_t *query_ct_host, uint32_t *responses_host, uint64_t responses_words,
@@ -289,6 +307,58 @@ int wally_load_clusters_replicated(wally_ctx *ctx, uint32_t total_clusters, cons
  *   out_dev       uint32 [count][2][L][n] (device, 16-byte aligned) */
 int wally_pack_queries(wally_ctx *ctx, uint32_t count, const uint32_t *index_dev, const uint32_t *query_ct_dev,
                        uint32_t *out_dev, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU data plane (north_star: "Clusters are partitioned across the 8
+ * GPUs of one B200 box ... queries are routed to the owning rank, with NCCL
+ * over NVLink only for query scatter and response gather"; the server
+ * "distributes them according to the correct clusters").  One
+ * context per rank (one process per GPU).  Alg 4's work is independent per
+ * query, so the scatter and the optional gather are the only
+ * exchange steps.  NCCL is loaded at run time (libnccl.so.2, the copy torch
+ * uses when it is loaded); the single-rank path never needs it.
+ * ------------------------------------------------------------------------- */
+#define WALLY_COMM_ID_BYTES 128
+
+/* An NCCL unique id (128 bytes) for a new communicator.  Called on one rank
+ * (the ingress); the caller hands the bytes to every rank (e.g. a
+ * torch.distributed broadcast).  Errors: WALLY_E_NCCL. */
+int wally_comm_unique_id(uint8_t *id_out);
+
+/* Join the communicator `id` as `rank` of `world` on the context's device
+ * (collective: every rank calls it).  Replaces an earlier communicator.
+ * Errors: WALLY_E_ARG, WALLY_E_NCCL. */
+int wally_comm_init(wally_ctx *ctx, int32_t rank, int32_t world, const uint8_t *id);
+
+/* WALLY_E_NCCL if the communicator saw an asynchronous error (a failed peer
+ * or transport), WALLY_E_STATE without a communicator. */
+int wally_comm_check(wally_ctx *ctx);
+
+/* Query scatter (collective over the communicator; stream-ordered).  Every
+ * rank passes the same counts_host, the per-rank query counts of
+ * wally_route_plan.  On the source rank `src` (the ingress):
+ *   order_dev     uint32 [nq] (device): wally_route_plan's order_out, nq = sum(counts)
+ *   query_ct_dev  uint32 [nq][2][L][n] (device, 16-byte aligned): the batch in input order
+ *   pack_dev      uint32 [nq][2][L][n] (device scratch, 16-byte aligned): the shares,
+ *                 packed contiguously in rank order (kernel pack_rows), from which
+ *                 rank r's block is sent with ncclSend
+ * On every rank (src included):
+ *   share_dev     uint32 [counts[rank]][2][L][n] (device) out: this rank's
+ *                 queries in its local order (wally_route_plan's order within the rank).
+ * Other ranks pass NULL for order/query/pack.  Errors: WALLY_E_STATE (no
+ * communicator), WALLY_E_ARG, WALLY_E_CUDA, WALLY_E_NCCL. */
+int wally_scatter_queries(wally_ctx *ctx, int32_t src, const uint32_t *counts_host, const uint32_t *order_dev,
+                          const uint32_t *query_ct_dev, uint32_t *pack_dev, uint32_t *share_dev, void *stream);
+
+/* Response gather to rank `dst` (collective; stream-ordered): the ranks'
+ * response buffers concatenated in rank order, the layout of
+ * wally_route_plan's gathered_off (query q's responses start there).
+ *   resp_words_host  uint64 [world]: wally_route_plan's resp_words_out (same on every rank)
+ *   resp_dev         this rank's responses, resp_words_host[rank] words (device)
+ *   gathered_dev     dst only: sum(resp_words_host) words (device); NULL elsewhere
+ * Errors: as wally_scatter_queries. */
+int wally_gather_responses(wally_ctx *ctx, int32_t dst, const uint64_t *resp_words_host, const uint32_t *resp_dev,
+                           uint32_t *gathered_dev, void *stream);
 
 /* Test hooks on the same device code as the hot path.
  * Forward NTT (the kernel of step 2): in_dev uint32 [count][L][n] canonical

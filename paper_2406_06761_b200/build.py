@@ -7,6 +7,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+import sysconfig
 from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
@@ -18,9 +19,13 @@ BUILD = os.path.join(PKG, "build")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + INCLUDE, "-I" + CSRC]
+# nccl.h of the NCCL torch ships (the library opens libnccl.so.2 at run time, no link dependency)
+NCCL_INCLUDE = os.path.join(sysconfig.get_paths()["purelib"], "nvidia", "nccl", "include")
+if not os.path.exists(os.path.join(NCCL_INCLUDE, "nccl.h")):
+    NCCL_INCLUDE = "/usr/include"
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + INCLUDE, "-I" + CSRC, "-I" + NCCL_INCLUDE]
 
-SOURCES = ["kernels.cu", "capi.cpp", "simd.cu"]
+SOURCES = ["kernels.cu", "capi.cpp", "comm.cpp", "simd.cu"]
 
 
 def _deps():
@@ -62,7 +67,7 @@ def build(force: bool = False, verbose: bool = False, lib: str = LIB, defines=()
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
     tmp = lib + f".tmp{os.getpid()}"
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"])
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-ldl"])
     os.replace(tmp, lib)
     return lib
 

@@ -17,53 +17,14 @@
 #include <vector>
 
 #include "ntt_device.cuh"
-#include "wally_internal.h"
+#include "wally_ctx.h"
 
 using namespace wally;
 
-struct wally_ctx {
-    wally_params p{};
-    int device = 0;
-    int num_sms = 148;
-    uint32_t E = 0;
-    uint64_t wpp = 0;  // response words per plaintext
-    KParams kp{};
-    uint2 *d_tw_fwd = nullptr, *d_tw_inv = nullptr;
-    uint2 *d_tw_mrg = nullptr;  // [L][n] merged inverse table psi^{-brev(i)} (pruned c0 transform)
-    // cluster layout
-    bool loaded = false;
-    uint32_t total_clusters = 0, n_local = 0, npt = 0, max_pt = 0;
-    std::vector<int32_t> local_of_cluster;     // host copy
-    std::vector<int32_t> owner;                // [total_clusters] (empty: all local)
-    int32_t rank = 0;
-    std::vector<uint32_t> pt_of_local;         // P_c per local cluster
-    uint64_t local_entries = 0;
-    int32_t *d_local_of_cluster = nullptr;
-    uint32_t *d_pt_base = nullptr, *d_n_pt = nullptr, *d_pt_li = nullptr, *d_pt_k = nullptr, *d_size = nullptr;
-    uint64_t *d_entry_base = nullptr;
-    // encoded plaintexts (caller-owned)
-    const uint32_t *store = nullptr;
-    // pinned staging for per-batch metadata (ids + response offsets), 2 slots
-    struct Slot {
-        uint32_t *ids = nullptr;
-        uint64_t *off = nullptr;
-        size_t cap = 0;
-        cudaEvent_t done = nullptr;
-        bool pending = false;
-    } slot[2];
-    int next_slot = 0;
-    cudaStream_t side = nullptr;  // second stream of the host pipeline
-    uint64_t launches = 0;
-    // optional per-stage timing: 4 events per recorded batch
-    bool timing = false;
-    std::vector<cudaEvent_t> ev_pool;
-    std::vector<std::array<cudaEvent_t, 4>> ev_rec;
-    std::string err;
-};
 
 static thread_local std::string g_create_err;
 
-static int fail(wally_ctx *c, int code, const char *fmt, ...) {
+int wally_fail(wally_ctx *c, int code, const char *fmt, ...) {
     char buf[512];
     va_list ap;
     va_start(ap, fmt);
@@ -72,6 +33,7 @@ static int fail(wally_ctx *c, int code, const char *fmt, ...) {
     if (c) c->err = buf; else g_create_err = buf;
     return code;
 }
+#define fail wally_fail
 
 #define CUDA_OK(ctx, call)                                                                              \
     do {                                                                                                \
@@ -192,6 +154,7 @@ static void build_pass_tables(uint32_t n, const uint2 *pf, const uint2 *pi, uint
 }
 
 extern "C" int wally_find_moduli(uint32_t n, uint32_t num_limbs, uint32_t *moduli_out) {
+    WALLY_NVTX("wally_find_moduli");
     if (!moduli_out || num_limbs == 0 || num_limbs > WALLY_MAX_LIMBS || n < 2 || (n & (n - 1)))
         return fail(nullptr, WALLY_E_ARG, "wally_find_moduli: bad arguments");
     const uint64_t step = 2ull * n;
@@ -214,6 +177,7 @@ extern "C" void wally_destroy(wally_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
+    wally_comm_release(c);
     cudaFree(c->d_tw_fwd);
     cudaFree(c->d_tw_inv);
     cudaFree(c->d_tw_mrg);
@@ -230,12 +194,14 @@ extern "C" void wally_destroy(wally_ctx *c) {
         if (s.done) cudaEventDestroy(s.done);
     }
     if (c->side) cudaStreamDestroy(c->side);
+    if (c->err_host) cudaFreeHost(c->err_host);
     for (auto &r : c->ev_rec) for (auto e : r) c->ev_pool.push_back(e);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     delete c;
 }
 
 extern "C" int wally_create(const wally_params *pp, int device, wally_ctx **out) {
+    WALLY_NVTX("wally_create");
     if (!pp || !out) return fail(nullptr, WALLY_E_ARG, "wally_create: null argument");
     *out = nullptr;
     const wally_params &p = *pp;
@@ -387,6 +353,7 @@ static int load_clusters_impl(wally_ctx *c, uint32_t total_clusters, const uint3
 
 extern "C" int wally_load_clusters(wally_ctx *c, uint32_t total_clusters, const uint32_t *sizes,
                                    const int32_t *owner, int32_t rank) {
+    WALLY_NVTX("wally_load_clusters");
     if (!c) return WALLY_E_ARG;
     return load_clusters_impl(
         c, total_clusters, sizes, [&](uint32_t cl) { return !owner || owner[cl] == rank; },
@@ -395,6 +362,7 @@ extern "C" int wally_load_clusters(wally_ctx *c, uint32_t total_clusters, const 
 
 extern "C" int wally_load_clusters_replicated(wally_ctx *c, uint32_t total_clusters, const uint32_t *sizes,
                                               const uint64_t *mask, int32_t rank) {
+    WALLY_NVTX("wally_load_clusters_replicated");
     if (!c) return WALLY_E_ARG;
     if (!mask || rank < 0 || rank >= 64) return fail(c, WALLY_E_ARG, "load_clusters_replicated: bad mask or rank");
     // owner[] (wally_route_queries) reports the lowest replica of each cluster
@@ -406,12 +374,14 @@ extern "C" int wally_load_clusters_replicated(wally_ctx *c, uint32_t total_clust
 }
 
 extern "C" int wally_response_words_per_plaintext(const wally_ctx *c, uint64_t *words) {
+    WALLY_NVTX("wally_response_words_per_plaintext");
     if (!c || !words) return WALLY_E_ARG;
     *words = c->wpp;
     return WALLY_OK;
 }
 
 extern "C" int wally_modmuls_per_pair(const wally_ctx *c, uint64_t *out) {
+    WALLY_NVTX("wally_modmuls_per_pair");
     if (!c || !out) return WALLY_E_ARG;
     const bool compact = c->p.resp_format != WALLY_RESP_FULL;
     *out = modmuls_per_pair(c->p.n, c->p.num_limbs, c->p.d, pruned_c0_path(c->p.n, c->p.num_limbs, c->p.d, compact));
@@ -419,6 +389,7 @@ extern "C" int wally_modmuls_per_pair(const wally_ctx *c, uint64_t *out) {
 }
 
 extern "C" int wally_plaintext_store_bytes(const wally_ctx *c, size_t *bytes) {
+    WALLY_NVTX("wally_plaintext_store_bytes");
     if (!c || !bytes) return WALLY_E_ARG;
     if (!c->loaded) return fail(const_cast<wally_ctx *>(c), WALLY_E_STATE, "load_clusters first");
     *bytes = (size_t)c->npt * c->p.num_limbs * 2 * c->p.n * sizeof(uint32_t);
@@ -426,6 +397,7 @@ extern "C" int wally_plaintext_store_bytes(const wally_ctx *c, size_t *bytes) {
 }
 
 extern "C" int wally_local_entry_count(const wally_ctx *c, uint64_t *count) {
+    WALLY_NVTX("wally_local_entry_count");
     if (!c || !count) return WALLY_E_ARG;
     if (!c->loaded) return fail(const_cast<wally_ctx *>(c), WALLY_E_STATE, "load_clusters first");
     *count = c->local_entries;
@@ -434,6 +406,7 @@ extern "C" int wally_local_entry_count(const wally_ctx *c, uint64_t *count) {
 
 extern "C" int wally_encode_plaintexts_ntt(wally_ctx *c, const int8_t *entries_dev, void *store_dev,
                                            size_t store_bytes, void *stream) {
+    WALLY_NVTX("wally_encode_plaintexts_ntt");
     if (!c) return WALLY_E_ARG;
     if (!c->loaded) return fail(c, WALLY_E_STATE, "load_clusters first");
     size_t need = 0;
@@ -488,6 +461,7 @@ WsLayout wally::ws_layout(uint32_t nq, uint32_t n_local, uint32_t n, uint32_t L)
 }
 
 extern "C" int wally_workspace_bytes(const wally_ctx *c, uint32_t nq, size_t *bytes) {
+    WALLY_NVTX("wally_workspace_bytes");
     if (!c || !bytes) return WALLY_E_ARG;
     if (!c->loaded) return fail(const_cast<wally_ctx *>(c), WALLY_E_STATE, "load_clusters first");
     *bytes = ws_layout(nq, c->n_local, c->p.n, c->p.num_limbs).total;
@@ -512,6 +486,7 @@ static int layout_impl(const wally_ctx *c, uint32_t nq, const uint32_t *ids, uin
 
 extern "C" int wally_response_layout(const wally_ctx *c, uint32_t nq, const uint32_t *ids, uint64_t *off,
                                      uint64_t *total) {
+    WALLY_NVTX("wally_response_layout");
     if (!c || (nq && !ids)) return WALLY_E_ARG;
     if (!c->loaded) return fail(const_cast<wally_ctx *>(c), WALLY_E_STATE, "load_clusters first");
     return layout_impl(c, nq, ids, off, total);
@@ -599,22 +574,33 @@ static int eval_impl(wally_ctx *c, uint32_t nq, const uint32_t *ids, const uint3
         c->ev_rec.push_back(ev);
         CUDA_OK(c, cudaEventRecord(ev[0], s));
     }
-    CUDA_OK(c, launch_batcher(a, s, &c->launches));
+    {
+        WALLY_NVTX("a1 batcher");
+        CUDA_OK(c, launch_batcher(a, s, &c->launches));
+    }
     if (c->timing) CUDA_OK(c, cudaEventRecord(ev[1], s));
-    CUDA_OK(c, launch_query_ntt(a, s, &c->launches));
+    {
+        WALLY_NVTX("a2 forward NTT");
+        CUDA_OK(c, launch_query_ntt(a, s, &c->launches));
+    }
     if (c->timing) CUDA_OK(c, cudaEventRecord(ev[2], s));
-    CUDA_OK(c, launch_eval(a, s, c->num_sms, &c->launches));
+    {
+        WALLY_NVTX("a3-a6 fused pointwise/iNTT/mod-switch");
+        CUDA_OK(c, launch_eval(a, s, c->num_sms, &c->launches));
+    }
     if (c->timing) CUDA_OK(c, cudaEventRecord(ev[3], s));
     return WALLY_OK;
 }
 
 extern "C" int wally_enable_stage_timing(wally_ctx *c, int enable) {
+    WALLY_NVTX("wally_enable_stage_timing");
     if (!c) return WALLY_E_ARG;
     c->timing = enable != 0;
     return WALLY_OK;
 }
 
 extern "C" int wally_stage_times(wally_ctx *c, double *ms, uint64_t *batches) {
+    WALLY_NVTX("wally_stage_times");
     if (!c || !ms) return WALLY_E_ARG;
     cudaSetDevice(c->device);
     ms[0] = ms[1] = ms[2] = 0.0;
@@ -634,12 +620,14 @@ extern "C" int wally_stage_times(wally_ctx *c, double *ms, uint64_t *batches) {
 
 extern "C" int wally_eval_batch(wally_ctx *c, uint32_t nq, const uint32_t *ids, const uint32_t *query_dev,
                                 uint32_t *resp_dev, uint64_t resp_words, void *ws_dev, size_t ws_bytes, void *stream) {
+    WALLY_NVTX("wally_eval_batch");
     if (!c) return WALLY_E_ARG;
     cudaSetDevice(c->device);
     return eval_impl(c, nq, ids, query_dev, resp_dev, resp_words, ws_dev, ws_bytes, (cudaStream_t)stream);
 }
 
 extern "C" int wally_check_batch(wally_ctx *c, const void *ws_dev, void *stream) {
+    WALLY_NVTX("wally_check_batch");
     if (!c || !ws_dev) return WALLY_E_ARG;
     cudaSetDevice(c->device);
     CUDA_OK(c, cudaStreamSynchronize((cudaStream_t)stream));
@@ -652,6 +640,7 @@ extern "C" int wally_check_batch(wally_ctx *c, const void *ws_dev, void *stream)
 
 extern "C" int wally_fetch_responses(wally_ctx *c, const uint32_t *resp_dev, uint64_t words, uint32_t *out_host,
                                      void *stream) {
+    WALLY_NVTX("wally_fetch_responses");
     if (!c || (words && (!resp_dev || !out_host))) return WALLY_E_ARG;
     cudaSetDevice(c->device);
     CUDA_OK(c, cudaMemcpyAsync(out_host, resp_dev, words * sizeof(uint32_t), cudaMemcpyDeviceToHost,
@@ -661,6 +650,7 @@ extern "C" int wally_fetch_responses(wally_ctx *c, const uint32_t *resp_dev, uin
 }
 
 extern "C" int wally_route_queries(const wally_ctx *c, uint32_t nq, const uint32_t *ids, int32_t *dest) {
+    WALLY_NVTX("wally_route_queries");
     if (!c || (nq && (!ids || !dest))) return WALLY_E_ARG;
     if (!c->loaded) return fail(const_cast<wally_ctx *>(c), WALLY_E_STATE, "load_clusters first");
     for (uint32_t q = 0; q < nq; q++) {
@@ -689,6 +679,7 @@ static HostWs host_ws(const wally_ctx *c, uint32_t sub) {
 }
 
 extern "C" int wally_host_workspace_bytes(const wally_ctx *c, uint32_t sub, size_t *bytes) {
+    WALLY_NVTX("wally_host_workspace_bytes");
     if (!c || !bytes || sub == 0) return WALLY_E_ARG;
     if (!c->loaded) return fail(const_cast<wally_ctx *>(c), WALLY_E_STATE, "load_clusters first");
     *bytes = host_ws(c, sub).total;
@@ -698,6 +689,7 @@ extern "C" int wally_host_workspace_bytes(const wally_ctx *c, uint32_t sub, size
 extern "C" int wally_eval_batch_host(wally_ctx *c, uint32_t nq, const uint32_t *ids, const uint32_t *query_host,
                                      uint32_t *resp_host, uint64_t resp_words, uint32_t sub, void *ws_dev,
                                      size_t ws_bytes, void *stream) {
+    WALLY_NVTX("wally_eval_batch_host");
     if (!c) return WALLY_E_ARG;
     if (!c->loaded) return fail(c, WALLY_E_STATE, "load_clusters first");
     if (!c->store) return fail(c, WALLY_E_STATE, "encode_plaintexts_ntt first");
@@ -711,6 +703,16 @@ extern "C" int wally_eval_batch_host(wally_ctx *c, uint32_t nq, const uint32_t *
     int rc = layout_impl(c, nq, ids, off.data(), &total);
     if (rc) return rc;
     if (resp_words < total) return fail(c, WALLY_E_ARG, "eval_host: response buffer too small");
+    const size_t nsub = (nq + (size_t)sub - 1) / sub;
+    if (c->err_cap < nsub) {
+        if (c->err_host) cudaFreeHost(c->err_host);
+        c->err_host = nullptr;
+        c->err_cap = 0;
+        if (cudaMallocHost(&c->err_host, sizeof(uint32_t) * nsub) != cudaSuccess)
+            return fail(c, WALLY_E_OOM, "pinned error-word allocation failed");
+        c->err_cap = nsub;
+    }
+    const WsLayout wl = ws_layout(sub, c->n_local, c->p.n, c->p.num_limbs);
     cudaStream_t st[2] = {(cudaStream_t)stream, c->side};
     cudaEvent_t start;
     CUDA_OK(c, cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
@@ -731,10 +733,15 @@ extern "C" int wally_eval_batch_host(wally_ctx *c, uint32_t nq, const uint32_t *
         rc = eval_impl(c, cnt, ids + q0, qdev, rdev, words, base, h.ws, s);
         if (rc) { cudaEventDestroy(start); return rc; }
         CUDA_OK(c, cudaMemcpyAsync(resp_host + off[q0], rdev, words * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        CUDA_OK(c, cudaMemcpyAsync(c->err_host + b, base + wl.misc + sizeof(uint32_t) * kMiscErr, sizeof(uint32_t),
+                                   cudaMemcpyDeviceToHost, s));
     }
     cudaEventDestroy(start);
     CUDA_OK(c, cudaStreamSynchronize(st[1]));
     CUDA_OK(c, cudaStreamSynchronize(st[0]));
+    uint32_t err = 0;
+    for (size_t i = 0; i < nsub; i++) err |= c->err_host[i];
+    if (err & kErrResidue) return fail(c, WALLY_E_RESIDUE, "a query ciphertext residue was >= its modulus");
     return WALLY_OK;
 }
 
@@ -742,6 +749,7 @@ extern "C" int wally_eval_batch_host(wally_ctx *c, uint32_t nq, const uint32_t *
 // test hooks
 // ---------------------------------------------------------------------------
 extern "C" int wally_ntt_forward(wally_ctx *c, const uint32_t *in, uint32_t *out, uint32_t count, void *stream) {
+    WALLY_NVTX("wally_ntt_forward");
     if (!c || (count && (!in || !out))) return WALLY_E_ARG;
     if ((uintptr_t)out % 16) return fail(c, WALLY_E_ARG, "ntt_forward: out must be 16-byte aligned");
     cudaSetDevice(c->device);
@@ -751,6 +759,7 @@ extern "C" int wally_ntt_forward(wally_ctx *c, const uint32_t *in, uint32_t *out
 }
 
 extern "C" int wally_ntt_inverse(wally_ctx *c, const uint32_t *in, uint32_t *out, uint32_t count, void *stream) {
+    WALLY_NVTX("wally_ntt_inverse");
     if (!c || (count && (!in || !out))) return WALLY_E_ARG;
     if ((uintptr_t)in % 16) return fail(c, WALLY_E_ARG, "ntt_inverse: in must be 16-byte aligned");
     cudaSetDevice(c->device);
@@ -763,6 +772,7 @@ extern "C" int wally_ntt_inverse(wally_ctx *c, const uint32_t *in, uint32_t *out
 // multi-GPU routing (host logic)
 // ---------------------------------------------------------------------------
 extern "C" int wally_assign_owners(uint32_t total_clusters, const double *weight, uint32_t world, int32_t *owner) {
+    WALLY_NVTX("wally_assign_owners");
     if (!weight || !owner || total_clusters == 0 || world == 0)
         return fail(nullptr, WALLY_E_ARG, "assign_owners: bad arguments");
     for (uint32_t c = 0; c < total_clusters; c++)
@@ -817,6 +827,7 @@ static int route_plan_dest(uint32_t nq, const uint32_t *ids, uint32_t total_clus
 extern "C" int wally_route_plan(uint32_t nq, const uint32_t *ids, uint32_t total_clusters, const uint32_t *sizes,
                                 const int32_t *owner, uint32_t n, uint32_t d, uint32_t resp_format, uint32_t world,
                                 uint32_t *counts, uint32_t *order, uint64_t *resp_words, uint64_t *gathered_off) {
+    WALLY_NVTX("wally_route_plan");
     if ((nq && (!ids || !order)) || !sizes || !counts || !resp_words || total_clusters == 0 || world == 0 ||
         n == 0 || d == 0 || d > n || !valid_resp_format(resp_format))
         return fail(nullptr, WALLY_E_ARG, "route_plan: bad arguments");
@@ -837,6 +848,7 @@ extern "C" int wally_route_plan(uint32_t nq, const uint32_t *ids, uint32_t total
 
 extern "C" int wally_assign_owners_replicated(uint32_t total_clusters, const double *weight, uint32_t world,
                                               uint64_t *mask) {
+    WALLY_NVTX("wally_assign_owners_replicated");
     if (!weight || !mask || total_clusters == 0 || world == 0 || world > 64)
         return fail(nullptr, WALLY_E_ARG, "assign_owners_replicated: bad arguments (world 1..64)");
     double W = 0.0;
@@ -872,6 +884,7 @@ extern "C" int wally_route_plan_replicated(uint32_t nq, const uint32_t *ids, uin
                                            const uint32_t *sizes, const uint64_t *mask, uint32_t n, uint32_t d,
                                            uint32_t resp_format, uint32_t world, uint32_t *counts, uint32_t *order,
                                            uint64_t *resp_words, uint64_t *gathered_off) {
+    WALLY_NVTX("wally_route_plan_replicated");
     if (!mask || world == 0 || world > 64 || (nq && (!ids || !order)) || !sizes || !counts || !resp_words ||
         total_clusters == 0 || n == 0 || d == 0 || d > n || !valid_resp_format(resp_format))
         return fail(nullptr, WALLY_E_ARG, "route_plan_replicated: bad arguments (world 1..64)");
@@ -902,6 +915,7 @@ extern "C" int wally_route_plan_replicated(uint32_t nq, const uint32_t *ids, uin
 
 extern "C" int wally_pack_queries(wally_ctx *c, uint32_t count, const uint32_t *index_dev, const uint32_t *query_dev,
                                   uint32_t *out_dev, void *stream) {
+    WALLY_NVTX("wally_pack_queries");
     if (!c) return WALLY_E_ARG;
     if (count == 0) return WALLY_OK;
     if (!index_dev || !query_dev || !out_dev) return fail(c, WALLY_E_ARG, "pack_queries: null pointer");

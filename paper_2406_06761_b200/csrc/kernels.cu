@@ -19,6 +19,13 @@
 #include "tmem.cuh"
 #include "wally_internal.h"
 
+#ifndef WALLY_OPLD_P8
+#define WALLY_OPLD_P8 3
+#endif
+#ifndef WALLY_OPLD_PR
+#define WALLY_OPLD_PR 1
+#endif
+
 namespace wally {
 
 // ---------------------------------------------------------------------------
@@ -1165,7 +1172,7 @@ struct LimbLoopPR {
             for (int c = 0; c < 2; c++)
 #pragma unroll
                 for (int v = 0; v < V / 4; v++)
-                    cpre[c][v] = ldg_stream(nsrc + (size_t)c * L * N + (size_t)g * V + 4 * v);
+                    cpre[c][v] = ldg_op<WALLY_OPLD_PR>(nsrc + (size_t)c * L * N + (size_t)g * V + 4 * v);
         }
         // c0: pass 0 keeping the last Y output of each block -> one value per thread
         const uint2 *twJ = cx.tw + (size_t)J * Gm::TW_LIMB;
@@ -1252,7 +1259,7 @@ __device__ __forceinline__ void eval_item_pr(const BatchArgs &ba, const ItemCurs
         const uint32_t *pv = phat + (size_t)J * 2 * N + (size_t)g * V;
 #pragma unroll
         for (int v = 0; v < 4; v++) {
-            const uint4 x = ldg_stream(pv + 4 * v), y = ldg_stream(pv + N + 4 * v);
+            const uint4 x = ldg_op<WALLY_OPLD_PR>(pv + 4 * v), y = ldg_op<WALLY_OPLD_PR>(pv + N + 4 * v);
             p[4 * v] = x.x; p[4 * v + 1] = x.y; p[4 * v + 2] = x.z; p[4 * v + 3] = x.w;
             pp[4 * v] = y.x; pp[4 * v + 1] = y.y; pp[4 * v + 2] = y.z; pp[4 * v + 3] = y.w;
         }
@@ -1267,7 +1274,7 @@ __device__ __forceinline__ void eval_item_pr(const BatchArgs &ba, const ItemCurs
 #pragma unroll
         for (int c = 0; c < 2; c++)
 #pragma unroll
-            for (int v = 0; v < V / 4; v++) cpre[c][v] = ldg_stream(src + (size_t)c * L * N + (size_t)g * V + 4 * v);
+            for (int v = 0; v < V / 4; v++) cpre[c][v] = ldg_op<WALLY_OPLD_PR>(src + (size_t)c * L * N + (size_t)g * V + 4 * v);
     }
     for (uint32_t qi = qb; qi < qe; qi++) {
         const uint32_t qn = (qi + 1 < qe) ? ba.perm[qi + 1] : 0xffffffffu;
@@ -1338,14 +1345,11 @@ __global__ void __launch_bounds__(kEvalGroups * NttGeom<4096>::T, 1) eval_kernel
 template <int L, int FMT>
 static cudaError_t launch_eval_pr(const BatchArgs &a, cudaStream_t s, int num_sms) {
     using Gm = NttGeom<4096>;
-    static bool configured = false;
+    static DeviceOnce once;
     const size_t smem =
         (size_t)L * Gm::TW_LIMB * sizeof(uint2) + (size_t)kEvalGroups * 2 * Gm::SMEM_WORDS * sizeof(uint32_t);
-    if (!configured) {
-        cudaError_t e = allow_smem(eval_kernel_pr<L, FMT>, smem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    cudaError_t e = device_once(once, [&](int *) { return allow_smem(eval_kernel_pr<L, FMT>, smem); });
+    if (e != cudaSuccess) return e;
     eval_kernel_pr<L, FMT><<<num_sms, kEvalGroups * Gm::T, smem, s>>>(a);
     return cudaGetLastError();
 }
@@ -1418,10 +1422,10 @@ struct LimbLoopP8M {
         for (int c = 0; c < 8; c++) {
             const uint4 p = np, pp = npp, x0 = nx0, x1 = nx1;
             if (c + 1 < 8) {     // the next chunk's loads fly while this chunk computes
-                np = ldg_stream(pv + c + 1);
-                npp = ldg_stream(ppv + c + 1);
-                nx0 = ldg_stream(c0v + c + 1);
-                nx1 = ldg_stream(c1v + c + 1);
+                np = ldg_op<WALLY_OPLD_P8>(pv + c + 1);
+                npp = ldg_op<WALLY_OPLD_P8>(ppv + c + 1);
+                nx0 = ldg_op<WALLY_OPLD_P8>(c0v + c + 1);
+                nx1 = ldg_op<WALLY_OPLD_P8>(c1v + c + 1);
             }
             a[0][4 * c + 0] = shoup_mul(x1.x, p.x, pp.x, q);
             a[0][4 * c + 1] = shoup_mul(x1.y, p.y, pp.y, q);
@@ -1449,10 +1453,10 @@ struct LimbLoopP8M {
         z[g] = c0_mid<N>(y, g, mu, s_mrg + J * 256, q, q2);
         if constexpr (J > 0) {   // the next limb's first chunk flies during this limb's transform
             const uint32_t *pn = phat + (size_t)(J - 1) * 2 * N + (size_t)g * V;
-            pre[0] = ldg_stream(pn);
-            pre[1] = ldg_stream(pn + N);
-            pre[2] = ldg_stream(chat_q + (size_t)(J - 1) * N + (size_t)g * V);
-            pre[3] = ldg_stream(chat_q + ((size_t)L + J - 1) * N + (size_t)g * V);
+            pre[0] = ldg_op<WALLY_OPLD_P8>(pn);
+            pre[1] = ldg_op<WALLY_OPLD_P8>(pn + N);
+            pre[2] = ldg_op<WALLY_OPLD_P8>(chat_q + (size_t)(J - 1) * N + (size_t)g * V);
+            pre[3] = ldg_op<WALLY_OPLD_P8>(chat_q + ((size_t)L + J - 1) * N + (size_t)g * V);
         }
         intt_chain<N, 1>(a, cx.tw + (size_t)J * Gm::TW_LIMB, g, q, q2, cx.bufA, cx.bufB);
         if (g < 32) {
@@ -1553,10 +1557,10 @@ __global__ void __launch_bounds__(NttGeom<8192>::T, 2) eval_kernel_p8(BatchArgs 
             uint4 pre[4];
             {
                 const uint32_t *pn = phat + (size_t)(L - 1) * 2 * N + (size_t)g * Gm::V;
-                pre[0] = ldg_stream(pn);
-                pre[1] = ldg_stream(pn + N);
-                pre[2] = ldg_stream(chat_q + (size_t)(L - 1) * N + (size_t)g * Gm::V);
-                pre[3] = ldg_stream(chat_q + (2 * (size_t)L - 1) * N + (size_t)g * Gm::V);
+                pre[0] = ldg_op<WALLY_OPLD_P8>(pn);
+                pre[1] = ldg_op<WALLY_OPLD_P8>(pn + N);
+                pre[2] = ldg_op<WALLY_OPLD_P8>(chat_q + (size_t)(L - 1) * N + (size_t)g * Gm::V);
+                pre[3] = ldg_op<WALLY_OPLD_P8>(chat_q + (2 * (size_t)L - 1) * N + (size_t)g * Gm::V);
             }
             LimbLoopP8M<L, L - 1>::run(a1, s_ba, chat_q, phat, g, cx, tcol, s_ybuf, par, s_cst, mu, s_mrg, pre);
             if (g < 32) c0_write_results<N>(s_ba, out_q, s_ybuf + (par ^ 1u) * Gm::T, g, mu);
@@ -1571,13 +1575,10 @@ __global__ void __launch_bounds__(NttGeom<8192>::T, 2) eval_kernel_p8(BatchArgs 
 
 template <int L, int FMT>
 static cudaError_t launch_eval_p8(const BatchArgs &a, cudaStream_t s, int num_sms) {
-    static bool configured = false;
+    static DeviceOnce once;
     const size_t smem = chain_smem<8192>(1);
-    if (!configured) {
-        cudaError_t e = allow_smem(eval_kernel_p8<L, FMT>, smem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    cudaError_t e = device_once(once, [&](int *) { return allow_smem(eval_kernel_p8<L, FMT>, smem); });
+    if (e != cudaSuccess) return e;
     eval_kernel_p8<L, FMT><<<num_sms * 2, NttGeom<8192>::T, smem, s>>>(a);   // two CTAs per SM
     return cudaGetLastError();
 }
@@ -1585,14 +1586,11 @@ static cudaError_t launch_eval_p8(const BatchArgs &a, cudaStream_t s, int num_sm
 template <int N, int L, int FMT>
 static cudaError_t launch_eval_tm(const BatchArgs &a, cudaStream_t s, int num_sms) {
     using Gm = NttGeom<N>;
-    static bool configured = false;
+    static DeviceOnce once;
     const size_t smem = (size_t)L * Gm::TW_LIMB * sizeof(uint2) +
                         (size_t)kEvalGroups * 2 * Gm::SMEM_WORDS * sizeof(uint32_t);
-    if (!configured) {
-        cudaError_t e = allow_smem(eval_kernel_tm<N, L, FMT>, smem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    cudaError_t e = device_once(once, [&](int *) { return allow_smem(eval_kernel_tm<N, L, FMT>, smem); });
+    if (e != cudaSuccess) return e;
     // one CTA per SM: it owns all 512 TMEM columns of its SM
     eval_kernel_tm<N, L, FMT><<<num_sms, kEvalGroups * Gm::T, smem, s>>>(a);
     return cudaGetLastError();
@@ -1601,8 +1599,8 @@ static cudaError_t launch_eval_tm(const BatchArgs &a, cudaStream_t s, int num_sm
 template <int N, int L>
 static cudaError_t launch_eval_nl(const BatchArgs &a, cudaStream_t s, int num_sms) {
     using Gm = NttGeom<N>;
-    static bool configured = false;
-    static int blocks_per_sm = 1;
+    static DeviceOnce once;
+    int blocks_per_sm = 1;
 #ifndef WALLY_EVAL_TMEM
 #define WALLY_EVAL_TMEM 1
 #endif
@@ -1620,29 +1618,27 @@ static cudaError_t launch_eval_nl(const BatchArgs &a, cudaStream_t s, int num_sm
     } else if constexpr (N <= 4096) {
         const size_t smem = (size_t)L * Gm::TW_LIMB * sizeof(uint2) +
                             (size_t)kEvalGroups * EvalCfg<N>::NC * Gm::SMEM_WORDS * sizeof(uint32_t);
-        if (!configured) {
-            cudaError_t e = allow_smem(eval_kernel_grp<N, L>, smem);
-            if (e != cudaSuccess) return e;
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, eval_kernel_grp<N, L>,
-                                                              kEvalGroups * Gm::T, smem);
-            if (e != cudaSuccess) return e;
-            if (blocks_per_sm < 1) blocks_per_sm = 1;
-            configured = true;
-        }
+        cudaError_t e = device_once(once, [&](int *v) {
+            cudaError_t r = allow_smem(eval_kernel_grp<N, L>, smem);
+            if (r == cudaSuccess)
+                r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(v, eval_kernel_grp<N, L>, kEvalGroups * Gm::T, smem);
+            return r;
+        }, &blocks_per_sm);
+        if (e != cudaSuccess) return e;
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
         eval_kernel_grp<N, L><<<num_sms * blocks_per_sm, kEvalGroups * Gm::T, smem, s>>>(a);
     } else {
         if constexpr (N == 8192 && WALLY_EVAL_TMEM) {
             if (pruned_c0_path(N, L, a.d, a.compact)) return launch_eval_p8<L, (int)WALLY_RESP_COMPACT>(a, s, num_sms);
         }
         const size_t smem = chain_smem<N>(EvalCfg<N>::NC);
-        if (!configured) {
-            cudaError_t e = allow_smem(eval_kernel<N, L>, smem);
-            if (e != cudaSuccess) return e;
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, eval_kernel<N, L>, Gm::T, smem);
-            if (e != cudaSuccess) return e;
-            if (blocks_per_sm < 1) blocks_per_sm = 1;
-            configured = true;
-        }
+        cudaError_t e = device_once(once, [&](int *v) {
+            cudaError_t r = allow_smem(eval_kernel<N, L>, smem);
+            if (r == cudaSuccess) r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(v, eval_kernel<N, L>, Gm::T, smem);
+            return r;
+        }, &blocks_per_sm);
+        if (e != cudaSuccess) return e;
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
         eval_kernel<N, L><<<num_sms * blocks_per_sm, Gm::T, smem, s>>>(a);
     }
     return cudaGetLastError();

@@ -54,6 +54,38 @@ __device__ __forceinline__ uint4 ldg_stream(const void *p) {
     return r;
 }
 
+// Operand loads of the fused kernels (plaintext slices and query NTTs, which
+// are re-read from L2 by the other queries / plaintexts of their cluster).
+// MODE 0: no L1 allocation, default L2 policy of .nc no_allocate loads;
+// MODE 1: L1-allocating read-only load (the other half of each 32-byte sector
+//         is read by the same thread's next chunk);
+// MODE 2: no L1 allocation, L2 evict_last cache hint;
+// MODE 3: L1-allocating, L2 evict_last cache hint.
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+template <int MODE>
+__device__ __forceinline__ uint4 ldg_op(const void *p) {
+    uint4 r;
+    if constexpr (MODE == 0) {
+        r = ldg_stream(p);
+    } else if constexpr (MODE == 1) {
+        r = __ldg(reinterpret_cast<const uint4 *>(p));
+    } else if constexpr (MODE == 2) {
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+            : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+            : "l"(p), "l"(l2_evict_last_policy()));
+    } else {
+        asm("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+            : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+            : "l"(p), "l"(l2_evict_last_policy()));
+    }
+    return r;
+}
+
 // ---------------------------------------------------------------------------
 // NTT pass geometry
 //

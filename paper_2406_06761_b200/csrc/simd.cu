@@ -28,6 +28,7 @@
 
 #include "ntt_device.cuh"
 #include "wally_simd.h"
+#include "wally_internal.h"
 
 namespace wally {
 namespace simd {
@@ -924,8 +925,8 @@ template <int N>
 static cudaError_t launch_ntt(wally_simd_ctx *c, uint32_t period, uint32_t grp, const uint32_t *in, size_t in_stride,
                               const uint32_t *sel, uint32_t *out, size_t out_stride, size_t count, uint32_t *err,
                               cudaStream_t s) {
-    static bool cfg = false;
-    if (!cfg) { cudaError_t e = allow(simd_ntt_kernel<N>, chain_smem<N>()); if (e) return e; cfg = true; }
+    static DeviceOnce once;
+    if (cudaError_t e = device_once(once, [&](int *) { return allow(simd_ntt_kernel<N>, chain_smem<N>()); })) return e;
     if (!count) return cudaSuccess;
     simd_ntt_kernel<N><<<(unsigned)count, NttGeom<N>::T, chain_smem<N>(), s>>>(c->md, c->d_twf, period, grp, in,
                                                                               in_stride, sel, out, out_stride, err);
@@ -937,13 +938,12 @@ template <int N>
 static cudaError_t launch_rotate(wally_simd_ctx *c, uint32_t units, const uint32_t *X, size_t xs, bool giant,
                                  uint32_t *ext, const uint32_t *keys, size_t key_stride, const uint32_t *uq,
                                  const uint32_t *add, size_t as, uint32_t *out, size_t os, cudaStream_t s) {
-    static bool cfg = false;
-    if (!cfg) {
-        cudaError_t e = allow(simd_modup_kernel<N>, chain_smem<N>());
-        if (!e) e = allow(simd_moddown_kernel<N>, chain_smem<N>());
-        if (e) return e;
-        cfg = true;
-    }
+    static DeviceOnce once;
+    if (cudaError_t e = device_once(once, [&](int *) {
+            cudaError_t r = allow(simd_modup_kernel<N>, chain_smem<N>());
+            return r ? r : allow(simd_moddown_kernel<N>, chain_smem<N>());
+        }))
+        return e;
     if (!units) return cudaSuccess;
     const uint32_t *perm = giant ? c->d_permg : c->d_perm1;
     simd_modup_kernel<N><<<dim3(units, c->L), NttGeom<N>::T, chain_smem<N>(), s>>>(c->md, c->d_twf, c->d_twi, X, xs,
@@ -965,12 +965,11 @@ static cudaError_t launch_chain(wally_simd_ctx *c, uint32_t units, bool giant, c
     if constexpr (N > 4096) {
         return cudaErrorNotSupported;
     } else {
-        static bool cfg = false;
-        if (!cfg) {
-            cudaError_t e = allow(simd_rot_chain_kernel<N>, chain_kernel_smem<N>(WALLY_MAX_LIMBS));
-            if (e) return e;
-            cfg = true;
-        }
+        static DeviceOnce once;
+        if (cudaError_t e = device_once(once, [&](int *) {
+                return allow(simd_rot_chain_kernel<N>, chain_kernel_smem<N>(WALLY_MAX_LIMBS));
+            }))
+            return e;
         if (!units || !steps) return cudaSuccess;
         simd_rot_chain_kernel<N><<<units, NttGeom<N>::T, chain_kernel_smem<N>(c->L), s>>>(
             c->md, c->d_twf, c->d_twi, giant ? c->d_permg : c->d_perm1, keys, key_stride, uq, X0, x0s, out_even,
@@ -1005,8 +1004,8 @@ template <int N>
 static cudaError_t launch_switch(wally_simd_ctx *c, uint32_t units, const uint32_t *X, size_t xs,
                                  const uint32_t *out_off, uint32_t *resp, cudaStream_t s) {
     const size_t smem = chain_smem<N>() + (size_t)c->L * N * sizeof(uint32_t);
-    static bool cfg = false;
-    if (!cfg) { cudaError_t e = allow(simd_switch_kernel<N>, chain_smem<N>() + (size_t)WALLY_MAX_LIMBS * N * 4); if (e) return e; cfg = true; }
+    static DeviceOnce once;
+    if (cudaError_t e = device_once(once, [&](int *) { return allow(simd_switch_kernel<N>, chain_smem<N>() + (size_t)WALLY_MAX_LIMBS * N * 4); })) return e;
     if (!units) return cudaSuccess;
     simd_switch_kernel<N><<<dim3(units, 2), NttGeom<N>::T, smem, s>>>(c->md, c->d_twi, X, xs, out_off, resp);
     c->launches++;
@@ -1015,8 +1014,8 @@ static cudaError_t launch_switch(wally_simd_ctx *c, uint32_t units, const uint32
 
 template <int N>
 static cudaError_t launch_encode(wally_simd_ctx *c, const BlockArgs &ba, uint32_t blocks, cudaStream_t s) {
-    static bool cfg = false;
-    if (!cfg) { cudaError_t e = allow(simd_encode_kernel<N>, chain_smem<N>()); if (e) return e; cfg = true; }
+    static DeviceOnce once;
+    if (cudaError_t e = device_once(once, [&](int *) { return allow(simd_encode_kernel<N>, chain_smem<N>()); })) return e;
     if (!blocks) return cudaSuccess;
     simd_encode_kernel<N><<<dim3(blocks, c->p.d), NttGeom<N>::T, chain_smem<N>(), s>>>(c->md, c->d_twf, c->d_twi, ba);
     c->launches++;

@@ -4,6 +4,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -120,6 +121,39 @@ inline uint64_t modmuls_per_pair(uint32_t n, uint32_t L, uint32_t d, bool pruned
     for (uint32_t s = 0; s < logn; s++) bf += (s < mu) ? (n >> (s + 1)) : n / (2 * M);
     const uint64_t c0 = (uint64_t)L * n + (uint64_t)L * bf + (n / M) * ms;
     return full + c0;
+}
+
+// One-time kernel configuration per device, safe under concurrent host
+// threads: cudaFuncSetAttribute(MaxDynamicSharedMemorySize) and occupancy
+// queries apply to the current device only, so a second context on another
+// device must configure again.  `f(int *value)` runs once per device; its
+// value (e.g. blocks per SM) is returned on every call.
+struct DeviceOnce {
+    std::mutex m;
+    uint64_t done = 0;
+    int value[64] = {};
+};
+template <typename F>
+inline cudaError_t device_once(DeviceOnce &o, F &&f, int *value_out = nullptr) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) {   // outside the cache: configure every time
+        int v = 0;
+        e = f(&v);
+        if (value_out) *value_out = v;
+        return e;
+    }
+    std::lock_guard<std::mutex> g(o.m);
+    if (!((o.done >> dev) & 1ull)) {
+        int v = 0;
+        e = f(&v);
+        if (e != cudaSuccess) return e;
+        o.value[dev] = v;
+        o.done |= 1ull << dev;
+    }
+    if (value_out) *value_out = o.value[dev];
+    return cudaSuccess;
 }
 
 // Kernel launchers (kernels.cu).  Each returns the cudaError_t of the launch

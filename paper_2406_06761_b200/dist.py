@@ -12,16 +12,20 @@ independent across queries and plaintexts, so nothing else is exchanged.
                  §8(f)-4, the Zipf skew of configs[4])
   * routing    : wally_route_plan (C ABI) -- identical on every rank, so only
                  the ciphertexts move; the ingress broadcasts the cluster ids
-  * scatter    : the ingress packs each rank's share contiguously with the
-                 wally_pack_queries kernel and sends it with grouped P2P
-                 (torch.distributed batch_isend_irecv: NCCL over NVLink on the
-                 GPU box, gloo in the CPU tests)
+                 over the control group (host tensors: no device sync)
+  * scatter    : the ingress packs each rank's share contiguously and sends
+                 it to its owner.  transport="wally": the C ABI's own NCCL
+                 data plane (wally_scatter_queries: pack_rows kernel + grouped
+                 ncclSend/ncclRecv inside libwally.so; Python only passes the
+                 NCCL unique id).  transport="torch": torch.distributed
+                 batch_isend_irecv (gloo on host tensors in the CPU tests and
+                 the two-process GPU test)
   * gather     : optional; each rank sends its response buffer to the
                  ingress, which receives the rank blocks back to back (the
                  layout wally_route_plan's gathered offsets describe)
 
 This module only marshals: the routing plan is computed by the C library,
-the packing by its kernel, the transfers by torch.distributed.
+the packing by its kernel, the transfers by NCCL (or torch.distributed).
 """
 from __future__ import annotations
 
@@ -32,19 +36,28 @@ from . import wally as W
 
 class Router:
     """Scatter/gather of one batch between the ingress rank `src` and the
-    owners.  `pack` (default: the wally_pack_queries kernel of `srv`) forms
-    the contiguous send buffer of a share on the ingress; tests inject a
-    host implementation to exercise the collective logic on CPU tensors."""
+    owners.
+
+    transport  "torch" (torch.distributed P2P on the tensors' device) or
+               "wally" (the C ABI's NCCL data plane; needs `srv`, device tensors)
+    group      process group of the torch transport and of comm setup (None = default)
+    ctrl_group process group for the host-side cluster-id broadcast (a gloo
+               group keeps it off the device; None = `group`)
+    pack       torch transport only: forms the contiguous send buffer of a
+               share on the ingress (default: the wally_pack_queries kernel of
+               `srv`); tests inject a host implementation."""
 
     def __init__(self, cluster_sizes, owner, n: int, d: int, L: int, group=None, src: int = 0, srv=None,
-                 pack=None, device=None, resp_format: int | None = None):
+                 pack=None, device=None, resp_format: int | None = None, transport: str = "torch",
+                 ctrl_group=None):
         import torch
         import torch.distributed as dist
         self.torch, self.dist = torch, dist
         self.group = group
+        self.ctrl_group = ctrl_group if ctrl_group is not None else group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
-        self.src = src
+        self.src = src                      # group-local rank of the ingress
         self.sizes = np.ascontiguousarray(cluster_sizes, dtype=np.uint32)
         # int32 owning rank per cluster, or uint64 replica masks (hot-cluster replication)
         if owner is None:
@@ -59,7 +72,17 @@ class Router:
         self.resp_format = resp_format
         self.row = 2 * L * n
         self.device = device if device is not None else "cpu"
-        if pack is None:
+        self.srv = srv
+        assert transport in ("torch", "wally")
+        self.transport = transport
+        if transport == "wally":
+            assert srv is not None, "the wally transport runs on the server context's NCCL communicator"
+            uid = torch.zeros(W.WALLY_COMM_ID_BYTES, dtype=torch.uint8)
+            if self.rank == src:
+                uid.copy_(torch.frombuffer(bytearray(W.wally_comm_unique_id()), dtype=torch.uint8))
+            self._bcast(uid, src, self.ctrl_group)
+            srv.comm_init(self.rank, self.world, bytes(uid.numpy()))
+        if pack is None and transport == "torch":
             assert srv is not None, "Router needs a WallyServer (pack kernel) or an explicit pack function"
 
             def pack(index_np, cts):
@@ -69,23 +92,49 @@ class Router:
                 return out
         self.pack = pack
 
+    # torch.distributed takes global ranks: map the group-local peers
+    def _peer(self, r: int, group=None) -> int:
+        g = self.group if group is None else group
+        return r if g is None else self.dist.get_global_rank(g, r)
+
+    def _bcast(self, t, src: int, group):
+        self.dist.broadcast(t, self._peer(src, group), group=group)
+
     def broadcast_ids(self, ids: np.ndarray | None, nq: int) -> np.ndarray:
-        """The ingress's cluster ids to every rank (small: 4 B per query)."""
+        """The ingress's cluster ids to every rank (4 B per query).  Over a
+        gloo control group the tensor stays on the host (no device sync)."""
         torch = self.torch
-        t = torch.empty(nq, dtype=torch.int32, device=self.device)
+        be = self.dist.get_backend(self.ctrl_group)
+        host = "gloo" in str(be)
+        t = torch.empty(nq, dtype=torch.int32, device="cpu" if host else self.device)
         if self.rank == self.src:
             t.copy_(torch.from_numpy(np.ascontiguousarray(ids, dtype=np.uint32).view(np.int32)))
-        self.dist.broadcast(t, self.src, group=self.group)
-        return t.cpu().numpy().view(np.uint32)
+        self._bcast(t, self.src, self.ctrl_group)
+        return (t if host else t.cpu()).numpy().view(np.uint32)
 
     def plan(self, ids: np.ndarray) -> W.RoutePlan:
         return W.wally_route_plan(ids, self.sizes, self.owner, self.n, self.d, self.world, self.resp_format)
 
-    def scatter(self, plan: W.RoutePlan, cts):
+    def scatter(self, plan: W.RoutePlan, cts, out=None, pack_buf=None, order_dev=None):
         """cts: [nq][2][L][n] int32 tensor on the ingress (ignored elsewhere).
-        Returns this rank's share [counts[rank]][2][L][n] in its local order."""
+        Returns this rank's share [counts[rank]][2][L][n] in its local order.
+        wally transport: `out` (the share buffer), `pack_buf` (ingress scratch
+        of cts' shape) and `order_dev` (plan.order on the device) may be passed
+        in to keep allocations and host->device copies out of a timed step."""
         torch, dist = self.torch, self.dist
         mine = int(plan.counts[self.rank])
+        if self.transport == "wally":
+            if out is None:
+                out = torch.empty((mine, 2, self.L, self.n), dtype=torch.int32, device=self.device)
+            if self.rank == self.src:
+                if order_dev is None:
+                    order_dev = torch.from_numpy(plan.order.view(np.int32)).to(self.device)
+                if pack_buf is None:
+                    pack_buf = torch.empty_like(cts)
+                self.srv.scatter_queries(self.src, plan.counts, order_dev, cts, pack_buf, out)
+            else:
+                self.srv.scatter_queries(self.src, plan.counts, share_dev=out)
+            return out[:mine]
         ops = []
         if self.rank == self.src:
             packed = self.pack(plan.order, cts) if plan.order.size else None
@@ -96,14 +145,14 @@ class Router:
                     local = packed[b:e] if e > b else torch.empty((0, 2, self.L, self.n), dtype=torch.int32,
                                                                    device=self.device)
                 elif e > b:
-                    ops.append(dist.P2POp(dist.isend, packed[b:e].contiguous(), r, group=self.group))
+                    ops.append(dist.P2POp(dist.isend, packed[b:e].contiguous(), self._peer(r), group=self.group))
             if ops:
                 for w in dist.batch_isend_irecv(ops):
                     w.wait()
             return local
         buf = torch.empty((mine, 2, self.L, self.n), dtype=torch.int32, device=self.device)
         if mine:
-            for w in dist.batch_isend_irecv([dist.P2POp(dist.irecv, buf, self.src, group=self.group)]):
+            for w in dist.batch_isend_irecv([dist.P2POp(dist.irecv, buf, self._peer(self.src), group=self.group)]):
                 w.wait()
         return buf
 
@@ -112,6 +161,12 @@ class Router:
         ingress (query q's responses start at plan.gathered_off[q]).  Returns
         the gathered int32 tensor on the ingress, None elsewhere."""
         torch, dist = self.torch, self.dist
+        if self.transport == "wally":
+            out = None
+            if self.rank == self.src:
+                out = torch.empty(max(1, int(plan.gathered_off[-1])), dtype=torch.int32, device=self.device)
+            self.srv.gather_responses(self.src, plan.resp_words, resp_local, out)
+            return out[:int(plan.gathered_off[-1])] if out is not None else None
         if self.rank == self.src:
             total = int(plan.gathered_off[-1])
             out = torch.empty(total, dtype=torch.int32, device=self.device)
@@ -124,14 +179,14 @@ class Router:
                 if r == self.src:
                     out[b:e].copy_(resp_local[:e - b])
                 else:
-                    ops.append(dist.P2POp(dist.irecv, out[b:e], r, group=self.group))
+                    ops.append(dist.P2POp(dist.irecv, out[b:e], self._peer(r), group=self.group))
             if ops:
                 for w in dist.batch_isend_irecv(ops):
                     w.wait()
             return out
         words = int(plan.resp_words[self.rank])
         if words:
-            for w in dist.batch_isend_irecv([dist.P2POp(dist.isend, resp_local[:words].contiguous(), self.src,
-                                                        group=self.group)]):
+            for w in dist.batch_isend_irecv([dist.P2POp(dist.isend, resp_local[:words].contiguous(),
+                                                        self._peer(self.src), group=self.group)]):
                 w.wait()
         return None

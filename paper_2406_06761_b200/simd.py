@@ -121,6 +121,7 @@ class SimdServer:
         form); resp_dev: device uint32/int32 with >= response_words(ids) words.  Returns the host offsets
         [nq+1] of each query's responses (words)."""
         ids = np.ascontiguousarray(ids, dtype=np.uint32)
+        self._check_buffers(ids, cts_dev, keys_dev, resp_dev, cuda=True)
         off = np.zeros(ids.size + 1, dtype=np.uint64)
         _check(lib.wally_simd_eval_batch(self.ctx, ids.size, ids.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
                                          cts_dev.data_ptr(), keys_dev.data_ptr(), resp_dev.data_ptr(),
@@ -132,12 +133,24 @@ class SimdServer:
         """The same from host buffers (torch CPU tensors, pinned for overlap); sub-batches are pipelined
         through device staging.  Returns the response offsets [nq+1] (words)."""
         ids = np.ascontiguousarray(ids, dtype=np.uint32)
+        self._check_buffers(ids, cts_host, keys_host, resp_host, cuda=False)
         off = np.zeros(ids.size + 1, dtype=np.uint64)
         _check(lib.wally_simd_eval_batch_host(self.ctx, ids.size, ids.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
                                               cts_host.data_ptr(), keys_host.data_ptr(), resp_host.data_ptr(),
                                               resp_host.numel(), off.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
                                               sub_batch, _stream(stream)), self.ctx)
         return off
+
+    def _check_buffers(self, ids, cts, keys, resp, cuda: bool):
+        """The C side reads nq*2*L*n ciphertext words and nq*key_words key
+        words and writes response_words(ids) words: check the tensors hold
+        exactly / at least that many contiguous 32-bit words on the right side."""
+        for name, t, words, exact in (("cts", cts, ids.size * 2 * self.L * self.n, True),
+                                      ("keys", keys, ids.size * self.key_words, True),
+                                      ("resp", resp, self.response_words(ids), False)):
+            assert t.is_cuda == cuda, f"{name} must be {'device' if cuda else 'host'} memory"
+            assert t.is_contiguous() and t.element_size() == 4, f"{name} must be contiguous 32-bit"
+            assert (t.numel() == words) if exact else (t.numel() >= words), f"{name}: {t.numel()} words, need {words}"
 
     def modmuls_per_query(self, blocks: int) -> int:
         return int(lib.wally_simd_modmuls_per_query(self.ctx, blocks))

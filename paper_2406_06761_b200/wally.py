@@ -22,7 +22,8 @@ _LIB_PATH = os.environ.get("WALLY_LIB", _build.LIB)
 
 WALLY_MAX_LIMBS = 4
 STATUS = {0: "WALLY_OK", -1: "WALLY_E_ARG", -2: "WALLY_E_PARAMS", -3: "WALLY_E_UNKNOWN_CLUSTER",
-          -4: "WALLY_E_RESIDUE", -5: "WALLY_E_STATE", -6: "WALLY_E_CUDA", -8: "WALLY_E_OOM"}
+          -4: "WALLY_E_RESIDUE", -5: "WALLY_E_STATE", -6: "WALLY_E_CUDA", -7: "WALLY_E_NCCL", -8: "WALLY_E_OOM"}
+WALLY_COMM_ID_BYTES = 128
 
 EXPORTED = [
     "wally_find_moduli", "wally_create", "wally_destroy", "wally_last_error", "wally_load_clusters",
@@ -32,7 +33,8 @@ EXPORTED = [
     "wally_ntt_forward", "wally_ntt_inverse", "wally_kernel_launches", "wally_enable_stage_timing",
     "wally_stage_times", "wally_assign_owners", "wally_route_plan", "wally_pack_queries",
     "wally_response_words_per_plaintext", "wally_assign_owners_replicated", "wally_route_plan_replicated",
-    "wally_load_clusters_replicated", "wally_modmuls_per_pair",
+    "wally_load_clusters_replicated", "wally_modmuls_per_pair", "wally_comm_unique_id", "wally_comm_init",
+    "wally_comm_check", "wally_scatter_queries", "wally_gather_responses",
 ]
 
 
@@ -93,6 +95,11 @@ def _load():
         "wally_load_clusters_replicated": ([vp, u32, P(u32), P(u64), i32], ctypes.c_int),
         "wally_modmuls_per_pair": ([vp, P(u64)], ctypes.c_int),
         "wally_pack_queries": ([vp, u32, vp, vp, vp, vp], ctypes.c_int),
+        "wally_comm_unique_id": ([vp], ctypes.c_int),
+        "wally_comm_init": ([vp, i32, i32, vp], ctypes.c_int),
+        "wally_comm_check": ([vp], ctypes.c_int),
+        "wally_scatter_queries": ([vp, i32, P(u32), vp, vp, vp, vp, vp], ctypes.c_int),
+        "wally_gather_responses": ([vp, i32, P(u64), vp, vp, vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -116,6 +123,21 @@ def _stream(stream) -> int | None:
     return getattr(stream, "cuda_stream", stream)
 
 
+def _check_host_words(buf, words: int, name: str, exact: bool = False) -> int:
+    """A host buffer the C side reads or writes `words` uint32 words of: a
+    contiguous 4-byte numpy array or CPU tensor with at least (or, with
+    exact=True, exactly) that many elements.  Returns its address."""
+    if hasattr(buf, "data_ptr"):
+        assert not buf.is_cuda, f"{name} must be host memory"
+        assert buf.is_contiguous() and buf.element_size() == 4, f"{name} must be contiguous 32-bit"
+        n, ptr = buf.numel(), buf.data_ptr()
+    else:
+        assert buf.flags["C_CONTIGUOUS"] and buf.dtype.itemsize == 4, f"{name} must be contiguous 32-bit"
+        n, ptr = buf.size, buf.ctypes.data
+    assert (n == words) if exact else (n >= words), f"{name} has {n} words, needs {words}"
+    return ptr
+
+
 def _check(rc: int, ctx=None):
     if rc != 0:
         msg = lib.wally_last_error(ctx)
@@ -126,6 +148,13 @@ def wally_find_moduli(n: int, num_limbs: int) -> list[int]:
     out = np.zeros(num_limbs, dtype=np.uint32)
     _check(lib.wally_find_moduli(n, num_limbs, _u32p(out)))
     return [int(x) for x in out]
+
+
+def wally_comm_unique_id() -> bytes:
+    """A fresh NCCL unique id (128 bytes) for wally_comm_init (call on one rank, share with all)."""
+    buf = (ctypes.c_uint8 * WALLY_COMM_ID_BYTES)()
+    _check(lib.wally_comm_unique_id(buf))
+    return bytes(buf)
 
 
 def wally_assign_owners(weights, world: int) -> np.ndarray:
@@ -305,8 +334,10 @@ class WallyServer:
 
     def fetch_responses(self, responses_dev, out_host: np.ndarray | None = None, stream=None) -> np.ndarray:
         words = responses_dev.numel()
+        assert responses_dev.is_cuda and responses_dev.is_contiguous() and responses_dev.element_size() == 4
         if out_host is None:
             out_host = np.empty(words, dtype=np.uint32)
+        _check_host_words(out_host, words, "out_host")
         _check(lib.wally_fetch_responses(self.ctx, responses_dev.data_ptr(), words, out_host.ctypes.data,
                                          _stream(stream)), self.ctx)
         return out_host
@@ -319,11 +350,10 @@ class WallyServer:
     def eval_batch_host(self, cluster_of_query, query_ct_host, responses_host, sub_batch, workspace, stream=None):
         """query_ct_host / responses_host: host buffers (numpy uint32 or pinned torch CPU tensors)."""
         ids = np.ascontiguousarray(cluster_of_query, dtype=np.uint32)
-        qptr = query_ct_host.data_ptr() if hasattr(query_ct_host, "data_ptr") else query_ct_host.ctypes.data
-        if hasattr(responses_host, "data_ptr"):
-            rptr, rwords = responses_host.data_ptr(), responses_host.numel()
-        else:
-            rptr, rwords = responses_host.ctypes.data, responses_host.size
+        qptr = _check_host_words(query_ct_host, ids.size * 2 * self.L * self.n, "query_ct_host", exact=True)
+        rwords = responses_host.numel() if hasattr(responses_host, "numel") else responses_host.size
+        rptr = _check_host_words(responses_host, rwords, "responses_host")
+        assert workspace.is_cuda and workspace.numel() * workspace.element_size() >= self.host_workspace_bytes(sub_batch)
         _check(lib.wally_eval_batch_host(self.ctx, ids.size, _u32p(ids), qptr, rptr, rwords, sub_batch,
                                          workspace.data_ptr(), workspace.numel() * 4, _stream(stream)), self.ctx)
 
@@ -340,6 +370,49 @@ class WallyServer:
         assert out_dev.numel() >= count * 2 * self.L * self.n
         _check(lib.wally_pack_queries(self.ctx, count, index_dev.data_ptr(), query_ct_dev.data_ptr(),
                                       out_dev.data_ptr(), _stream(stream)), self.ctx)
+
+    # ---- multi-GPU data plane (NCCL inside the C ABI) ----
+    def comm_init(self, rank: int, world: int, unique_id: bytes):
+        """Join the NCCL communicator `unique_id` (wally_comm_unique_id on one rank) as rank of world."""
+        assert len(unique_id) == WALLY_COMM_ID_BYTES
+        buf = (ctypes.c_uint8 * WALLY_COMM_ID_BYTES).from_buffer_copy(unique_id)
+        _check(lib.wally_comm_init(self.ctx, rank, world, buf), self.ctx)
+        self.comm_rank, self.comm_world = rank, world
+
+    def comm_check(self):
+        _check(lib.wally_comm_check(self.ctx), self.ctx)
+
+    def scatter_queries(self, src: int, counts, order_dev=None, query_ct_dev=None, pack_dev=None, share_dev=None,
+                        stream=None):
+        """Query scatter over NCCL (include/wally.h): counts uint32 [world] on every rank; on src the
+        route order (device uint32/int32 [nq]), the batch [nq][2][L][n] and a pack buffer of the same
+        shape; share_dev [counts[rank]][2][L][n] receives this rank's queries."""
+        counts = np.ascontiguousarray(counts, dtype=np.uint32)
+        assert counts.size == self.comm_world
+        row = 2 * self.L * self.n
+        nq = int(counts.sum())
+        mine = int(counts[self.comm_rank])
+        if share_dev is not None:
+            assert share_dev.is_cuda and share_dev.is_contiguous() and share_dev.numel() >= mine * row
+        if self.comm_rank == src and nq:
+            for t, words in ((order_dev, nq), (query_ct_dev, nq * row), (pack_dev, nq * row)):
+                assert t is not None and t.is_cuda and t.is_contiguous() and t.element_size() == 4
+                assert t.numel() >= words
+        ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+        _check(lib.wally_scatter_queries(self.ctx, src, _u32p(counts), ptr(order_dev), ptr(query_ct_dev),
+                                         ptr(pack_dev), ptr(share_dev), _stream(stream)), self.ctx)
+
+    def gather_responses(self, dst: int, resp_words, resp_dev, gathered_dev=None, stream=None):
+        """Response gather over NCCL: resp_words uint64 [world] on every rank; gathered_dev on dst only."""
+        words = np.ascontiguousarray(resp_words, dtype=np.uint64)
+        assert words.size == self.comm_world
+        if int(words[self.comm_rank]):
+            assert resp_dev.is_cuda and resp_dev.numel() >= int(words[self.comm_rank])
+        if self.comm_rank == dst and int(words.sum()):
+            assert gathered_dev is not None and gathered_dev.is_cuda and gathered_dev.numel() >= int(words.sum())
+        ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+        _check(lib.wally_gather_responses(self.ctx, dst, words.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                          ptr(resp_dev), ptr(gathered_dev), _stream(stream)), self.ctx)
 
     def ntt_forward(self, x_dev, out_dev, count: int, stream=None):
         _check(lib.wally_ntt_forward(self.ctx, x_dev.data_ptr(), out_dev.data_ptr(), count, _stream(stream)),
