@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 
 #include "ntt_device.cuh"
 #include "tmem.cuh"
@@ -57,9 +58,11 @@ __global__ void __launch_bounds__(NttGeom<N>::T) ntt_forward_kernel(KParams kp, 
         }
     if (bad && err) atomicOr(err, (uint32_t)kErrResidue);
     ntt_chain<N, 1>(a, tw + (size_t)limb * Gm::TW_LIMB, g, q, q2, bufA, bufB);
-    uint4 *dst = reinterpret_cast<uint4 *>(out + poly * N + (size_t)g * V);
+    uint32_t *dst = out + poly * N;
 #pragma unroll
-    for (int v = 0; v < V / 4; v++) dst[v] = make_uint4(a[0][4 * v], a[0][4 * v + 1], a[0][4 * v + 2], a[0][4 * v + 3]);
+    for (int v = 0; v < V / 4; v++)
+        *reinterpret_cast<uint4 *>(dst + ntt_word<N>(g, v)) =
+            make_uint4(a[0][4 * v], a[0][4 * v + 1], a[0][4 * v + 2], a[0][4 * v + 3]);
 }
 
 // Debug/test inverse NTT: out = n^{-1} INTT(in), canonical.
@@ -76,10 +79,10 @@ __global__ void __launch_bounds__(NttGeom<N>::T) ntt_inverse_kernel(KParams kp, 
     const uint32_t limb = (uint32_t)(poly % L);
     const uint32_t q = kp.q[limb], q2 = kp.q2[limb];
     uint32_t a[1][V];
-    const uint4 *src = reinterpret_cast<const uint4 *>(in + poly * N + (size_t)g * V);
+    const uint32_t *src = in + poly * N;
 #pragma unroll
     for (int v = 0; v < V / 4; v++) {
-        const uint4 x = __ldg(src + v);
+        const uint4 x = __ldg(reinterpret_cast<const uint4 *>(src + ntt_word<N>(g, v)));
         // scale first (the transform is linear); Shoup accepts any 32-bit input -> [0, 2q)
         a[0][4 * v + 0] = shoup_mul(x.x, kp.ninv[limb], kp.ninvp[limb], q);
         a[0][4 * v + 1] = shoup_mul(x.y, kp.ninv[limb], kp.ninvp[limb], q);
@@ -125,12 +128,17 @@ __global__ void __launch_bounds__(NttGeom<N>::T) encode_kernel(EncodeArgs ea) {
             a[0][j * Gm::R2 + kk] = (x < 0) ? (uint32_t)((int64_t)q + x) : (uint32_t)x;  // x mod q (reading S8)
         }
     ntt_chain<N, 1>(a, ea.tw_fwd + (size_t)limb * Gm::TW_LIMB, g, q, q2, bufA, bufB);
-    uint32_t *dst = ea.store + ((size_t)pt * ea.L + limb) * 2 * N + (size_t)g * V;
+    uint32_t *dst = ea.store + ((size_t)pt * ea.L + limb) * 2 * N;
 #pragma unroll
-    for (int v = 0; v < V; v++) {
-        uint32_t y = csub(shoup_mul(a[0][v], ea.kp.fold[limb], ea.kp.foldp[limb], q), q);  // canonical
-        dst[v] = y;
-        dst[N + v] = (uint32_t)(((uint64_t)y << 32) / q);                                  // Shoup companion
+    for (int v = 0; v < V / 4; v++) {
+        uint32_t y[4], yp[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            y[i] = csub(shoup_mul(a[0][4 * v + i], ea.kp.fold[limb], ea.kp.foldp[limb], q), q);  // canonical
+            yp[i] = (uint32_t)(((uint64_t)y[i] << 32) / q);                                    // Shoup companion
+        }
+        *reinterpret_cast<uint4 *>(dst + ntt_word<N>(g, v)) = make_uint4(y[0], y[1], y[2], y[3]);
+        *reinterpret_cast<uint4 *>(dst + N + ntt_word<N>(g, v)) = make_uint4(yp[0], yp[1], yp[2], yp[3]);
     }
 }
 
@@ -332,13 +340,13 @@ __device__ __forceinline__ void eval_limb(EvalState<N, L, NC> &st, const BatchAr
     using Gm = NttGeom<N>;
     constexpr int V = Gm::V;
     const uint32_t q = ba.kp.q[J], q2 = ba.kp.q2[J];
-    const uint32_t *pv = phat + (size_t)J * 2 * N + (size_t)g * V;
+    const uint32_t *pv = phat + (size_t)J * 2 * N;
 #pragma unroll
     for (int v = 0; v < V / 4; v++) {
-        const uint4 p = ldg_stream(pv + 4 * v), pp = ldg_stream(pv + N + 4 * v);
+        const uint4 p = ldg_stream(pv + ntt_word<N>(g, v)), pp = ldg_stream(pv + N + ntt_word<N>(g, v));
 #pragma unroll
         for (int c = 0; c < NC; c++) {
-            const uint4 x = ldg_stream(chat_q + ((size_t)(comp0 + c) * L + J) * N + (size_t)g * V + 4 * v);
+            const uint4 x = ldg_stream(chat_q + ((size_t)(comp0 + c) * L + J) * N + ntt_word<N>(g, v));
             st.a[c][4 * v + 0] = shoup_mul(x.x, p.x, pp.x, q);
             st.a[c][4 * v + 1] = shoup_mul(x.y, p.y, pp.y, q);
             st.a[c][4 * v + 2] = shoup_mul(x.z, p.z, pp.z, q);
@@ -696,6 +704,7 @@ __device__ __forceinline__ void eval_item_tm(const BatchArgs &ba, const ItemCurs
                                              const volatile uint32_t *s_next, ItemCursor &ncur) {
     using Gm = NttGeom<N>;
     constexpr int V = Gm::V, NC = 2;
+    static_assert(!NttStore<N>::CHUNK_MAJOR, "thread-major NTT-domain storage (ntt_word)");
     const uint32_t li = cur.li;
     const uint32_t cnt = ba.counts[li];
     const uint32_t local = item - cur.b;
@@ -1245,6 +1254,7 @@ __device__ __forceinline__ void eval_item_pr(const BatchArgs &ba, const ItemCurs
     constexpr int N = 4096;
     using Gm = NttGeom<N>;
     constexpr int V = Gm::V;
+    static_assert(!NttStore<N>::CHUNK_MAJOR, "thread-major NTT-domain storage (ntt_word)");
     const uint32_t li = cur.li;
     const uint32_t cnt = ba.counts[li];
     const uint32_t local = item - cur.b;
@@ -1409,10 +1419,11 @@ struct LimbLoopP8M {
         static_assert(V == 32, "the c0 tree assumes 32 values per thread");
         constexpr int NA = (L > 2) ? (L - 2) : 1;
         const uint32_t q = ba.kp.q[J], q2 = ba.kp.q2[J];
-        const uint4 *pv = reinterpret_cast<const uint4 *>(phat + (size_t)J * 2 * N + (size_t)g * V);
-        const uint4 *ppv = reinterpret_cast<const uint4 *>(phat + (size_t)J * 2 * N + N + (size_t)g * V);
-        const uint4 *c0v = reinterpret_cast<const uint4 *>(chat_q + (size_t)J * N + (size_t)g * V);
-        const uint4 *c1v = reinterpret_cast<const uint4 *>(chat_q + ((size_t)L + J) * N + (size_t)g * V);
+        static_assert(NttStore<N>::CHUNK_MAJOR, "chunk c of thread g at uint4 index c T + g");
+        const uint4 *pv = reinterpret_cast<const uint4 *>(phat + (size_t)J * 2 * N) + g;
+        const uint4 *ppv = reinterpret_cast<const uint4 *>(phat + (size_t)J * 2 * N + N) + g;
+        const uint4 *c0v = reinterpret_cast<const uint4 *>(chat_q + (size_t)J * N) + g;
+        const uint4 *c1v = reinterpret_cast<const uint4 *>(chat_q + ((size_t)L + J) * N) + g;
         const uint4 *t4 = reinterpret_cast<const uint4 *>(ba.tw_inv + (size_t)J * Gm::TW_LIMB) + g;
         auto tw = [&](int slot) -> uint2 { return __ldg(reinterpret_cast<const uint2 *>(t4 + (slot / 2) * T) + (slot % 2)); };
         auto yo = [&](uint32_t X, uint32_t Y, uint2 w) { return shoup_mul(X - Y + q2, w.x, w.y, q); };
@@ -1422,10 +1433,10 @@ struct LimbLoopP8M {
         for (int c = 0; c < 8; c++) {
             const uint4 p = np, pp = npp, x0 = nx0, x1 = nx1;
             if (c + 1 < 8) {     // the next chunk's loads fly while this chunk computes
-                np = ldg_op<WALLY_OPLD_P8>(pv + c + 1);
-                npp = ldg_op<WALLY_OPLD_P8>(ppv + c + 1);
-                nx0 = ldg_op<WALLY_OPLD_P8>(c0v + c + 1);
-                nx1 = ldg_op<WALLY_OPLD_P8>(c1v + c + 1);
+                np = ldg_op<WALLY_OPLD_P8>(pv + (c + 1) * T);
+                npp = ldg_op<WALLY_OPLD_P8>(ppv + (c + 1) * T);
+                nx0 = ldg_op<WALLY_OPLD_P8>(c0v + (c + 1) * T);
+                nx1 = ldg_op<WALLY_OPLD_P8>(c1v + (c + 1) * T);
             }
             a[0][4 * c + 0] = shoup_mul(x1.x, p.x, pp.x, q);
             a[0][4 * c + 1] = shoup_mul(x1.y, p.y, pp.y, q);
@@ -1452,11 +1463,11 @@ struct LimbLoopP8M {
         uint32_t *z = ybuf + par * T;
         z[g] = c0_mid<N>(y, g, mu, s_mrg + J * 256, q, q2);
         if constexpr (J > 0) {   // the next limb's first chunk flies during this limb's transform
-            const uint32_t *pn = phat + (size_t)(J - 1) * 2 * N + (size_t)g * V;
+            const uint32_t *pn = phat + (size_t)(J - 1) * 2 * N + 4 * g;
             pre[0] = ldg_op<WALLY_OPLD_P8>(pn);
             pre[1] = ldg_op<WALLY_OPLD_P8>(pn + N);
-            pre[2] = ldg_op<WALLY_OPLD_P8>(chat_q + (size_t)(J - 1) * N + (size_t)g * V);
-            pre[3] = ldg_op<WALLY_OPLD_P8>(chat_q + ((size_t)L + J - 1) * N + (size_t)g * V);
+            pre[2] = ldg_op<WALLY_OPLD_P8>(chat_q + (size_t)(J - 1) * N + 4 * g);
+            pre[3] = ldg_op<WALLY_OPLD_P8>(chat_q + ((size_t)L + J - 1) * N + 4 * g);
         }
         intt_chain<N, 1>(a, cx.tw + (size_t)J * Gm::TW_LIMB, g, q, q2, cx.bufA, cx.bufB);
         if (g < 32) {
@@ -1556,11 +1567,11 @@ __global__ void __launch_bounds__(NttGeom<8192>::T, 2) eval_kernel_p8(BatchArgs 
             uint32_t a1[1][Gm::V];
             uint4 pre[4];
             {
-                const uint32_t *pn = phat + (size_t)(L - 1) * 2 * N + (size_t)g * Gm::V;
+                const uint32_t *pn = phat + (size_t)(L - 1) * 2 * N + 4 * g;
                 pre[0] = ldg_op<WALLY_OPLD_P8>(pn);
                 pre[1] = ldg_op<WALLY_OPLD_P8>(pn + N);
-                pre[2] = ldg_op<WALLY_OPLD_P8>(chat_q + (size_t)(L - 1) * N + (size_t)g * Gm::V);
-                pre[3] = ldg_op<WALLY_OPLD_P8>(chat_q + (2 * (size_t)L - 1) * N + (size_t)g * Gm::V);
+                pre[2] = ldg_op<WALLY_OPLD_P8>(chat_q + (size_t)(L - 1) * N + 4 * g);
+                pre[3] = ldg_op<WALLY_OPLD_P8>(chat_q + (2 * (size_t)L - 1) * N + 4 * g);
             }
             LimbLoopP8M<L, L - 1>::run(a1, s_ba, chat_q, phat, g, cx, tcol, s_ybuf, par, s_cst, mu, s_mrg, pre);
             if (g < 32) c0_write_results<N>(s_ba, out_q, s_ybuf + (par ^ 1u) * Gm::T, g, mu);
@@ -1580,6 +1591,362 @@ static cudaError_t launch_eval_p8(const BatchArgs &a, cudaStream_t s, int num_sm
     cudaError_t e = device_once(once, [&](int *) { return allow_smem(eval_kernel_p8<L, FMT>, smem); });
     if (e != cudaSuccess) return e;
     eval_kernel_p8<L, FMT><<<num_sms * 2, NttGeom<8192>::T, smem, s>>>(a);   // two CTAs per SM
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// n = 8192, compact responses, 32 | d (c4), v5: operands staged by bulk
+// asynchronous copies (cp.async.bulk + mbarrier, "TMA or cp.async staging of
+// the NTT-domain plaintexts", north_star) instead of register prefetch.
+//
+// One CTA of two 256-thread groups per SM; the groups evaluate two queries
+// of the same work item in step (group 0 the even, group 1 the odd queries of
+// the chunk of queries), so every staged plaintext chunk and twiddle block
+// serves both.  The operands of one (query pair, limb) stream through a ring
+// of NSLOT shared-memory slots, one per 4-value chunk c of every thread
+// (chunk-major NTT-domain storage, ntt_store: chunk c of all threads is one
+// 4 KB block):
+//   [p chunk][p' chunk][pass-0 stage-0 twiddle block c][c0, c1 chunk of
+//   group 0's query][c0, c1 chunk of group 1's query]      (28 KB per slot)
+// A producer thread (thread 0) keeps the ring NSLOT - 1 chunks ahead; a
+// full barrier per slot carries the transaction bytes, an empty barrier per
+// slot collects one arrival per warp.  The limb's other pass-0 twiddle blocks
+// (stages 1-4: 32 KB) go to a limb buffer refilled after every warp is done
+// with the limb's last chunk; the pass-1/2 tables of all limbs stay resident.
+// c1's pass 0 runs inside the chunk loop as a tree over the chunks sharing
+// the twiddle reads of c0's Y-only tree; passes 1 and 2 through the group's
+// exchange buffer; c0's shuffle stages and warp-0 tail as in v3; c1's
+// switch state in tensor memory.  No register holds a prefetched operand.
+// ---------------------------------------------------------------------------
+namespace p8t {
+constexpr int N = 8192;
+constexpr int T = NttGeom<N>::T;                 // 256 threads per group
+constexpr int NSLOT = 3;
+constexpr int CHUNK_BYTES = T * 16;              // one 16-byte chunk of every thread: 4 KB
+constexpr int SLOT_BYTES = 7 * CHUNK_BYTES;      // p, p', stage-0 twiddles, 2 x (c0, c1)
+constexpr int LTW_BYTES = 8 * CHUNK_BYTES;       // pass-0 twiddle blocks 8..15 (stages 1-4)
+constexpr int TW12 = NttGeom<N>::TW_LIMB - NttGeom<N>::TW1;   // pass-1/2 table entries per limb
+constexpr int XB_WORDS = NttGeom<N>::SMEM_WORDS;
+__host__ __device__ constexpr size_t smem_bytes(int L) {
+    return (size_t)NSLOT * SLOT_BYTES + LTW_BYTES + (size_t)L * TW12 * 8 + 2ull * XB_WORDS * 4;
+}
+}  // namespace p8t
+
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t mbar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(mbar)
+                 : "memory");
+}
+
+// c1's passes 1 and 2 for one group (pass 0 done), tables in shared memory,
+// one exchange buffer, named barrier `bar` (four barriers).
+__device__ __forceinline__ void p8t_intt_tail(uint32_t (&a)[1][32], const uint2 *tw12, int g, uint32_t q, uint32_t q2,
+                                              uint32_t *buf, int bar) {
+    constexpr int N = 8192;
+    using Gm = NttGeom<N>;
+    group_sync(bar, Gm::T);
+    smem_store<N, Gm::TB0, Gm::R0, 1, 0>(buf, a, g);
+    group_sync(bar, Gm::T);
+    smem_load<N, Gm::TB1, Gm::R1, 1, 0>(buf, a, g);
+    ntt_pass<N, Gm::TB1, Gm::R1, true, 1, true>(a, tw12, g, q, q2);
+    group_sync(bar, Gm::T);
+    smem_store<N, Gm::TB1, Gm::R1, 1, 1>(buf, a, g);
+    group_sync(bar, Gm::T);
+    smem_load<N, Gm::TB2, Gm::R2, 1, 1>(buf, a, g);
+    ntt_pass<N, Gm::TB2, Gm::R2, true, 1, true>(a, tw12 + (Gm::TW2 - Gm::TW1), g, q, q2);
+}
+
+// Modulus-switch step of limb J for c1's 32 values per thread (n = 8192),
+// the drop-last state in tensor memory (rtop in columns 0..31, acc[l] in
+// 32 l .. 32 l + 31), eight values at a time.
+template <int L, int J>
+__device__ __forceinline__ void p8_ms_limb(uint32_t (&a)[1][32], uint32_t tcol, const KParams &kp) {
+    constexpr int NA = (L > 2) ? (L - 2) : 1;
+    if constexpr (L > 1 && J < L - 1) tmem_wait_st_all();
+#pragma unroll
+    for (int c8 = 0; c8 < 4; c8++) {
+        uint32_t rt[8], ac[NA][8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            rt[k] = 0;
+#pragma unroll
+            for (int l = 0; l < NA; l++) ac[l][k] = 0;
+        }
+        if constexpr (L > 1 && J == L - 2) {
+            tmem_ld<8>(tcol + 8 * c8, rt);
+            tmem_wait_ld<8>(rt);
+        }
+        if constexpr (L > 2 && J < L - 2) {
+#pragma unroll
+            for (int l = 0; l <= J; l++) {
+                tmem_ld<8>(tcol + 32 * l + 8 * c8, ac[l]);
+                tmem_wait_ld<8>(ac[l]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            uint32_t acc[NA];
+#pragma unroll
+            for (int l = 0; l < NA; l++) acc[l] = ac[l][k];
+            ms_elem<L, J, NA>(a[0][8 * c8 + k], rt[k], acc, kp);
+#pragma unroll
+            for (int l = 0; l < NA; l++) ac[l][k] = acc[l];
+        }
+        if constexpr (L > 1 && J == L - 1) tmem_st<8>(tcol + 8 * c8, rt);
+        if constexpr (L > 2 && J > 0 && J <= L - 2) {
+#pragma unroll
+            for (int l = 0; l < J; l++) tmem_st<8>(tcol + 32 * l + 8 * c8, ac[l]);
+        }
+    }
+}
+
+// Run-time limb index -> the compile-time instantiations (limbs J < L).
+template <int L, typename F>
+__device__ __forceinline__ void limb_dispatch(int J, F &&f) {
+    switch (J) {
+        case 0: f(std::integral_constant<int, 0>{}); break;
+        case 1: if constexpr (L > 1) f(std::integral_constant<int, (L > 1 ? 1 : 0)>{}); break;
+        case 2: if constexpr (L > 2) f(std::integral_constant<int, (L > 2 ? 2 : 0)>{}); break;
+        default: if constexpr (L > 3) f(std::integral_constant<int, (L > 3 ? 3 : 0)>{}); break;
+    }
+}
+
+template <int L, int FMT>
+__global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(BatchArgs ba) {
+    using namespace p8t;
+    using Gm = NttGeom<N>;
+    constexpr int V = Gm::V;
+    constexpr int NA = (L > 2) ? (L - 2) : 1;
+    constexpr int CHUNKS = V / 4;                 // 8 chunks of 4 values per thread and limb
+    extern __shared__ __align__(128) uint8_t smem8[];
+    uint8_t *slots = smem8;
+    const uint4 *ltw = reinterpret_cast<const uint4 *>(smem8 + NSLOT * SLOT_BYTES);
+    uint2 *s_tw12 = reinterpret_cast<uint2 *>(smem8 + NSLOT * SLOT_BYTES + LTW_BYTES);
+    uint32_t *xbuf = reinterpret_cast<uint32_t *>(smem8 + NSLOT * SLOT_BYTES + LTW_BYTES + (size_t)L * TW12 * 8);
+    __shared__ BatchArgs s_ba;
+    __shared__ uint32_t s_taddr;
+    __shared__ uint32_t s_item[2];
+    __shared__ uint32_t s_rmap[ResultMap<N>::WORDS];
+    __shared__ uint32_t s_ybuf[2][2 * T];
+    __shared__ uint32_t s_cst[2][(N / 32) * (1 + NA)];
+    __shared__ uint2 s_mrg[L * 256];
+    __shared__ __align__(8) uint64_t s_bar[2 * NSLOT + 2];   // full[NSLOT], empty[NSLOT], full_tw, empty_tw
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int grp = threadIdx.x / T, g = threadIdx.x % T;
+    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(s_bar);
+    auto full_b = [&](int i) { return bar0 + 8u * i; };
+    auto empty_b = [&](int i) { return bar0 + 8u * (NSLOT + i); };
+    const uint32_t full_tw = bar0 + 8u * (2 * NSLOT), empty_tw = bar0 + 8u * (2 * NSLOT + 1);
+    if (threadIdx.x == 0) {
+        s_ba = ba;
+        for (int i = 0; i < NSLOT; i++) {
+            mbar_init(full_b(i), 1);
+            mbar_init(empty_b(i), 2 * T / 32);
+        }
+        mbar_init(full_tw, 1);
+        mbar_init(empty_tw, 2 * T / 32);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {   // 512 columns: four warps share a lane quadrant, 128 columns each
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&s_taddr);
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(dst) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    for (int i = threadIdx.x; i < L * 256; i += blockDim.x) s_mrg[i] = __ldg(ba.tw_mrg + (size_t)(i >> 8) * N + (i & 255));
+    for (int i = threadIdx.x; i < L * TW12; i += blockDim.x)
+        s_tw12[i] = __ldg(ba.tw_inv + (size_t)(i / TW12) * Gm::TW_LIMB + Gm::TW1 + (i % TW12));
+    build_result_map<N>(s_rmap, ba.d);
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tcol = s_taddr + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 128);
+    uint32_t *xb = xbuf + grp * XB_WORDS;
+    const int bar = 1 + grp;
+    const int mu = min(__ffs((int)ba.d) - 1, 13);
+    const uint32_t total = ba.misc[kMiscTotalItems];
+    const uint32_t slots_s = (uint32_t)__cvta_generic_to_shared(slots);
+    const uint32_t ltw_s = (uint32_t)__cvta_generic_to_shared(ltw);
+    uint32_t seq = 0;      // chunk slots consumed by this CTA so far (ring position and phases)
+    uint32_t tseq = 0;     // limb twiddle buffers consumed so far
+    uint32_t par = 0;
+    ItemCursor cur;
+    for (uint32_t it = 0;; it++) {
+        if (threadIdx.x == 0) s_item[it & 1] = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
+        __syncthreads();
+        const uint32_t item = s_item[it & 1];
+        if (item >= total) break;
+        cur.seek(s_ba, item);
+        const uint32_t li = cur.li;
+        const uint32_t cnt = s_ba.counts[li];
+        const uint32_t P = s_ba.n_pt[li];
+        const uint32_t ch = (item - cur.b) / P, k = (item - cur.b) % P;
+        const uint32_t qb = s_ba.seg[li] + ch * s_ba.chunk;
+        const uint32_t qe = min(qb + s_ba.chunk, s_ba.seg[li] + cnt);
+        const uint32_t *phat = s_ba.store + (size_t)(s_ba.pt_base[li] + k) * L * 2 * N;
+        const uint32_t rounds = (qe - qb + 1) / 2;
+        const uint32_t nchunks = rounds * L * CHUNKS;    // the item's chunk stream: round, limb L-1..0, chunk
+        const uint32_t seq0 = seq, tseq0 = tseq;
+        // producer: stream element j -> slot (seq0 + j) % NSLOT
+        auto produce = [&](uint32_t j) {
+            const uint32_t sq = seq0 + j, sl = sq % NSLOT;
+            if (sq >= NSLOT) mbar_wait(empty_b(sl), ((sq / NSLOT) + 1) & 1u);   // consumers of sq - NSLOT done
+            const uint32_t r = j / (L * CHUNKS), J = L - 1 - (j / CHUNKS) % L, c = j % CHUNKS;
+            const uint32_t q0 = qb + 2 * r, nq = min(2u, qe - q0);
+            mbar_expect_tx(full_b(sl), (3 + 2 * nq) * CHUNK_BYTES);
+            const uint32_t dst = slots_s + sl * SLOT_BYTES;
+            const uint32_t *pj = phat + (size_t)J * 2 * N + (size_t)c * 4 * T;
+            bulk_g2s(dst, pj, CHUNK_BYTES, full_b(sl));
+            bulk_g2s(dst + CHUNK_BYTES, pj + N, CHUNK_BYTES, full_b(sl));
+            bulk_g2s(dst + 2 * CHUNK_BYTES, reinterpret_cast<const uint4 *>(s_ba.tw_inv + (size_t)J * Gm::TW_LIMB) + c * T,
+                     CHUNK_BYTES, full_b(sl));
+            for (uint32_t u = 0; u < nq; u++) {
+                const uint32_t *cq = s_ba.chat + (size_t)s_ba.perm[q0 + u] * 2 * L * N + (size_t)c * 4 * T;
+                bulk_g2s(dst + (3 + 2 * u) * CHUNK_BYTES, cq + (size_t)J * N, CHUNK_BYTES, full_b(sl));
+                bulk_g2s(dst + (4 + 2 * u) * CHUNK_BYTES, cq + ((size_t)L + J) * N, CHUNK_BYTES, full_b(sl));
+            }
+        };
+        // limb twiddle buffer use u of this item (limb J = L - 1 - u % L)
+        auto produce_tw = [&](uint32_t u) {
+            const uint32_t ts = tseq0 + u;
+            if (ts >= 1) mbar_wait(empty_tw, (ts - 1) & 1u);
+            const uint32_t J = L - 1 - u % L;
+            mbar_expect_tx(full_tw, LTW_BYTES);
+            bulk_g2s(ltw_s, reinterpret_cast<const uint4 *>(s_ba.tw_inv + (size_t)J * Gm::TW_LIMB) + 8 * T, LTW_BYTES,
+                     full_tw);
+        };
+        if (threadIdx.x == 0) {
+            produce_tw(0);
+            for (uint32_t j = 0; j + 1 < NSLOT && j < nchunks; j++) produce(j);
+        }
+        for (uint32_t r = 0; r < rounds; r++) {
+            const uint32_t qi = qb + 2 * r + grp;
+            const bool active = qi < qe;
+            const uint32_t qo = active ? s_ba.perm[qi] : 0;
+            uint32_t a[1][V];
+#pragma unroll 1
+            for (int Jr = 0; Jr < L; Jr++) {
+                const int J = L - 1 - Jr;
+                const uint32_t q = s_ba.kp.q[J], q2 = s_ba.kp.q2[J];
+                auto yo = [&](uint32_t X, uint32_t Y, uint2 w) { return shoup_mul(X - Y + q2, w.x, w.y, q); };
+                auto bf = [&](int i, int j, uint2 w) { gs_bfly(a[0][i], a[0][j], w.x, w.y, q, q2); };
+                const uint32_t u = r * L + Jr;                     // limb-buffer use within the item
+                mbar_wait(full_tw, (tseq0 + u) & 1u);
+                uint32_t l2 = 0, l3 = 0, l4 = 0, y = 0;
+#pragma unroll
+                for (int c = 0; c < CHUNKS; c++) {
+                    const uint32_t j = u * CHUNKS + c;             // stream element
+                    if (threadIdx.x == 0 && j + NSLOT - 1 < nchunks) produce(j + NSLOT - 1);
+                    const uint32_t sq = seq0 + j, sl = sq % NSLOT;
+                    mbar_wait(full_b(sl), (sq / NSLOT) & 1u);
+                    const uint4 *sp = reinterpret_cast<const uint4 *>(slots + sl * SLOT_BYTES);
+                    if (active) {
+                        const uint4 p = sp[g], pp = sp[T + g], w0 = sp[2 * T + g];
+                        const uint4 x0 = sp[(3 + 2 * grp) * T + g], x1 = sp[(4 + 2 * grp) * T + g];
+                        a[0][4 * c + 0] = shoup_mul(x1.x, p.x, pp.x, q);
+                        a[0][4 * c + 1] = shoup_mul(x1.y, p.y, pp.y, q);
+                        a[0][4 * c + 2] = shoup_mul(x1.z, p.z, pp.z, q);
+                        a[0][4 * c + 3] = shoup_mul(x1.w, p.w, pp.w, q);
+                        const uint32_t y0 = shoup_mul(x0.x, p.x, pp.x, q), y1 = shoup_mul(x0.y, p.y, pp.y, q);
+                        const uint32_t y2 = shoup_mul(x0.z, p.z, pp.z, q), y3 = shoup_mul(x0.w, p.w, pp.w, q);
+                        // pass-0 stages of this chunk: c1 in full, c0 the last Y output of each block
+                        const uint2 wa = make_uint2(w0.x, w0.y), wb = make_uint2(w0.z, w0.w);
+                        bf(4 * c, 4 * c + 1, wa);
+                        bf(4 * c + 2, 4 * c + 3, wb);
+                        const uint32_t u0 = yo(y0, y1, wa), u1 = yo(y2, y3, wb);
+                        const uint4 t1 = ltw[(c / 2) * T + g];                       // stage 1, block c
+                        const uint2 w1 = (c % 2 == 0) ? make_uint2(t1.x, t1.y) : make_uint2(t1.z, t1.w);
+                        bf(4 * c, 4 * c + 2, w1);
+                        bf(4 * c + 1, 4 * c + 3, w1);
+                        const uint32_t v = yo(u0, u1, w1);
+                        if (c % 2 == 0) {
+                            l2 = v;
+                        } else {
+                            const uint4 t2 = ltw[(4 + c / 4) * T + g];               // stage 2, block c / 2
+                            const uint2 w2 = ((c / 2) % 2 == 0) ? make_uint2(t2.x, t2.y) : make_uint2(t2.z, t2.w);
+#pragma unroll
+                            for (int kk = 0; kk < 4; kk++) bf(8 * (c / 2) + kk, 8 * (c / 2) + kk + 4, w2);
+                            const uint32_t v2 = yo(l2, v, w2);
+                            if ((c / 2) % 2 == 0) {
+                                l3 = v2;
+                            } else {
+                                const uint4 t3 = ltw[6 * T + g];                     // stage 3, block c / 4
+                                const uint2 w3 = (c / 4 == 0) ? make_uint2(t3.x, t3.y) : make_uint2(t3.z, t3.w);
+#pragma unroll
+                                for (int kk = 0; kk < 8; kk++) bf(16 * (c / 4) + kk, 16 * (c / 4) + kk + 8, w3);
+                                const uint32_t v3 = yo(l3, v2, w3);
+                                if (c / 4 == 0) {
+                                    l4 = v3;
+                                } else {
+                                    const uint4 t4 = ltw[7 * T + g];                 // stage 4
+                                    const uint2 w4 = make_uint2(t4.x, t4.y);
+#pragma unroll
+                                    for (int kk = 0; kk < 16; kk++) bf(kk, kk + 16, w4);
+                                    y = yo(l4, v3, w4);
+                                }
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive(empty_b(sl));
+                        if (c == CHUNKS - 1) mbar_arrive(empty_tw);
+                    }
+                }
+                // the next limb's twiddle blocks: after every warp is done with this limb's last chunk
+                if (threadIdx.x == 0 && u + 1 < rounds * L) produce_tw(u + 1);
+                if (!active) continue;
+                uint32_t *z = s_ybuf[grp] + par * T;
+                z[g] = c0_mid<N>(y, g, mu, s_mrg + J * 256, q, q2);
+                p8t_intt_tail(a, s_tw12 + (size_t)J * TW12, g, q, q2, xb, bar);
+                if (g < 32) {
+                    limb_dispatch<L>(J, [&](auto JC) {
+                        constexpr int JJ = decltype(JC)::value;
+                        if (mu == 9) c0_tail_fast8<L, JJ>(z, s_cst[grp], s_mrg + JJ * 256, g, s_ba.kp);
+                        else c0_tail<N, L, JJ>(z, s_cst[grp], s_mrg + JJ * 256, g, mu, s_ba.kp);
+                    });
+                }
+                par ^= 1u;
+                limb_dispatch<L>(J, [&](auto JC) { p8_ms_limb<L, decltype(JC)::value>(a, tcol, s_ba.kp); });
+            }
+            if (active) {
+                uint32_t *out_q = s_ba.resp + s_ba.resp_off[qo] + (size_t)k * s_ba.wpp;
+                if (g < 32) c0_write_results<N>(s_ba, out_q, s_ybuf[grp] + (par ^ 1u) * T, g, mu);
+                write_component<N, FMT>(s_ba, out_q, a[0], 1, g, s_rmap);
+            }
+        }
+        seq = seq0 + nchunks;
+        tseq = tseq0 + rounds * L;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_taddr) : "memory");
+}
+
+template <int L, int FMT>
+static cudaError_t launch_eval_p8t(const BatchArgs &a, cudaStream_t s, int num_sms) {
+    static DeviceOnce once;
+    const size_t smem = p8t::smem_bytes(L);
+    cudaError_t e = device_once(once, [&](int *) { return allow_smem(eval_kernel_p8t<L, FMT>, smem); });
+    if (e != cudaSuccess) return e;
+    eval_kernel_p8t<L, FMT><<<num_sms, 2 * NttGeom<8192>::T, smem, s>>>(a);   // one CTA (two groups) per SM
     return cudaGetLastError();
 }
 
@@ -1629,7 +1996,13 @@ static cudaError_t launch_eval_nl(const BatchArgs &a, cudaStream_t s, int num_sm
         eval_kernel_grp<N, L><<<num_sms * blocks_per_sm, kEvalGroups * Gm::T, smem, s>>>(a);
     } else {
         if constexpr (N == 8192 && WALLY_EVAL_TMEM) {
-            if (pruned_c0_path(N, L, a.d, a.compact)) return launch_eval_p8<L, (int)WALLY_RESP_COMPACT>(a, s, num_sms);
+#ifndef WALLY_P8_V
+#define WALLY_P8_V 5
+#endif
+            if (pruned_c0_path(N, L, a.d, a.compact)) {
+                if (WALLY_P8_V == 5) return launch_eval_p8t<L, (int)WALLY_RESP_COMPACT>(a, s, num_sms);
+                return launch_eval_p8<L, (int)WALLY_RESP_COMPACT>(a, s, num_sms);
+            }
         }
         const size_t smem = chain_smem<N>(EvalCfg<N>::NC);
         cudaError_t e = device_once(once, [&](int *v) {

@@ -146,6 +146,23 @@ struct NttGeom {
     static constexpr int TW_LIMB = N / TB0 + N / TB1 + N / TB2;
 };
 
+// Storage order of NTT-domain polynomials (query NTTs, the plaintext store).
+// Thread g of a transform holds the V consecutive (bit-reversed-order)
+// elements g V .. g V + V - 1 after the forward transform.  At n <= 4096 they
+// are stored in that order; at n = 8192 CHUNK-MAJOR: value 4 v + i of thread
+// g (its v-th 16-byte chunk) at word v (4 T) + 4 g + i, so the fused kernel's
+// per-chunk 16-byte loads of a warp cover 512 contiguous bytes, and chunk v of
+// all threads is one 4 KB block a bulk copy can stage.  The order is internal:
+// every producer and consumer goes through ntt_word.
+template <int N>
+struct NttStore { static constexpr bool CHUNK_MAJOR = (N == 8192); };
+
+template <int N>
+__host__ __device__ constexpr size_t ntt_word(int g, int v) {
+    return NttStore<N>::CHUNK_MAJOR ? (size_t)v * 4 * NttGeom<N>::T + 4 * (size_t)g
+                                    : (size_t)g * NttGeom<N>::V + 4 * (size_t)v;
+}
+
 template <int R>
 struct Log2 { static constexpr int v = (R <= 1) ? 0 : 1 + Log2<R / 2>::v; };
 template <>
