@@ -92,7 +92,10 @@ typedef struct wally_ctx wally_ctx;
  *                       The client decrypts with c1' ~ 64 h mod q_0; the dropped
  *                       part adds e_drop = -(c1' - 64 h) * s with |c1' - 64 h| <= 32,
  *                       which keeps ||e + e_drop|| < q_0 / 2t for q_0 ~ 2^30,
- *                       t <= 65537 at n = 4096. */
+ *                       t <= 65537 at n = 4096.
+ *                       wally_create accepts this format only when the paper's
+ *                       z = 8 rule holds for it: 8 sqrt(2n/9) 2^5 < q_0 / 2t
+ *                       (reading S20; WALLY_E_PARAMS otherwise). */
 #define WALLY_RESP_COMPACT_DROP 2u
 #define WALLY_RESP_DROP_BITS 6u
 

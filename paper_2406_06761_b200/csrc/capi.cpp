@@ -216,6 +216,17 @@ extern "C" int wally_create(const wally_params *pp, int device, wally_ctx **out)
     if (p.resp_format == WALLY_RESP_COMPACT_DROP && p.n != 4096)
         return fail(nullptr, WALLY_E_PARAMS,
                     "WALLY_RESP_COMPACT_DROP is specified for n = 4096 (its noise bound and plane order; DESIGN.md)");
+    if (p.resp_format == WALLY_RESP_COMPACT_DROP) {
+        // the paper's LSB-drop rule (z = 8; correctness ||e + e_drop|| < q_0 / 2t) for
+        // c1 rounded to 2^b (|c1^l| <= 2^(b-1)) and c0 not dropped: z sqrt(2n/9) 2^(b-1) < q_0 / (2t)
+        // (reading S20)
+        const double lhs = 8.0 * std::sqrt(2.0 * p.n / 9.0) * (double)(1u << (WALLY_RESP_DROP_BITS - 1));
+        const double rhs = (double)p.moduli[0] / (2.0 * (double)p.t);
+        if (!(lhs < rhs))
+            return fail(nullptr, WALLY_E_PARAMS,
+                        "WALLY_RESP_COMPACT_DROP: z sqrt(2n/9) 2^%u = %.1f is not below q_0/2t = %.1f (P:L1005, z = 8)",
+                        WALLY_RESP_DROP_BITS - 1, lhs, rhs);
+    }
     for (uint32_t i = 0; i < p.num_limbs; i++) {
         uint32_t q = p.moduli[i];
         if (q >= (1u << 30) || q % (2 * p.n) != 1 || !is_prime32(q))

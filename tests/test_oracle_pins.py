@@ -498,3 +498,104 @@ def test_server_pairs_batch_matches_single():
     assert used >= 1
     for k in range(pq.size):
         assert np.array_equal(out[k], capi.server_pair(qs, cts[pq[k]], pcs[pp[k]]))
+
+
+# --------------------------------------------------------------------------
+# o9 pinned: the noise budget (decryption is correct while the
+# noise stays below Q/2t) against ciphertexts with a KNOWN error, built with
+# the big-integer tiny_ref (no oracle encryption involved).  With message 0
+# the phase is exactly the error, so nu = t max|e| and the budget is
+# log2(Q) - 1 - log2(t max|e|); with error 0 and message m, [t Delta m]_Q =
+# -(Q mod t) m, so nu = (Q mod t) max m.  A dropped "-1", an uncentred lift
+# or a wrong CRT would move these by >= 1 bit or flip the sign.
+# --------------------------------------------------------------------------
+
+def _tiny_ct(moduli, t, msg, s, e, seed):
+    rng = np.random.default_rng(seed)
+    n = len(msg)
+    a_res = [[int(x) for x in rng.integers(0, q, size=n)] for q in moduli]
+    c0, c1 = tiny_ref.encrypt(moduli, t, msg, s, a_res, e)
+    return np.array([tiny_ref.to_residues(c0, moduli), tiny_ref.to_residues(c1, moduli)], dtype=np.uint32)
+
+
+@pytest.mark.parametrize("L", [1, 2, 3])
+def test_noise_budget_Q_known_error_and_message(L):
+    n, t = 16, 65537
+    qs = capi.find_primes(4096, L)
+    Q = tiny_ref.product(qs)
+    rng = np.random.default_rng(L)
+    s = rng.integers(-1, 2, size=n).astype(np.int8)
+    e = np.zeros(n, np.int64)
+    e[3], e[11] = 5, -9
+    ct = _tiny_ct(qs, t, [0] * n, s.tolist(), e.tolist(), 1)
+    want = math.log2(Q) - 1 - math.log2(9 * t)
+    assert abs(capi.noise_budget_Q(qs, t, ct, s) - want) < 1e-6
+    msg = [i % 21 for i in range(n)]                  # max m = 15 (n = 16)
+    ct = _tiny_ct(qs, t, msg, s.tolist(), [0] * n, 2)
+    want = math.log2(Q) - 1 - math.log2((Q % t) * max(msg))
+    assert abs(capi.noise_budget_Q(qs, t, ct, s) - want) < 1e-6
+
+
+def test_noise_budget_q0_known_error_message_and_correctness_threshold():
+    n, t = 16, 65537
+    q0 = capi.find_primes(4096, 2)[0]
+    rng = np.random.default_rng(9)
+    s = rng.integers(-1, 2, size=n).astype(np.int8)
+    e = np.zeros(n, np.int64)
+    e[0], e[7] = -2, 6
+    resp = _tiny_ct([q0], t, [0] * n, s.tolist(), e.tolist(), 3)[:, 0, :]
+    assert abs(capi.noise_budget_q0(q0, t, resp, s) - (math.log2(q0) - 1 - math.log2(6 * t))) < 1e-9
+    msg = [0] * n
+    msg[4] = 5
+    resp = _tiny_ct([q0], t, msg, s.tolist(), [0] * n, 4)[:, 0, :]
+    assert (q0 % t) * 5 < q0 // 2
+    assert abs(capi.noise_budget_q0(q0, t, resp, s) - (math.log2(q0) - 1 - math.log2((q0 % t) * 5))) < 1e-9
+    # the budget runs out at the paper's bound |e| < q0 / 2t (message 0): half-way there it is
+    # one bit, just inside it is ~0 and decryption is still exact, one step beyond it fails
+    emax = (q0 // 2) // t                              # t * emax < q0 / 2 <= t * (emax + 1)
+    for ev, want_b, ok in ((emax // 2, 1.0, True), (emax, 0.0, True), (emax + 1, 0.0, False)):
+        e = np.zeros(n, np.int64)
+        e[2] = ev
+        resp = _tiny_ct([q0], t, [0] * n, s.tolist(), e.tolist(), 5)[:, 0, :]
+        b = capi.noise_budget_q0(q0, t, resp, s)
+        dec = capi.decrypt_q0(q0, t, resp, s)
+        assert abs(b - want_b) < 1e-3 and (int(dec[2]) == 0) == ok and not dec[np.arange(n) != 2].any()
+
+
+# --------------------------------------------------------------------------
+# Reading S20 pinned to the paper's LSB-drop rule (z sqrt(2n/9)
+# 2^l1 + 2^l0 < q_l/t, z = 8; correctness ||e + e_drop|| < Q'/2t).
+# WALLY_RESP_COMPACT_DROP rounds c1 to 2^6 (|c1^l| <= 2^5, i.e. the
+# truncation formula's 2^l1 with l1 = b - 1) and keeps c0 whole (c0^l = 0):
+# the rule is z sqrt(2n/9) 2^5 < q_0 / 2t.  Every config it is used on must
+# satisfy it, and the library must reject exactly the parameters that do not.
+# --------------------------------------------------------------------------
+
+def _drop_rule(n, q0, t, b=6, z=8.0):
+    return z * math.sqrt(2 * n / 9) * 2 ** (b - 1) < q0 / (2 * t)
+
+
+def test_compact_drop_rule_holds_for_the_configs_and_is_enforced():
+    for name in ("c1", "c2", "c3", "c5"):
+        w = synth.WORKLOADS[name]
+        q0 = capi.find_primes(w.n, w.num_limbs)[0]
+        assert w.n == 4096 and _drop_rule(w.n, q0, w.t)
+        assert not _drop_rule(w.n, q0, w.t, b=7)         # 6 is the largest b the rule allows
+        # the paper's own floor formula with its 2-bit headroom gives l1 = 4 (truncated),
+        # i.e. 5 rounded bits; the S20 reading spends that headroom because c0 is not dropped
+        l1 = math.floor(math.log2(q0 / w.t) - 2 - math.log2(8 * math.sqrt(2 * w.n / 9)))
+        assert l1 == 4
+    import ctypes
+    from paper_2406_06761_b200 import build
+    build.build()
+    from paper_2406_06761_b200 import wally as W
+    qs = W.wally_find_moduli(4096, 3)
+    for t in (2, 40961, 65537, 68000, 70001, 131073):
+        p = W.wally_params(n=4096, num_limbs=3, t=t, d=192, resp_format=W.WALLY_RESP_COMPACT_DROP)
+        for i, q in enumerate(qs):
+            p.moduli[i] = q
+        h = ctypes.c_void_p()
+        rc = W.lib.wally_create(ctypes.byref(p), 0, ctypes.byref(h))
+        if rc == 0:
+            W.lib.wally_destroy(h)
+        assert (rc != -2) == _drop_rule(4096, qs[0], t), (t, rc)
