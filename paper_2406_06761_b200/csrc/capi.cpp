@@ -552,6 +552,7 @@ static int eval_impl(wally_ctx *c, uint32_t nq, const uint32_t *ids, const uint3
     // a small batch would leave most thread groups idle with 8 queries per
     // work item (c1: 32 items for 296 groups): one query per item instead
     a.chunk = (nq < 4u * (uint32_t)c->num_sms) ? 1u : kQueryChunk;
+    a.ppi = eval_plaintexts_per_item(a.n, a.L, a.d, a.compact);
     a.n_local = c->n_local;
     a.total_clusters = c->total_clusters;
     a.tw_fwd = c->d_tw_fwd;

@@ -156,9 +156,10 @@ __global__ void batch_count_kernel(const uint32_t *__restrict__ ids, uint32_t nq
 }
 
 // One CTA of 1024 threads: exclusive scans of query counts (segment starts)
-// and of work items  P_c * ceil(count_c / chunk)  (item starts).
+// and of work items  ceil(P_c / ppi) * ceil(count_c / chunk)  (item starts;
+// ppi = plaintexts per work item: 1, or 2 for the n = 8192 kernel v5).
 __device__ __forceinline__ void batch_scan_block(const uint32_t *__restrict__ counts, uint32_t n_local,
-                                                 const uint32_t *__restrict__ n_pt, uint32_t chunk,
+                                                 const uint32_t *__restrict__ n_pt, uint32_t chunk, uint32_t ppi,
                                                  uint32_t *__restrict__ seg, uint32_t *__restrict__ item_start,
                                                  uint32_t *__restrict__ misc) {
     __shared__ uint32_t wsum_q[32], wsum_i[32];
@@ -168,7 +169,7 @@ __device__ __forceinline__ void batch_scan_block(const uint32_t *__restrict__ co
     for (uint32_t i = b; i < e; i++) {
         uint32_t c = counts[i];
         sq += c;
-        si += n_pt[i] * ((c + chunk - 1) / chunk);
+        si += ((n_pt[i] + ppi - 1) / ppi) * ((c + chunk - 1) / chunk);
     }
     // block exclusive scan of (sq, si)
     uint32_t iq = sq, ii = si;
@@ -197,7 +198,7 @@ __device__ __forceinline__ void batch_scan_block(const uint32_t *__restrict__ co
         seg[i] = oq;
         item_start[i] = oi;
         oq += c;
-        oi += n_pt[i] * ((c + chunk - 1) / chunk);
+        oi += ((n_pt[i] + ppi - 1) / ppi) * ((c + chunk - 1) / chunk);
     }
     if (tid == 1023) {
         item_start[n_local] = oi;
@@ -206,10 +207,10 @@ __device__ __forceinline__ void batch_scan_block(const uint32_t *__restrict__ co
 }
 
 __global__ void __launch_bounds__(1024) batch_scan_kernel(const uint32_t *__restrict__ counts, uint32_t n_local,
-                                                          const uint32_t *__restrict__ n_pt, uint32_t chunk,
+                                                          const uint32_t *__restrict__ n_pt, uint32_t chunk, uint32_t ppi,
                                                           uint32_t *__restrict__ seg, uint32_t *__restrict__ item_start,
                                                           uint32_t *__restrict__ misc) {
-    batch_scan_block(counts, n_local, n_pt, chunk, seg, item_start, misc);
+    batch_scan_block(counts, n_local, n_pt, chunk, ppi, seg, item_start, misc);
 }
 
 // The whole batcher in one CTA for small batches (one launch instead of
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(1024) batch_small_kernel(const uint32_t *__res
                                                            const int32_t *__restrict__ local_of_cluster,
                                                            uint32_t total_clusters, uint32_t *__restrict__ counts,
                                                            uint32_t n_local, const uint32_t *__restrict__ n_pt,
-                                                           uint32_t chunk, uint32_t *__restrict__ seg,
+                                                           uint32_t chunk, uint32_t ppi, uint32_t *__restrict__ seg,
                                                            uint32_t *__restrict__ item_start, uint32_t *__restrict__ misc,
                                                            uint32_t *__restrict__ fill, uint32_t *__restrict__ perm) {
     for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(1024) batch_small_kernel(const uint32_t *__res
         if (li >= 0) atomicAdd(&counts[li], 1u);
     }
     __syncthreads();
-    batch_scan_block(counts, n_local, n_pt, chunk, seg, item_start, misc);
+    batch_scan_block(counts, n_local, n_pt, chunk, ppi, seg, item_start, misc);
     __syncthreads();
     for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
         const uint32_t c = ids[q];
@@ -1599,36 +1600,40 @@ static cudaError_t launch_eval_p8(const BatchArgs &a, cudaStream_t s, int num_sm
 // asynchronous copies (cp.async.bulk + mbarrier, "TMA or cp.async staging of
 // the NTT-domain plaintexts", north_star) instead of register prefetch.
 //
-// One CTA of two 256-thread groups per SM; the groups evaluate two queries
-// of the same work item in step (group 0 the even, group 1 the odd queries of
-// the chunk of queries), so every staged plaintext chunk and twiddle block
-// serves both.  The operands of one (query pair, limb) stream through a ring
-// of NSLOT shared-memory slots, one per 4-value chunk c of every thread
-// (chunk-major NTT-domain storage, ntt_store: chunk c of all threads is one
-// 4 KB block):
-//   [p chunk][p' chunk][pass-0 stage-0 twiddle block c][c0, c1 chunk of
-//   group 0's query][c0, c1 chunk of group 1's query]      (28 KB per slot)
-// A producer thread (thread 0) keeps the ring NSLOT - 1 chunks ahead; a
-// full barrier per slot carries the transaction bytes, an empty barrier per
-// slot collects one arrival per warp.  The limb's other pass-0 twiddle blocks
-// (stages 1-4: 32 KB) go to a limb buffer refilled after every warp is done
-// with the limb's last chunk; the pass-1/2 tables of all limbs stay resident.
+// One CTA of two 256-thread groups per SM.  A work item is (cluster, two
+// consecutive plaintexts k0, k0 + 1, a chunk of queries); the groups take one
+// plaintext each and walk the same queries in step, so each staged query
+// chunk and twiddle block serves both (P_c is even at c4: no idle group).
+// The operands of one (query, limb) stream through a ring of NSLOT shared-
+// memory slots, one per 4-value chunk c of every thread (chunk-major
+// NTT-domain storage, ntt_word: chunk c of all threads is one 4 KB block):
+//   [p, p' of k0][p, p' of k1][pass-0 stage-0 twiddle block c]
+//   [pass-0 twiddle block B(c)][c0 chunk][c1 chunk]          (32 KB per slot)
+// B(c) = 8, 12, 9, 14, 10, 13, 11, 15 delivers each later-stage twiddle block
+// with the first chunk that needs it (a thread keeps the half it needs again
+// in a register).  A producer thread (thread 0) keeps the ring NSLOT - 1
+// chunks ahead across limbs and queries; a full barrier per slot carries the
+// transaction bytes, an empty barrier per slot collects one arrival per warp.
 // c1's pass 0 runs inside the chunk loop as a tree over the chunks sharing
 // the twiddle reads of c0's Y-only tree; passes 1 and 2 through the group's
-// exchange buffer; c0's shuffle stages and warp-0 tail as in v3; c1's
-// switch state in tensor memory.  No register holds a prefetched operand.
+// exchange buffer (their tables resident in shared memory); c0's shuffle
+// stages and warp-0 tail as in v3; c1's switch state in tensor memory.  No
+// register holds a prefetched operand.
 // ---------------------------------------------------------------------------
 namespace p8t {
 constexpr int N = 8192;
 constexpr int T = NttGeom<N>::T;                 // 256 threads per group
-constexpr int NSLOT = 3;
+constexpr int NSLOT = 4;
 constexpr int CHUNK_BYTES = T * 16;              // one 16-byte chunk of every thread: 4 KB
-constexpr int SLOT_BYTES = 7 * CHUNK_BYTES;      // p, p', stage-0 twiddles, 2 x (c0, c1)
-constexpr int LTW_BYTES = 8 * CHUNK_BYTES;       // pass-0 twiddle blocks 8..15 (stages 1-4)
+constexpr int SLOT_BYTES = 8 * CHUNK_BYTES;      // 2 x (p, p'), 2 twiddle blocks, c0, c1
 constexpr int TW12 = NttGeom<N>::TW_LIMB - NttGeom<N>::TW1;   // pass-1/2 table entries per limb
 constexpr int XB_WORDS = NttGeom<N>::SMEM_WORDS;
 __host__ __device__ constexpr size_t smem_bytes(int L) {
-    return (size_t)NSLOT * SLOT_BYTES + LTW_BYTES + (size_t)L * TW12 * 8 + 2ull * XB_WORDS * 4;
+    return (size_t)NSLOT * SLOT_BYTES + (size_t)L * TW12 * 8 + 2ull * XB_WORDS * 4;
+}
+// pass-0 twiddle block (uint4 index / T) delivered with chunk c besides block c
+__host__ __device__ constexpr int aux_block(int c) {
+    return c == 0 ? 8 : c == 1 ? 12 : c == 2 ? 9 : c == 3 ? 14 : c == 4 ? 10 : c == 5 ? 13 : c == 6 ? 11 : 15;
 }
 }  // namespace p8t
 
@@ -1737,9 +1742,8 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
     constexpr int CHUNKS = V / 4;                 // 8 chunks of 4 values per thread and limb
     extern __shared__ __align__(128) uint8_t smem8[];
     uint8_t *slots = smem8;
-    const uint4 *ltw = reinterpret_cast<const uint4 *>(smem8 + NSLOT * SLOT_BYTES);
-    uint2 *s_tw12 = reinterpret_cast<uint2 *>(smem8 + NSLOT * SLOT_BYTES + LTW_BYTES);
-    uint32_t *xbuf = reinterpret_cast<uint32_t *>(smem8 + NSLOT * SLOT_BYTES + LTW_BYTES + (size_t)L * TW12 * 8);
+    uint2 *s_tw12 = reinterpret_cast<uint2 *>(smem8 + NSLOT * SLOT_BYTES);
+    uint32_t *xbuf = reinterpret_cast<uint32_t *>(smem8 + NSLOT * SLOT_BYTES + (size_t)L * TW12 * 8);
     __shared__ BatchArgs s_ba;
     __shared__ uint32_t s_taddr;
     __shared__ uint32_t s_item[2];
@@ -1747,21 +1751,18 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
     __shared__ uint32_t s_ybuf[2][2 * T];
     __shared__ uint32_t s_cst[2][(N / 32) * (1 + NA)];
     __shared__ uint2 s_mrg[L * 256];
-    __shared__ __align__(8) uint64_t s_bar[2 * NSLOT + 2];   // full[NSLOT], empty[NSLOT], full_tw, empty_tw
+    __shared__ __align__(8) uint64_t s_bar[2 * NSLOT];   // full[NSLOT], empty[NSLOT]
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int grp = threadIdx.x / T, g = threadIdx.x % T;
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(s_bar);
-    auto full_b = [&](int i) { return bar0 + 8u * i; };
-    auto empty_b = [&](int i) { return bar0 + 8u * (NSLOT + i); };
-    const uint32_t full_tw = bar0 + 8u * (2 * NSLOT), empty_tw = bar0 + 8u * (2 * NSLOT + 1);
+    auto full_b = [&](uint32_t i) { return bar0 + 8u * i; };
+    auto empty_b = [&](uint32_t i) { return bar0 + 8u * (NSLOT + i); };
     if (threadIdx.x == 0) {
         s_ba = ba;
         for (int i = 0; i < NSLOT; i++) {
             mbar_init(full_b(i), 1);
             mbar_init(empty_b(i), 2 * T / 32);
         }
-        mbar_init(full_tw, 1);
-        mbar_init(empty_tw, 2 * T / 32);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {   // 512 columns: four warps share a lane quadrant, 128 columns each
@@ -1782,9 +1783,7 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
     const int mu = min(__ffs((int)ba.d) - 1, 13);
     const uint32_t total = ba.misc[kMiscTotalItems];
     const uint32_t slots_s = (uint32_t)__cvta_generic_to_shared(slots);
-    const uint32_t ltw_s = (uint32_t)__cvta_generic_to_shared(ltw);
     uint32_t seq = 0;      // chunk slots consumed by this CTA so far (ring position and phases)
-    uint32_t tseq = 0;     // limb twiddle buffers consumed so far
     uint32_t par = 0;
     ItemCursor cur;
     for (uint32_t it = 0;; it++) {
@@ -1795,50 +1794,39 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
         cur.seek(s_ba, item);
         const uint32_t li = cur.li;
         const uint32_t cnt = s_ba.counts[li];
-        const uint32_t P = s_ba.n_pt[li];
-        const uint32_t ch = (item - cur.b) / P, k = (item - cur.b) % P;
+        const uint32_t P = s_ba.n_pt[li], PP = (P + 1) / 2;
+        const uint32_t ch = (item - cur.b) / PP, k0 = 2 * ((item - cur.b) % PP);
+        const uint32_t np = min(2u, P - k0);                    // plaintexts of this item (1 only for odd P_c)
+        const uint32_t k = k0 + grp;
+        const bool active = (uint32_t)grp < np;
         const uint32_t qb = s_ba.seg[li] + ch * s_ba.chunk;
         const uint32_t qe = min(qb + s_ba.chunk, s_ba.seg[li] + cnt);
-        const uint32_t *phat = s_ba.store + (size_t)(s_ba.pt_base[li] + k) * L * 2 * N;
-        const uint32_t rounds = (qe - qb + 1) / 2;
-        const uint32_t nchunks = rounds * L * CHUNKS;    // the item's chunk stream: round, limb L-1..0, chunk
-        const uint32_t seq0 = seq, tseq0 = tseq;
+        const uint32_t *phat0 = s_ba.store + (size_t)(s_ba.pt_base[li] + k0) * L * 2 * N;
+        const uint32_t nchunks = (qe - qb) * L * CHUNKS;         // the item's chunk stream: query, limb L-1..0, chunk
+        const uint32_t seq0 = seq;
         // producer: stream element j -> slot (seq0 + j) % NSLOT
         auto produce = [&](uint32_t j) {
             const uint32_t sq = seq0 + j, sl = sq % NSLOT;
             if (sq >= NSLOT) mbar_wait(empty_b(sl), ((sq / NSLOT) + 1) & 1u);   // consumers of sq - NSLOT done
             const uint32_t r = j / (L * CHUNKS), J = L - 1 - (j / CHUNKS) % L, c = j % CHUNKS;
-            const uint32_t q0 = qb + 2 * r, nq = min(2u, qe - q0);
-            mbar_expect_tx(full_b(sl), (3 + 2 * nq) * CHUNK_BYTES);
+            mbar_expect_tx(full_b(sl), (4 + 2 * np) * CHUNK_BYTES);
             const uint32_t dst = slots_s + sl * SLOT_BYTES;
-            const uint32_t *pj = phat + (size_t)J * 2 * N + (size_t)c * 4 * T;
-            bulk_g2s(dst, pj, CHUNK_BYTES, full_b(sl));
-            bulk_g2s(dst + CHUNK_BYTES, pj + N, CHUNK_BYTES, full_b(sl));
-            bulk_g2s(dst + 2 * CHUNK_BYTES, reinterpret_cast<const uint4 *>(s_ba.tw_inv + (size_t)J * Gm::TW_LIMB) + c * T,
-                     CHUNK_BYTES, full_b(sl));
-            for (uint32_t u = 0; u < nq; u++) {
-                const uint32_t *cq = s_ba.chat + (size_t)s_ba.perm[q0 + u] * 2 * L * N + (size_t)c * 4 * T;
-                bulk_g2s(dst + (3 + 2 * u) * CHUNK_BYTES, cq + (size_t)J * N, CHUNK_BYTES, full_b(sl));
-                bulk_g2s(dst + (4 + 2 * u) * CHUNK_BYTES, cq + ((size_t)L + J) * N, CHUNK_BYTES, full_b(sl));
+            for (uint32_t u = 0; u < np; u++) {
+                const uint32_t *pj = phat0 + ((size_t)u * L + J) * 2 * N + (size_t)c * 4 * T;
+                bulk_g2s(dst + (2 * u) * CHUNK_BYTES, pj, CHUNK_BYTES, full_b(sl));
+                bulk_g2s(dst + (2 * u + 1) * CHUNK_BYTES, pj + N, CHUNK_BYTES, full_b(sl));
             }
+            const uint4 *twJ = reinterpret_cast<const uint4 *>(s_ba.tw_inv + (size_t)J * Gm::TW_LIMB);
+            bulk_g2s(dst + 4 * CHUNK_BYTES, twJ + c * T, CHUNK_BYTES, full_b(sl));
+            bulk_g2s(dst + 5 * CHUNK_BYTES, twJ + aux_block(c) * T, CHUNK_BYTES, full_b(sl));
+            const uint32_t *cq = s_ba.chat + (size_t)s_ba.perm[qb + r] * 2 * L * N + (size_t)c * 4 * T;
+            bulk_g2s(dst + 6 * CHUNK_BYTES, cq + (size_t)J * N, CHUNK_BYTES, full_b(sl));
+            bulk_g2s(dst + 7 * CHUNK_BYTES, cq + ((size_t)L + J) * N, CHUNK_BYTES, full_b(sl));
         };
-        // limb twiddle buffer use u of this item (limb J = L - 1 - u % L)
-        auto produce_tw = [&](uint32_t u) {
-            const uint32_t ts = tseq0 + u;
-            if (ts >= 1) mbar_wait(empty_tw, (ts - 1) & 1u);
-            const uint32_t J = L - 1 - u % L;
-            mbar_expect_tx(full_tw, LTW_BYTES);
-            bulk_g2s(ltw_s, reinterpret_cast<const uint4 *>(s_ba.tw_inv + (size_t)J * Gm::TW_LIMB) + 8 * T, LTW_BYTES,
-                     full_tw);
-        };
-        if (threadIdx.x == 0) {
-            produce_tw(0);
+        if (threadIdx.x == 0)
             for (uint32_t j = 0; j + 1 < NSLOT && j < nchunks; j++) produce(j);
-        }
-        for (uint32_t r = 0; r < rounds; r++) {
-            const uint32_t qi = qb + 2 * r + grp;
-            const bool active = qi < qe;
-            const uint32_t qo = active ? s_ba.perm[qi] : 0;
+        for (uint32_t r = 0; qb + r < qe; r++) {
+            const uint32_t qo = s_ba.perm[qb + r];
             uint32_t a[1][V];
 #pragma unroll 1
             for (int Jr = 0; Jr < L; Jr++) {
@@ -1846,19 +1834,19 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
                 const uint32_t q = s_ba.kp.q[J], q2 = s_ba.kp.q2[J];
                 auto yo = [&](uint32_t X, uint32_t Y, uint2 w) { return shoup_mul(X - Y + q2, w.x, w.y, q); };
                 auto bf = [&](int i, int j, uint2 w) { gs_bfly(a[0][i], a[0][j], w.x, w.y, q, q2); };
-                const uint32_t u = r * L + Jr;                     // limb-buffer use within the item
-                mbar_wait(full_tw, (tseq0 + u) & 1u);
                 uint32_t l2 = 0, l3 = 0, l4 = 0, y = 0;
+                uint2 k1 = make_uint2(0, 0), k2 = make_uint2(0, 0), k3 = make_uint2(0, 0);  // twiddle halves kept
 #pragma unroll
                 for (int c = 0; c < CHUNKS; c++) {
-                    const uint32_t j = u * CHUNKS + c;             // stream element
+                    const uint32_t j = (r * L + Jr) * CHUNKS + c;   // stream element
                     if (threadIdx.x == 0 && j + NSLOT - 1 < nchunks) produce(j + NSLOT - 1);
                     const uint32_t sq = seq0 + j, sl = sq % NSLOT;
                     mbar_wait(full_b(sl), (sq / NSLOT) & 1u);
                     const uint4 *sp = reinterpret_cast<const uint4 *>(slots + sl * SLOT_BYTES);
                     if (active) {
-                        const uint4 p = sp[g], pp = sp[T + g], w0 = sp[2 * T + g];
-                        const uint4 x0 = sp[(3 + 2 * grp) * T + g], x1 = sp[(4 + 2 * grp) * T + g];
+                        const uint4 p = sp[2 * grp * T + g], pp = sp[(2 * grp + 1) * T + g];
+                        const uint4 w0 = sp[4 * T + g], ta = sp[5 * T + g];
+                        const uint4 x0 = sp[6 * T + g], x1 = sp[7 * T + g];
                         a[0][4 * c + 0] = shoup_mul(x1.x, p.x, pp.x, q);
                         a[0][4 * c + 1] = shoup_mul(x1.y, p.y, pp.y, q);
                         a[0][4 * c + 2] = shoup_mul(x1.z, p.z, pp.z, q);
@@ -1870,32 +1858,50 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
                         bf(4 * c, 4 * c + 1, wa);
                         bf(4 * c + 2, 4 * c + 3, wb);
                         const uint32_t u0 = yo(y0, y1, wa), u1 = yo(y2, y3, wb);
-                        const uint4 t1 = ltw[(c / 2) * T + g];                       // stage 1, block c
-                        const uint2 w1 = (c % 2 == 0) ? make_uint2(t1.x, t1.y) : make_uint2(t1.z, t1.w);
+                        // stage 1, block c (twiddle slot 16 + c = block 8 + c/2, delivered with chunk c & ~1)
+                        uint2 w1;
+                        if (c % 2 == 0) {
+                            w1 = make_uint2(ta.x, ta.y);
+                            k1 = make_uint2(ta.z, ta.w);
+                        } else {
+                            w1 = k1;
+                        }
                         bf(4 * c, 4 * c + 2, w1);
                         bf(4 * c + 1, 4 * c + 3, w1);
                         const uint32_t v = yo(u0, u1, w1);
                         if (c % 2 == 0) {
                             l2 = v;
                         } else {
-                            const uint4 t2 = ltw[(4 + c / 4) * T + g];               // stage 2, block c / 2
-                            const uint2 w2 = ((c / 2) % 2 == 0) ? make_uint2(t2.x, t2.y) : make_uint2(t2.z, t2.w);
+                            // stage 2, block c / 2 (block 12 + c/4, delivered with chunks 1 and 5)
+                            uint2 w2;
+                            if ((c / 2) % 2 == 0) {
+                                w2 = make_uint2(ta.x, ta.y);
+                                k2 = make_uint2(ta.z, ta.w);
+                            } else {
+                                w2 = k2;
+                            }
 #pragma unroll
                             for (int kk = 0; kk < 4; kk++) bf(8 * (c / 2) + kk, 8 * (c / 2) + kk + 4, w2);
                             const uint32_t v2 = yo(l2, v, w2);
                             if ((c / 2) % 2 == 0) {
                                 l3 = v2;
                             } else {
-                                const uint4 t3 = ltw[6 * T + g];                     // stage 3, block c / 4
-                                const uint2 w3 = (c / 4 == 0) ? make_uint2(t3.x, t3.y) : make_uint2(t3.z, t3.w);
+                                // stage 3, block c / 4 (block 14, delivered with chunk 3)
+                                uint2 w3;
+                                if (c / 4 == 0) {
+                                    w3 = make_uint2(ta.x, ta.y);
+                                    k3 = make_uint2(ta.z, ta.w);
+                                } else {
+                                    w3 = k3;
+                                }
 #pragma unroll
                                 for (int kk = 0; kk < 8; kk++) bf(16 * (c / 4) + kk, 16 * (c / 4) + kk + 8, w3);
                                 const uint32_t v3 = yo(l3, v2, w3);
                                 if (c / 4 == 0) {
                                     l4 = v3;
                                 } else {
-                                    const uint4 t4 = ltw[7 * T + g];                 // stage 4
-                                    const uint2 w4 = make_uint2(t4.x, t4.y);
+                                    // stage 4 (block 15, delivered with chunk 7)
+                                    const uint2 w4 = make_uint2(ta.x, ta.y);
 #pragma unroll
                                     for (int kk = 0; kk < 16; kk++) bf(kk, kk + 16, w4);
                                     y = yo(l4, v3, w4);
@@ -1904,13 +1910,8 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
                         }
                     }
                     __syncwarp();
-                    if (lane == 0) {
-                        mbar_arrive(empty_b(sl));
-                        if (c == CHUNKS - 1) mbar_arrive(empty_tw);
-                    }
+                    if (lane == 0) mbar_arrive(empty_b(sl));
                 }
-                // the next limb's twiddle blocks: after every warp is done with this limb's last chunk
-                if (threadIdx.x == 0 && u + 1 < rounds * L) produce_tw(u + 1);
                 if (!active) continue;
                 uint32_t *z = s_ybuf[grp] + par * T;
                 z[g] = c0_mid<N>(y, g, mu, s_mrg + J * 256, q, q2);
@@ -1932,7 +1933,6 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
             }
         }
         seq = seq0 + nchunks;
-        tseq = tseq0 + rounds * L;
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -1996,9 +1996,6 @@ static cudaError_t launch_eval_nl(const BatchArgs &a, cudaStream_t s, int num_sm
         eval_kernel_grp<N, L><<<num_sms * blocks_per_sm, kEvalGroups * Gm::T, smem, s>>>(a);
     } else {
         if constexpr (N == 8192 && WALLY_EVAL_TMEM) {
-#ifndef WALLY_P8_V
-#define WALLY_P8_V 5
-#endif
             if (pruned_c0_path(N, L, a.d, a.compact)) {
                 if (WALLY_P8_V == 5) return launch_eval_p8t<L, (int)WALLY_RESP_COMPACT>(a, s, num_sms);
                 return launch_eval_p8<L, (int)WALLY_RESP_COMPACT>(a, s, num_sms);
@@ -2060,14 +2057,14 @@ cudaError_t launch_batcher(const BatchArgs &a, cudaStream_t s, uint64_t *launche
     if (a.nq == 0) return cudaSuccess;
     if (a.nq <= 4096) {
         batch_small_kernel<<<1, 1024, 0, s>>>(a.ids, a.nq, a.local_of_cluster, a.total_clusters, a.counts, a.n_local,
-                                              a.n_pt, a.chunk, a.seg, a.item_start, a.misc, a.fill, a.perm);
+                                              a.n_pt, a.chunk, a.ppi, a.seg, a.item_start, a.misc, a.fill, a.perm);
         *launches += 1;
         return cudaGetLastError();
     }
     const unsigned threads = 256;
     const unsigned blocks = (a.nq + threads - 1) / threads;
     batch_count_kernel<<<blocks, threads, 0, s>>>(a.ids, a.nq, a.local_of_cluster, a.total_clusters, a.counts);
-    batch_scan_kernel<<<1, 1024, 0, s>>>(a.counts, a.n_local, a.n_pt, a.chunk, a.seg, a.item_start, a.misc);
+    batch_scan_kernel<<<1, 1024, 0, s>>>(a.counts, a.n_local, a.n_pt, a.chunk, a.ppi, a.seg, a.item_start, a.misc);
     batch_scatter_kernel<<<blocks, threads, 0, s>>>(a.ids, a.nq, a.local_of_cluster, a.total_clusters, a.seg, a.fill,
                                                     a.perm);
     *launches += 3;

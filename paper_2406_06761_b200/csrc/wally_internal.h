@@ -56,6 +56,7 @@ struct BatchArgs {
     uint32_t drop;                // WALLY_RESP_COMPACT_DROP (c1 rounded to 2^6, 24-bit planes)
     uint32_t nq;
     uint32_t chunk;               // queries per work item (kQueryChunk, or 1 for small batches)
+    uint32_t ppi;                 // plaintexts per work item (eval_plaintexts_per_item)
     uint32_t n_local;
     uint32_t total_clusters;
     const uint2 *tw_fwd;          // [L][n] (w, w') psi^{brev(i)}
@@ -102,6 +103,21 @@ inline bool pruned_c0_path(uint32_t n, uint32_t L, uint32_t d, bool compact) {
     if (n == 4096) return L >= 2 && L <= 3 && (d & 15u) == 0;   // v6 (two groups, TMEM)
     if (n == 8192) return (d & 31u) == 0;                      // whole-CTA kernel (c4)
     return false;
+}
+
+// The n = 8192 pruned-c0 fused kernel: v3 (register prefetch, two CTAs per
+// SM) or v5 (bulk-copy staging, two groups per CTA on two plaintexts of one
+// work item; kernels.cu).
+#ifndef WALLY_P8_V
+#define WALLY_P8_V 5
+#endif
+
+// Plaintexts per work item of the fused kernel a batch runs: 2 for the v5
+// n = 8192 kernel (its two thread groups take plaintexts k and k + 1 of the
+// item's cluster for the same queries), 1 otherwise.  Shared by the batcher
+// (item count) and the kernel (item decode).
+inline uint32_t eval_plaintexts_per_item(uint32_t n, uint32_t L, uint32_t d, bool compact) {
+    return (n == 8192 && WALLY_P8_V == 5 && pruned_c0_path(n, L, d, compact)) ? 2u : 1u;
 }
 
 // Algorithmic modular multiplications per (query, plaintext) pair of the

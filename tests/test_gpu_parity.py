@@ -220,73 +220,7 @@ def test_host_buffer_path_matches_device_path():
     srv.close()
 
 
-# --------------------------------------------------------------------------
-# Full BASELINE configs, in the bench's launch configuration, sampled pairs
-# --------------------------------------------------------------------------
-
-def _sampled_full_config(name, n_pairs=384, real_queries=4, fmt=0):
-    w = synth.WORKLOADS[name]
-    ents = synth.cluster_entries(w)
-    ids = synth.query_clusters(w)
-    srv = H.make_server(w, ents, resp_format=fmt)
-    qs = srv.moduli
-    cts_dev = synth.uniform_ciphertexts_torch(w, qs)
-    # a few real encryptions (decrypt check) replace uniform stand-ins
-    qv = synth.query_vectors(w, ids)
-    real = np.linspace(0, w.num_queries - 1, real_queries).astype(np.int64)
-    rcts, keys = H.encrypt_queries(w, qs, qv[real], index_base=0)
-    cts_dev[torch.from_numpy(real).cuda()] = torch.from_numpy(rcts.view(np.int32)).cuda()
-    off = srv.response_layout(ids)
-    resp = torch.empty(int(off[-1]), dtype=torch.int32, device="cuda")
-    ws = srv.alloc_workspace(w.num_queries)
-    srv.eval_batch(ids, cts_dev, resp, ws)
-    srv.check_batch(ws)
-    rng = np.random.default_rng(99)
-    E = w.n // w.d
-    P = -(-w.cluster_size // E)
-    qsel = np.concatenate([real, rng.integers(0, w.num_queries, size=n_pairs // 2)])
-    pq = np.repeat(qsel, 2)
-    pp = np.empty_like(pq)
-    pp[0::2] = 0
-    pp[1::2] = P - 1                      # first and last (partial) plaintext
-    extra_q = rng.integers(0, w.num_queries, size=n_pairs // 4)
-    pq = np.concatenate([pq, extra_q])
-    pp = np.concatenate([pp, rng.integers(0, P, size=extra_q.size)])
-    uq, inv = np.unique(pq, return_inverse=True)
-    cts_h = cts_dev[torch.from_numpy(uq).cuda()].cpu().numpy().view(np.uint32)
-    # plaintext coefficients of every (cluster, k) needed
-    need = sorted(set((int(ids[q]), int(k)) for q, k in zip(pq, pp)))
-    pidx = {ck: i for i, ck in enumerate(need)}
-    pcs = np.stack([capi.encode_plaintext(ents[c][k * E:(k + 1) * E], w.d, w.n) for c, k in need])
-    want = H.oracle_pairs(qs, cts_h, pcs, inv, [pidx[(int(ids[q]), int(k))] for q, k in zip(pq, pp)])
-    # only the sampled responses are copied back
-    wpp = H.words_per_pt(w.n, w.d, fmt)
-    for i, (q, k) in enumerate(zip(pq, pp)):
-        b = int(off[q]) + int(k) * wpp
-        got = resp[b:b + wpp].cpu().numpy().view(np.uint32)
-        if fmt == 0:
-            got = got.reshape(2, w.n)
-        assert H.matches_oracle(got, want[i], w.n, w.d, fmt), (name, q, k)
-    for i, q in enumerate(real):
-        c = int(ids[q])
-        for k in (0, P - 1):
-            b = int(off[q]) + k * wpp
-            got = resp[b:b + wpp].cpu().numpy().view(np.uint32)
-            if fmt:
-                got = H.expand_compact(got, w.n, w.d, fmt, qs[0])
-            dec = capi.decrypt_q0(qs[0], w.t, got, keys[i].s)
-            cnt = min(E, w.cluster_size - k * E)
-            for j in range(cnt):
-                assert int(dec[j * w.d + w.d - 1]) == int(np.dot(qv[q].astype(np.int64),
-                                                                 ents[c][k * E + j].astype(np.int64))) % w.t
-    srv.close()
-    del resp, ws, cts_dev
-    torch.cuda.empty_cache()
-
-
-@pytest.mark.parametrize("name,fmt", [("c2", 0), ("c3", 0), ("c3", 1), ("c3", 2), ("c4", 1), ("c5", 2)])
-def test_full_config_sampled_bit_exact(name, fmt):
-    _sampled_full_config(name, fmt=fmt)
+# Full BASELINE configs at full size: tests/test_gpu_fullconfig.py
 
 
 # --------------------------------------------------------------------------
