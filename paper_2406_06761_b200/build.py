@@ -91,6 +91,15 @@ def build_imma_bench(force: bool = False) -> str:
     return exe
 
 
+def build_tc_ntt_bench(force: bool = False) -> str:
+    """The tensor-core NTT-stage experiment (tcgen05.mma kind::i8 vs the IMAD pipe), a standalone binary."""
+    exe = os.path.join(PKG, "tc_ntt_bench")
+    src = os.path.join(CSRC, "tc_ntt_bench.cu")
+    if force or not os.path.exists(exe) or os.path.getmtime(src) > os.path.getmtime(exe):
+        subprocess.check_call([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", src, "-o", exe])
+    return exe
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
     print(build_intpipe_bench(force="--force" in sys.argv))

@@ -134,6 +134,12 @@ __global__ void __launch_bounds__(512, 1) tmem_kernel(uint32_t iters, uint32_t *
     }
 }
 
+// Rates from the kernel's elapsed time (CUDA events around the launch) and
+// the SM clock: ops / (SMs x elapsed seconds x clock).  The clock is the
+// ratio of a block's clock64 window to its globaltimer window (both taken
+// inside the same block, so the ratio is valid even though the windows of
+// co-resident blocks overlap -- dividing ops by those windows, as round 1
+// did, double-counts co-resident blocks and overstates the rate).
 static void report(const char *name, double ops_per_block, int blocks, int blocks_per_sm, int num_sms, float ms,
                    const unsigned long long *h, const char *unit) {
     double cyc = 0, ns = 0;
@@ -143,11 +149,14 @@ static void report(const char *name, double ops_per_block, int blocks, int block
     }
     cyc /= blocks;
     ns /= blocks;
-    const double per_clk = ops_per_block * blocks_per_sm / cyc;
+    const double clk_hz = cyc / ns * 1e9;
+    const double total = ops_per_block * blocks;
+    const double per_clk = total / num_sms / (ms * 1e-3 * clk_hz);
     printf("{\"op\": \"%s\", \"%s_per_clk_per_sm\": %.2f, \"tera_per_s\": %.3f, \"blocks_per_sm\": %d, "
-           "\"mean_cycles\": %.0f, \"mean_ns\": %.0f, \"sm_clock_mhz\": %.0f, \"event_ms\": %.3f, \"err\": \"%s\"}\n",
-           name, unit, per_clk, ops_per_block * blocks / (ns * 1e-9) / 1e12, blocks_per_sm, cyc, ns, cyc / ns * 1e3,
-           ms, cudaGetErrorString(cudaGetLastError()));
+           "\"sm_clock_mhz\": %.0f, \"event_ms\": %.3f, \"basis\": \"kernel elapsed (CUDA events) x SM clock\", "
+           "\"err\": \"%s\"}\n",
+           name, unit, per_clk, total / (ms * 1e-3) / 1e12, blocks_per_sm, clk_hz / 1e6, ms,
+           cudaGetErrorString(cudaGetLastError()));
     fflush(stdout);
 }
 

@@ -748,11 +748,7 @@ __device__ __forceinline__ void eval_item_tm(const BatchArgs &ba, const ItemCurs
         const uint32_t *chat_next = (qn != 0xffffffffu) ? ba.chat + (size_t)qn * 2 * L * N : nullptr;
         EvalState<N, L, NC> st;
         LimbLoopTM<N, L, L - 1>::run(st, cpre, ba, chat_q, chat_next, tcol, g, cx);
-#ifndef WALLY_NO_L2_PREFETCH
         if (qi == qb) {
-#else
-        if (false) {
-#endif
             // the group's next work item was published before this item started
             // (and the limb loop passed group barriers): pull this thread's slice of
             // its plaintext toward L2 now -- each plaintext is read by one item only,

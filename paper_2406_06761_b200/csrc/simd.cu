@@ -279,55 +279,6 @@ __global__ void __launch_bounds__(256) simd_ptmac_kernel(Mods md, uint32_t N, ui
     }
 }
 
-// The same with the baby step outermost and the m accumulators of a thread
-// in registers (MAXM >= m): every baby ciphertext and plaintext word is read
-// once.  Units are ordered by cluster, so the CTAs sharing a plaintext
-// chunk run together and the plaintexts are served from L2.
-template <int MAXM>
-__global__ void __launch_bounds__(256) simd_ptmac_reg_kernel(Mods md, uint32_t N, uint32_t d, uint32_t g, uint32_t m,
-                                                             const uint32_t *__restrict__ baby,
-                                                             const uint32_t *__restrict__ uq,
-                                                             const uint32_t *__restrict__ ublk,
-                                                             const uint32_t *__restrict__ ptv,
-                                                             const uint32_t *__restrict__ ptc,
-                                                             uint32_t *__restrict__ I) {
-    const uint32_t L = md.L;
-    const uint32_t u = blockIdx.x;
-    const uint32_t w = (blockIdx.y * blockDim.x + threadIdx.x) * 2;
-    if (w >= L * N) return;
-    const uint32_t l = w / N;
-    const uint32_t q = md.q[l], q2 = md.q2[l];
-    const size_t CT = (size_t)2 * L * N, LN = (size_t)L * N;
-    const uint32_t *bq = baby + (size_t)uq[u] * g * CT + w;
-    const uint32_t *pv0 = ptv + (size_t)ublk[u] * d * LN + w, *pc0 = ptc + (size_t)ublk[u] * d * LN + w;
-    uint32_t acc[MAXM][4];
-#pragma unroll
-    for (int j = 0; j < MAXM; j++) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0;
-    for (uint32_t b = 0; b < g; b++) {
-        const uint2 x0 = __ldg(reinterpret_cast<const uint2 *>(bq + (size_t)b * CT));
-        const uint2 x1 = __ldg(reinterpret_cast<const uint2 *>(bq + (size_t)b * CT + LN));
-#pragma unroll
-        for (int j = 0; j < MAXM; j++) {
-            const uint32_t i = (uint32_t)j * g + b;
-            if ((uint32_t)j < m && i < d) {
-                const uint2 pv = __ldg(reinterpret_cast<const uint2 *>(pv0 + (size_t)i * LN));
-                const uint2 pc = __ldg(reinterpret_cast<const uint2 *>(pc0 + (size_t)i * LN));
-                acc[j][0] = csub(acc[j][0] + shoup_mul(x0.x, pv.x, pc.x, q), q2);
-                acc[j][1] = csub(acc[j][1] + shoup_mul(x0.y, pv.y, pc.y, q), q2);
-                acc[j][2] = csub(acc[j][2] + shoup_mul(x1.x, pv.x, pc.x, q), q2);
-                acc[j][3] = csub(acc[j][3] + shoup_mul(x1.y, pv.y, pc.y, q), q2);
-            }
-        }
-    }
-    uint32_t *Iu = I + (size_t)u * m * CT + w;
-#pragma unroll
-    for (int j = 0; j < MAXM; j++) {
-        if ((uint32_t)j < m) {
-            *reinterpret_cast<uint2 *>(Iu + (size_t)j * CT) = make_uint2(csub(acc[j][0], q), csub(acc[j][1], q));
-            *reinterpret_cast<uint2 *>(Iu + (size_t)j * CT + LN) = make_uint2(csub(acc[j][2], q), csub(acc[j][3], q));
-        }
-    }
-}
 
 // ---------------------------------------------------------------------------
 // A chain of rotations in one CTA per unit (n <= 4096): step s = 1..steps
@@ -983,19 +934,7 @@ static cudaError_t launch_ptmac(wally_simd_ctx *c, uint32_t U, const uint32_t *b
                                 const uint32_t *ublk, uint32_t *I, cudaStream_t s) {
     const uint32_t n = c->p.n, thr = 256, words = c->L * n / 2;
     const dim3 grid(U, (words + thr - 1) / thr);
-#ifndef WALLY_SIMD_PTMAC_REG
-#define WALLY_SIMD_PTMAC_REG 0
-#endif
-    if (!WALLY_SIMD_PTMAC_REG)
-        simd_ptmac_kernel<<<grid, thr, 0, s>>>(c->md, n, c->p.d, c->g, c->m, baby, uq, ublk, c->d_ptv, c->d_ptc, I);
-    else if (c->m <= 16)
-        simd_ptmac_reg_kernel<16><<<grid, thr, 0, s>>>(c->md, n, c->p.d, c->g, c->m, baby, uq, ublk, c->d_ptv,
-                                                        c->d_ptc, I);
-    else if (c->m <= 32)
-        simd_ptmac_reg_kernel<32><<<grid, thr, 0, s>>>(c->md, n, c->p.d, c->g, c->m, baby, uq, ublk, c->d_ptv,
-                                                        c->d_ptc, I);
-    else
-        simd_ptmac_kernel<<<grid, thr, 0, s>>>(c->md, n, c->p.d, c->g, c->m, baby, uq, ublk, c->d_ptv, c->d_ptc, I);
+    simd_ptmac_kernel<<<grid, thr, 0, s>>>(c->md, n, c->p.d, c->g, c->m, baby, uq, ublk, c->d_ptv, c->d_ptc, I);
     c->launches++;
     return cudaGetLastError();
 }

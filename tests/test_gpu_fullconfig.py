@@ -88,8 +88,8 @@ def _run(name, fmt, all_pairs=False):
         assert checked == w.num_queries * P
     else:
         rng = np.random.default_rng(99)
-        nq_s = MIN_PAIRS // 3
-        qsel = np.unique(np.concatenate([real, rng.integers(0, w.num_queries, size=nq_s)]))
+        nq_s = -(-MIN_PAIRS // 3)
+        qsel = np.unique(np.concatenate([real, rng.choice(w.num_queries, size=nq_s, replace=False)]))
         pq, pk = [], []
         for q in qsel:                                  # first and last (partial) plaintext of each
             pq += [q, q, q]
