@@ -1655,6 +1655,15 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
                  "l"(src), "r"(bytes), "r"(mbar)
                  : "memory");
 }
+// the same with an L2 cache-eviction policy (createpolicy)
+__device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void *src, uint32_t bytes, uint32_t mbar,
+                                              uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            dst),
+        "l"(src), "r"(bytes), "r"(mbar), "l"(pol)
+        : "memory");
+}
 
 // c1's passes 1 and 2 for one group (pass 0 done), tables in shared memory,
 // one exchange buffer, named barrier `bar` (four barriers).
@@ -1779,6 +1788,8 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
     const int mu = min(__ffs((int)ba.d) - 1, 13);
     const uint32_t total = ba.misc[kMiscTotalItems];
     const uint32_t slots_s = (uint32_t)__cvta_generic_to_shared(slots);
+    constexpr int PRODUCER_WARP = 2 * T / 32 - 1;
+    const uint64_t pol_keep = l2_evict_last_policy();
     uint32_t seq = 0;      // chunk slots consumed by this CTA so far (ring position and phases)
     uint32_t par = 0;
     ItemCursor cur;
@@ -1800,26 +1811,31 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
         const uint32_t *phat0 = s_ba.store + (size_t)(s_ba.pt_base[li] + k0) * L * 2 * N;
         const uint32_t nchunks = (qe - qb) * L * CHUNKS;         // the item's chunk stream: query, limb L-1..0, chunk
         const uint32_t seq0 = seq;
-        // producer: stream element j -> slot (seq0 + j) % NSLOT
+        // producer warp (the last warp, which runs no c0 tail): stream element j -> slot (seq0 + j) % NSLOT;
+        // lane 0 waits for the slot to drain and posts the byte count, lanes 0..7 issue one 4 KB copy each.
+        // The item's plaintexts and the twiddles are re-read by every query round: kept in L2 (evict_last).
         auto produce = [&](uint32_t j) {
             const uint32_t sq = seq0 + j, sl = sq % NSLOT;
-            if (sq >= NSLOT) mbar_wait(empty_b(sl), ((sq / NSLOT) + 1) & 1u);   // consumers of sq - NSLOT done
-            const uint32_t r = j / (L * CHUNKS), J = L - 1 - (j / CHUNKS) % L, c = j % CHUNKS;
-            mbar_expect_tx(full_b(sl), (4 + 2 * np) * CHUNK_BYTES);
-            const uint32_t dst = slots_s + sl * SLOT_BYTES;
-            for (uint32_t u = 0; u < np; u++) {
-                const uint32_t *pj = phat0 + ((size_t)u * L + J) * 2 * N + (size_t)c * 4 * T;
-                bulk_g2s(dst + (2 * u) * CHUNK_BYTES, pj, CHUNK_BYTES, full_b(sl));
-                bulk_g2s(dst + (2 * u + 1) * CHUNK_BYTES, pj + N, CHUNK_BYTES, full_b(sl));
+            if (lane == 0) {
+                if (sq >= NSLOT) mbar_wait(empty_b(sl), ((sq / NSLOT) + 1) & 1u);   // consumers of sq - NSLOT done
+                mbar_expect_tx(full_b(sl), (4 + 2 * np) * CHUNK_BYTES);
             }
+            __syncwarp();
+            const uint32_t r = j / (L * CHUNKS), J = L - 1 - (j / CHUNKS) % L, c = j % CHUNKS;
+            const uint32_t dst = slots_s + sl * SLOT_BYTES + lane * CHUNK_BYTES;
             const uint4 *twJ = reinterpret_cast<const uint4 *>(s_ba.tw_inv + (size_t)J * Gm::TW_LIMB);
-            bulk_g2s(dst + 4 * CHUNK_BYTES, twJ + c * T, CHUNK_BYTES, full_b(sl));
-            bulk_g2s(dst + 5 * CHUNK_BYTES, twJ + aux_block(c) * T, CHUNK_BYTES, full_b(sl));
-            const uint32_t *cq = s_ba.chat + (size_t)s_ba.perm[qb + r] * 2 * L * N + (size_t)c * 4 * T;
-            bulk_g2s(dst + 6 * CHUNK_BYTES, cq + (size_t)J * N, CHUNK_BYTES, full_b(sl));
-            bulk_g2s(dst + 7 * CHUNK_BYTES, cq + ((size_t)L + J) * N, CHUNK_BYTES, full_b(sl));
+            if (lane < 4) {
+                if ((uint32_t)(lane / 2) < np)
+                    bulk_g2s_hint(dst, phat0 + ((size_t)(lane / 2) * L + J) * 2 * N + (lane % 2) * N + (size_t)c * 4 * T,
+                                  CHUNK_BYTES, full_b(sl), pol_keep);
+            } else if (lane < 6) {
+                bulk_g2s_hint(dst, twJ + (lane == 4 ? c : aux_block(c)) * T, CHUNK_BYTES, full_b(sl), pol_keep);
+            } else if (lane < 8) {
+                const uint32_t *cq = s_ba.chat + (size_t)s_ba.perm[qb + r] * 2 * L * N + (size_t)c * 4 * T;
+                bulk_g2s(dst, cq + ((size_t)(lane - 6) * L + J) * N, CHUNK_BYTES, full_b(sl));
+            }
         };
-        if (threadIdx.x == 0)
+        if (warp == PRODUCER_WARP)
             for (uint32_t j = 0; j + 1 < NSLOT && j < nchunks; j++) produce(j);
         for (uint32_t r = 0; qb + r < qe; r++) {
             const uint32_t qo = s_ba.perm[qb + r];
@@ -1835,7 +1851,7 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
 #pragma unroll
                 for (int c = 0; c < CHUNKS; c++) {
                     const uint32_t j = (r * L + Jr) * CHUNKS + c;   // stream element
-                    if (threadIdx.x == 0 && j + NSLOT - 1 < nchunks) produce(j + NSLOT - 1);
+                    if (warp == PRODUCER_WARP && j + NSLOT - 1 < nchunks) produce(j + NSLOT - 1);
                     const uint32_t sq = seq0 + j, sl = sq % NSLOT;
                     mbar_wait(full_b(sl), (sq / NSLOT) & 1u);
                     const uint4 *sp = reinterpret_cast<const uint4 *>(slots + sl * SLOT_BYTES);
