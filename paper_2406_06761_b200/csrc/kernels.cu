@@ -664,10 +664,12 @@ struct LimbLoopTM {
         intt_chain_group<N, NC>(st.a, cx.tw + (size_t)J * Gm::TW_LIMB, g, q, q2, cx.bufA, cx.bar);
         // mod-switch state through TMEM between limbs: L = 3 (its registers are
         // what the chat prefetch needs).  L = 2 keeps its single 16-word state
-        // in registers -- with it in TMEM the L = 2 build faulted on B200
-        // (illegal address; compute-sanitizer is unavailable on this pool), so
-        // that variant is not used.
-        if constexpr (L == 3) {
+        // in registers (round 1: the TMEM variant faulted once on B200;
+        // WALLY_TM_L2_TMEM = 1 builds it again for that investigation).
+#ifndef WALLY_TM_L2_TMEM
+#define WALLY_TM_L2_TMEM 0
+#endif
+        if constexpr (L == 3 || (L == 2 && WALLY_TM_L2_TMEM)) {
             if constexpr (J < L - 1) {
                 // state written at limb J + 1: rtop (J == L - 2) or acc (J < L - 2)
                 tmem_wait_st_all();
@@ -1616,6 +1618,12 @@ static cudaError_t launch_eval_p8(const BatchArgs &a, cudaStream_t s, int num_sm
 // stages and warp-0 tail as in v3; c1's switch state in tensor memory.  No
 // register holds a prefetched operand.
 // ---------------------------------------------------------------------------
+#ifndef WALLY_P8T_HINT
+#define WALLY_P8T_HINT 0
+#endif
+#ifndef WALLY_P8T_PRODUCER_WARP
+#define WALLY_P8T_PRODUCER_WARP -1
+#endif
 namespace p8t {
 constexpr int N = 8192;
 constexpr int T = NttGeom<N>::T;                 // 256 threads per group
@@ -1788,7 +1796,7 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
     const int mu = min(__ffs((int)ba.d) - 1, 13);
     const uint32_t total = ba.misc[kMiscTotalItems];
     const uint32_t slots_s = (uint32_t)__cvta_generic_to_shared(slots);
-    constexpr int PRODUCER_WARP = 2 * T / 32 - 1;
+    constexpr int PRODUCER_WARP = WALLY_P8T_PRODUCER_WARP;
     const uint64_t pol_keep = l2_evict_last_policy();
     uint32_t seq = 0;      // chunk slots consumed by this CTA so far (ring position and phases)
     uint32_t par = 0;
@@ -1811,32 +1819,61 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
         const uint32_t *phat0 = s_ba.store + (size_t)(s_ba.pt_base[li] + k0) * L * 2 * N;
         const uint32_t nchunks = (qe - qb) * L * CHUNKS;         // the item's chunk stream: query, limb L-1..0, chunk
         const uint32_t seq0 = seq;
-        // producer warp (the last warp, which runs no c0 tail): stream element j -> slot (seq0 + j) % NSLOT;
-        // lane 0 waits for the slot to drain and posts the byte count, lanes 0..7 issue one 4 KB copy each.
-        // The item's plaintexts and the twiddles are re-read by every query round: kept in L2 (evict_last).
+        // producer: stream element j -> slot (seq0 + j) % NSLOT.  Thread 0 waits for the slot to drain,
+        // posts the byte count and issues the eight 4 KB copies (WALLY_P8T_PRODUCER_WARP = w >= 0: warp w,
+        // lanes 0..7 one copy each, measured 1.5% slower; WALLY_P8T_HINT = 1: L2 evict_last on the
+        // plaintexts and twiddles, no change)
         auto produce = [&](uint32_t j) {
             const uint32_t sq = seq0 + j, sl = sq % NSLOT;
             if (lane == 0) {
                 if (sq >= NSLOT) mbar_wait(empty_b(sl), ((sq / NSLOT) + 1) & 1u);   // consumers of sq - NSLOT done
                 mbar_expect_tx(full_b(sl), (4 + 2 * np) * CHUNK_BYTES);
             }
+            if (PRODUCER_WARP < 0) {     // single-thread producer (thread 0): issue all eight copies itself
+                if (lane == 0) {
+                    const uint32_t r = j / (L * CHUNKS), J = L - 1 - (j / CHUNKS) % L, c = j % CHUNKS;
+                    const uint32_t dst = slots_s + sl * SLOT_BYTES;
+                    for (uint32_t u = 0; u < np; u++) {
+                        const uint32_t *pj = phat0 + ((size_t)u * L + J) * 2 * N + (size_t)c * 4 * T;
+                        bulk_g2s(dst + (2 * u) * CHUNK_BYTES, pj, CHUNK_BYTES, full_b(sl));
+                        bulk_g2s(dst + (2 * u + 1) * CHUNK_BYTES, pj + N, CHUNK_BYTES, full_b(sl));
+                    }
+                    const uint4 *twJ = reinterpret_cast<const uint4 *>(s_ba.tw_inv + (size_t)J * Gm::TW_LIMB);
+                    bulk_g2s(dst + 4 * CHUNK_BYTES, twJ + c * T, CHUNK_BYTES, full_b(sl));
+                    bulk_g2s(dst + 5 * CHUNK_BYTES, twJ + aux_block(c) * T, CHUNK_BYTES, full_b(sl));
+                    const uint32_t *cq = s_ba.chat + (size_t)s_ba.perm[qb + r] * 2 * L * N + (size_t)c * 4 * T;
+                    bulk_g2s(dst + 6 * CHUNK_BYTES, cq + (size_t)J * N, CHUNK_BYTES, full_b(sl));
+                    bulk_g2s(dst + 7 * CHUNK_BYTES, cq + ((size_t)L + J) * N, CHUNK_BYTES, full_b(sl));
+                }
+                return;
+            }
             __syncwarp();
             const uint32_t r = j / (L * CHUNKS), J = L - 1 - (j / CHUNKS) % L, c = j % CHUNKS;
             const uint32_t dst = slots_s + sl * SLOT_BYTES + lane * CHUNK_BYTES;
             const uint4 *twJ = reinterpret_cast<const uint4 *>(s_ba.tw_inv + (size_t)J * Gm::TW_LIMB);
             if (lane < 4) {
-                if ((uint32_t)(lane / 2) < np)
-                    bulk_g2s_hint(dst, phat0 + ((size_t)(lane / 2) * L + J) * 2 * N + (lane % 2) * N + (size_t)c * 4 * T,
-                                  CHUNK_BYTES, full_b(sl), pol_keep);
+                if ((uint32_t)(lane / 2) < np) {
+                    const uint32_t *src = phat0 + ((size_t)(lane / 2) * L + J) * 2 * N + (lane % 2) * N + (size_t)c * 4 * T;
+                    if (WALLY_P8T_HINT) bulk_g2s_hint(dst, src, CHUNK_BYTES, full_b(sl), pol_keep);
+                    else bulk_g2s(dst, src, CHUNK_BYTES, full_b(sl));
+                }
             } else if (lane < 6) {
-                bulk_g2s_hint(dst, twJ + (lane == 4 ? c : aux_block(c)) * T, CHUNK_BYTES, full_b(sl), pol_keep);
+                const uint4 *src = twJ + (lane == 4 ? c : aux_block(c)) * T;
+                if (WALLY_P8T_HINT) bulk_g2s_hint(dst, src, CHUNK_BYTES, full_b(sl), pol_keep);
+                else bulk_g2s(dst, src, CHUNK_BYTES, full_b(sl));
             } else if (lane < 8) {
                 const uint32_t *cq = s_ba.chat + (size_t)s_ba.perm[qb + r] * 2 * L * N + (size_t)c * 4 * T;
                 bulk_g2s(dst, cq + ((size_t)(lane - 6) * L + J) * N, CHUNK_BYTES, full_b(sl));
             }
         };
-        if (warp == PRODUCER_WARP)
-            for (uint32_t j = 0; j + 1 < NSLOT && j < nchunks; j++) produce(j);
+        // `produced`: stream elements issued so far (the producer warp's count), NSLOT - 1 ahead of the
+        // chunk being consumed.  (Issuing one more into the slot a limb's last chunk frees, so that the
+        // next limb's first NSLOT chunks load during the transform, measured slower: 93.6 vs 88.3 ms --
+        // the producer then waits for every warp before its own transform.)
+        uint32_t produced = 0;
+        const bool producer = warp == (PRODUCER_WARP < 0 ? 0 : PRODUCER_WARP);
+        if (producer)
+            for (; produced + 1 < NSLOT && produced < nchunks; produced++) produce(produced);
         for (uint32_t r = 0; qb + r < qe; r++) {
             const uint32_t qo = s_ba.perm[qb + r];
             uint32_t a[1][V];
@@ -1851,7 +1888,8 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
 #pragma unroll
                 for (int c = 0; c < CHUNKS; c++) {
                     const uint32_t j = (r * L + Jr) * CHUNKS + c;   // stream element
-                    if (warp == PRODUCER_WARP && j + NSLOT - 1 < nchunks) produce(j + NSLOT - 1);
+                    if (producer)
+                        for (; produced <= j + NSLOT - 1 && produced < nchunks; produced++) produce(produced);
                     const uint32_t sq = seq0 + j, sl = sq % NSLOT;
                     mbar_wait(full_b(sl), (sq / NSLOT) & 1u);
                     const uint4 *sp = reinterpret_cast<const uint4 *>(slots + sl * SLOT_BYTES);
