@@ -1866,14 +1866,13 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
                 bulk_g2s(dst, cq + ((size_t)(lane - 6) * L + J) * N, CHUNK_BYTES, full_b(sl));
             }
         };
-        // `produced`: stream elements issued so far (the producer warp's count), NSLOT - 1 ahead of the
-        // chunk being consumed.  (Issuing one more into the slot a limb's last chunk frees, so that the
-        // next limb's first NSLOT chunks load during the transform, measured slower: 93.6 vs 88.3 ms --
-        // the producer then waits for every warp before its own transform.)
-        uint32_t produced = 0;
+        // elements are issued NSLOT - 1 ahead of the chunk being consumed.  (Issuing one more into the
+        // slot a limb's last chunk frees, so that the next limb's first NSLOT chunks load during the
+        // transform, measured slower: 93.6 vs 88.3 ms -- the producer then waits for every warp
+        // before its own transform.)
         const bool producer = warp == (PRODUCER_WARP < 0 ? 0 : PRODUCER_WARP);
         if (producer)
-            for (; produced + 1 < NSLOT && produced < nchunks; produced++) produce(produced);
+            for (uint32_t j = 0; j + 1 < NSLOT && j < nchunks; j++) produce(j);
         for (uint32_t r = 0; qb + r < qe; r++) {
             const uint32_t qo = s_ba.perm[qb + r];
             uint32_t a[1][V];
@@ -1888,8 +1887,7 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
 #pragma unroll
                 for (int c = 0; c < CHUNKS; c++) {
                     const uint32_t j = (r * L + Jr) * CHUNKS + c;   // stream element
-                    if (producer)
-                        for (; produced <= j + NSLOT - 1 && produced < nchunks; produced++) produce(produced);
+                    if (producer && j + NSLOT - 1 < nchunks) produce(j + NSLOT - 1);
                     const uint32_t sq = seq0 + j, sl = sq % NSLOT;
                     mbar_wait(full_b(sl), (sq / NSLOT) & 1u);
                     const uint4 *sp = reinterpret_cast<const uint4 *>(slots + sl * SLOT_BYTES);
