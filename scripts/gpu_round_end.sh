@@ -1,14 +1,29 @@
-# Everything the profiles/ directory holds, in one gpurun call (about 20 GPU-minutes):
-# GPU suite, the default bench line, per-config lines, SIMD lines, the launch list,
-# DRAM traffic of c3/c4/c5, ncu --set full of the c3 and c4 fused kernels, the microbenchmarks.
+# Round-2 evidence in one gpurun call: GPU suite, every bench line (all configs, response formats,
+# SIMD formulation), the launch list of the default bench, ncu --set full of the c3 and c4 fused
+# kernels, the microbenchmarks and smoke.  Outputs under gpurun_out/ (copied to profiles/ by hand).
 set -o pipefail
 mkdir -p gpurun_out
-CFGS="c1 c2 c4 c5" TRAFFIC="c3 c4 c5" bash scripts/gpu_refresh.sh
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/smi.txt 2>&1
+timeout 1800 python -m pytest tests -m gpu -q -rA > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu.log
+timeout 900 python bench.py > gpurun_out/bench_c3_default.json 2> gpurun_out/bench_c3_default.err; echo "bench rc=$?"; head -c 400 gpurun_out/bench_c3_default.json; echo
+for c in c1 c2 c4 c5; do
+  timeout 900 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
+  python -c "import json;d=json.load(open('gpurun_out/bench_$c.json'));r=d['roofline'];print('$c',d['value'],r['fused_ms_per_launch'],r['frac'],d['e2e']['value'],d['clocks'])"
+done
+for f in full compact; do
+  timeout 900 python bench.py --config c3 --resp $f --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3_$f.json 2> gpurun_out/bench_c3_$f.err
+  python -c "import json;d=json.load(open('gpurun_out/bench_c3_$f.json'));r=d['roofline'];print('c3 $f',d['value'],r['fused_ms_per_launch'],r['frac'],d['e2e']['value'])"
+done
+timeout 900 python bench.py --config c4 --resp full --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c4_full.json 2> gpurun_out/bench_c4_full.err
+python -c "import json;d=json.load(open('gpurun_out/bench_c4_full.json'));r=d['roofline'];print('c4 full',d['value'],r['fused_ms_per_launch'],r['frac'],d['e2e']['value'])"
 bash scripts/gpu_simd_refresh.sh
+B="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline"
+timeout 600 $B > gpurun_out/plain_launch.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv $B > gpurun_out/ncu_launch.log 2>&1; echo "ncu launch rc=$?"
 for c in c3 c4; do
   P="python bench.py --config $c --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:eval_kernel -s 1 -c 1 -o gpurun_out/prof_final_$c $P > gpurun_out/ncu_final_$c.log 2>&1; echo "$c ncu rc=$?"
+  timeout 600 $P > gpurun_out/plain_full_$c.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k regex:eval_kernel -s 1 -c 1 -o gpurun_out/prof_final_$c $P > gpurun_out/ncu_final_$c.log 2>&1; echo "$c ncu rc=$?"
 done
 ./paper_2406_06761_b200/intpipe_bench > gpurun_out/intpipe.jsonl 2>&1
 ./paper_2406_06761_b200/imma_bench > gpurun_out/imma.jsonl 2>&1
+./paper_2406_06761_b200/tc_ntt_bench --reps 16 --mma-only > gpurun_out/tc_ntt.jsonl 2>&1
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
