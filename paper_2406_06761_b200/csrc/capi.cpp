@@ -553,6 +553,7 @@ static int eval_impl(wally_ctx *c, uint32_t nq, const uint32_t *ids, const uint3
     // work item (c1: 32 items for 296 groups): one query per item instead
     a.chunk = (nq < 4u * (uint32_t)c->num_sms) ? 1u : kQueryChunk;
     a.ppi = eval_plaintexts_per_item(a.n, a.L, a.d, a.compact);
+    if (a.ppi == 2) a.chunk = kP8QueryChunk;   // n = 8192 kernel v5 (wally_internal.h)
     a.n_local = c->n_local;
     a.total_clusters = c->total_clusters;
     a.tw_fwd = c->d_tw_fwd;

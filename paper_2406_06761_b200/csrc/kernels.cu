@@ -20,9 +20,6 @@
 #include "tmem.cuh"
 #include "wally_internal.h"
 
-#ifndef WALLY_OPLD_P8
-#define WALLY_OPLD_P8 3
-#endif
 #ifndef WALLY_OPLD_PR
 #define WALLY_OPLD_PR 1
 #endif
@@ -669,10 +666,20 @@ struct LimbLoopTM {
 #ifndef WALLY_TM_L2_TMEM
 #define WALLY_TM_L2_TMEM 0
 #endif
+#ifndef WALLY_TM_SYNC_LD
+#define WALLY_TM_SYNC_LD 0
+#endif
         if constexpr (L == 3 || (L == 2 && WALLY_TM_L2_TMEM)) {
             if constexpr (J < L - 1) {
                 // state written at limb J + 1: rtop (J == L - 2) or acc (J < L - 2)
                 tmem_wait_st_all();
+#if WALLY_TM_SYNC_LD
+#pragma unroll
+                for (int c = 0; c < NC; c++) {
+                    if constexpr (J == L - 2) tmem_ld_sync16(tcol + 96 + 16 * c, st.rtop[c]);
+                    else tmem_ld_sync16(tcol + 96 + 16 * c, st.acc[c][0]);
+                }
+#else
 #pragma unroll
                 for (int c = 0; c < NC; c++) {
                     if constexpr (J == L - 2) tmem_ld<16>(tcol + 96 + 16 * c, st.rtop[c]);
@@ -683,6 +690,7 @@ struct LimbLoopTM {
                     if constexpr (J == L - 2) tmem_wait_ld<16>(st.rtop[c]);
                     else tmem_wait_ld<16>(st.acc[c][0]);
                 }
+#endif
             }
 #pragma unroll
             for (int c = 0; c < NC; c++) ms_step<L, J, V>(st.a[c], st.rtop[c], st.acc[c], ba.kp);
@@ -1365,9 +1373,9 @@ static cudaError_t launch_eval_pr(const BatchArgs &a, cudaStream_t s, int num_sm
 
 
 // ---------------------------------------------------------------------------
-// n = 8192 with compact responses and 32 | d (c4): the whole-CTA kernel with
-// c0's transform pruned as in v6 (pass 0 on V = 32 values per thread, five
-// shuffle stages, the rest on warp 0); c1 unchanged.
+// n = 8192 with compact responses and 32 | d (c4): c0's transform pruned as
+// in v6 (pass 0 on V = 32 values per thread, five shuffle stages, the rest
+// on warp 0 of the group).
 // ---------------------------------------------------------------------------
 // Register tail for n = 8192 and mu = 9 (c4: d = 512): after stage 9 the
 // survivors are positions 512 k + 511, c = 16 k + 15 (k < 16); lanes 0..15
@@ -1399,200 +1407,6 @@ __device__ __forceinline__ void c0_tail_fast8(uint32_t *z, uint32_t *cst, const 
     __syncwarp();
 }
 
-// One limb of both components, merged (n = 8192): the operands are streamed
-// in chunks of four values, so the plaintext is loaded once for c0 and c1;
-// c0's pass 0 (Y outputs only) runs as a reduction tree over the chunks
-// (stage s block b combines the last elements of its two halves, exactly
-// as C0Pass0), leaving one value per thread for the shuffle stages; c1 goes
-// through the whole-CTA inverse NTT and the switch step (state in TMEM);
-// c0's tail runs on warp 0 after c1's transform (whose barriers publish z).
-template <int L, int J>
-struct LimbLoopP8M {
-    static constexpr int N = 8192;
-    static __device__ __forceinline__ void run(uint32_t (&a)[1][NttGeom<N>::V], const BatchArgs &ba,
-                                               const uint32_t *chat_q, const uint32_t *phat, int g,
-                                               const ChainCtx &cx, uint32_t tcol, uint32_t *ybuf, uint32_t &par,
-                                               uint32_t *cst, int mu, const uint2 *s_mrg, uint4 (&pre)[4]) {
-        using Gm = NttGeom<N>;
-        constexpr int V = Gm::V, T = Gm::T;
-        static_assert(V == 32, "the c0 tree assumes 32 values per thread");
-        constexpr int NA = (L > 2) ? (L - 2) : 1;
-        const uint32_t q = ba.kp.q[J], q2 = ba.kp.q2[J];
-        static_assert(NttStore<N>::CHUNK_MAJOR, "chunk c of thread g at uint4 index c T + g");
-        const uint4 *pv = reinterpret_cast<const uint4 *>(phat + (size_t)J * 2 * N) + g;
-        const uint4 *ppv = reinterpret_cast<const uint4 *>(phat + (size_t)J * 2 * N + N) + g;
-        const uint4 *c0v = reinterpret_cast<const uint4 *>(chat_q + (size_t)J * N) + g;
-        const uint4 *c1v = reinterpret_cast<const uint4 *>(chat_q + ((size_t)L + J) * N) + g;
-        const uint4 *t4 = reinterpret_cast<const uint4 *>(ba.tw_inv + (size_t)J * Gm::TW_LIMB) + g;
-        auto tw = [&](int slot) -> uint2 { return __ldg(reinterpret_cast<const uint2 *>(t4 + (slot / 2) * T) + (slot % 2)); };
-        auto yo = [&](uint32_t X, uint32_t Y, uint2 w) { return shoup_mul(X - Y + q2, w.x, w.y, q); };
-        uint32_t l2 = 0, l3 = 0, l4 = 0, y = 0;
-        uint4 np = pre[0], npp = pre[1], nx0 = pre[2], nx1 = pre[3];
-#pragma unroll
-        for (int c = 0; c < 8; c++) {
-            const uint4 p = np, pp = npp, x0 = nx0, x1 = nx1;
-            if (c + 1 < 8) {     // the next chunk's loads fly while this chunk computes
-                np = ldg_op<WALLY_OPLD_P8>(pv + (c + 1) * T);
-                npp = ldg_op<WALLY_OPLD_P8>(ppv + (c + 1) * T);
-                nx0 = ldg_op<WALLY_OPLD_P8>(c0v + (c + 1) * T);
-                nx1 = ldg_op<WALLY_OPLD_P8>(c1v + (c + 1) * T);
-            }
-            a[0][4 * c + 0] = shoup_mul(x1.x, p.x, pp.x, q);
-            a[0][4 * c + 1] = shoup_mul(x1.y, p.y, pp.y, q);
-            a[0][4 * c + 2] = shoup_mul(x1.z, p.z, pp.z, q);
-            a[0][4 * c + 3] = shoup_mul(x1.w, p.w, pp.w, q);
-            const uint32_t y0 = shoup_mul(x0.x, p.x, pp.x, q), y1 = shoup_mul(x0.y, p.y, pp.y, q);
-            const uint32_t y2 = shoup_mul(x0.z, p.z, pp.z, q), y3 = shoup_mul(x0.w, p.w, pp.w, q);
-            const uint4 w0 = __ldg(t4 + c * T);                       // stage 0, blocks 2c, 2c + 1
-            const uint32_t u0 = yo(y0, y1, make_uint2(w0.x, w0.y)), u1 = yo(y2, y3, make_uint2(w0.z, w0.w));
-            const uint32_t v = yo(u0, u1, tw(16 + c));                // stage 1, block c
-            if (c % 2 == 0) {
-                l2 = v;
-            } else {
-                const uint32_t v2 = yo(l2, v, tw(24 + c / 2));         // stage 2, block c / 2
-                if ((c / 2) % 2 == 0) {
-                    l3 = v2;
-                } else {
-                    const uint32_t v3 = yo(l3, v2, tw(28 + c / 4));    // stage 3, block c / 4
-                    if (c / 4 == 0) l4 = v3;
-                    else y = yo(l4, v3, tw(30));                       // stage 4
-                }
-            }
-        }
-        uint32_t *z = ybuf + par * T;
-        z[g] = c0_mid<N>(y, g, mu, s_mrg + J * 256, q, q2);
-        if constexpr (J > 0) {   // the next limb's first chunk flies during this limb's transform
-            const uint32_t *pn = phat + (size_t)(J - 1) * 2 * N + 4 * g;
-            pre[0] = ldg_op<WALLY_OPLD_P8>(pn);
-            pre[1] = ldg_op<WALLY_OPLD_P8>(pn + N);
-            pre[2] = ldg_op<WALLY_OPLD_P8>(chat_q + (size_t)(J - 1) * N + 4 * g);
-            pre[3] = ldg_op<WALLY_OPLD_P8>(chat_q + ((size_t)L + J - 1) * N + 4 * g);
-        }
-        intt_chain<N, 1>(a, cx.tw + (size_t)J * Gm::TW_LIMB, g, q, q2, cx.bufA, cx.bufB);
-        if (g < 32) {
-            if (mu == 9) c0_tail_fast8<L, J>(z, cst, s_mrg + J * 256, g, ba.kp);
-            else c0_tail<N, L, J>(z, cst, s_mrg + J * 256, g, mu, ba.kp);
-        }
-        par ^= 1u;
-        if constexpr (L > 1 && J < L - 1) tmem_wait_st_all();
-#pragma unroll
-        for (int c8 = 0; c8 < V / 8; c8++) {
-            uint32_t rt[8], ac[NA][8];
-#pragma unroll
-            for (int k = 0; k < 8; k++) {
-                rt[k] = 0;
-#pragma unroll
-                for (int l = 0; l < NA; l++) ac[l][k] = 0;
-            }
-            if constexpr (L > 1 && J == L - 2) {
-                tmem_ld<8>(tcol + 8 * c8, rt);
-                tmem_wait_ld<8>(rt);
-            }
-            if constexpr (L > 2 && J < L - 2) {
-#pragma unroll
-                for (int l = 0; l <= J; l++) {
-                    tmem_ld<8>(tcol + 32 * l + 8 * c8, ac[l]);
-                    tmem_wait_ld<8>(ac[l]);
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < 8; k++) {
-                uint32_t acc[NA];
-#pragma unroll
-                for (int l = 0; l < NA; l++) acc[l] = ac[l][k];
-                ms_elem<L, J, NA>(a[0][8 * c8 + k], rt[k], acc, ba.kp);
-#pragma unroll
-                for (int l = 0; l < NA; l++) ac[l][k] = acc[l];
-            }
-            if constexpr (L > 1 && J == L - 1) tmem_st<8>(tcol + 8 * c8, rt);
-            if constexpr (L > 2 && J > 0 && J <= L - 2) {
-#pragma unroll
-                for (int l = 0; l < J; l++) tmem_st<8>(tcol + 32 * l + 8 * c8, ac[l]);
-            }
-        }
-        if constexpr (J > 0)
-            LimbLoopP8M<L, J - 1>::run(a, ba, chat_q, phat, g, cx, tcol, ybuf, par, cst, mu, s_mrg, pre);
-    }
-};
-
-template <int L, int FMT>
-__global__ void __launch_bounds__(NttGeom<8192>::T, 2) eval_kernel_p8(BatchArgs ba) {
-    constexpr int N = 8192;
-    using Gm = NttGeom<N>;
-    constexpr int NA = (L > 2) ? (L - 2) : 1;
-    extern __shared__ uint32_t smem[];
-    ChainCtx cx{ba.tw_inv, smem, smem + Gm::SMEM_WORDS, 0};
-    __shared__ BatchArgs s_ba;     // the limb loop reads the arguments from here (fewer spills than param space)
-    __shared__ uint32_t s_taddr;
-    const int warp = threadIdx.x / 32;
-    if (threadIdx.x == 0) s_ba = ba;
-    if (warp == 0) {   // 128 columns: NA x 32 per thread, warps w and w + 4 share a lane quadrant
-        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&s_taddr);
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(dst) : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tcol = s_taddr + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 64);
-    __shared__ uint32_t s_item[2];
-    __shared__ uint32_t s_rmap[ResultMap<N>::WORDS];
-    __shared__ uint32_t s_ybuf[2 * Gm::T];
-    __shared__ uint32_t s_cst[(N / 32) * (1 + NA)];
-    __shared__ uint2 s_mrg[L * 256];
-    for (int i = threadIdx.x; i < L * 256; i += blockDim.x) s_mrg[i] = __ldg(ba.tw_mrg + (size_t)(i >> 8) * N + (i & 255));
-    const int g = threadIdx.x;
-    const int mu = min(__ffs((int)ba.d) - 1, 13);
-    const uint32_t total = ba.misc[kMiscTotalItems];
-    uint32_t par = 0;
-    ItemCursor cur;
-    for (uint32_t it = 0;; it++) {
-        if (g == 0) s_item[it & 1] = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
-        __syncthreads();
-        const uint32_t item = s_item[it & 1];
-        if (item >= total) break;
-        cur.seek(ba, item);
-        const uint32_t li = cur.li;
-        const uint32_t cnt = ba.counts[li];
-        const uint32_t P = ba.n_pt[li];
-        const uint32_t ch = (item - cur.b) / P, k = (item - cur.b) % P;
-        const uint32_t qb = ba.seg[li] + ch * ba.chunk;
-        const uint32_t qe = min(qb + ba.chunk, ba.seg[li] + cnt);
-        const uint32_t *phat = ba.store + (size_t)(ba.pt_base[li] + k) * L * 2 * N;
-        for (uint32_t qi = qb; qi < qe; qi++) {
-            const uint32_t qo = ba.perm[qi];
-            uint32_t *out_q = ba.resp + ba.resp_off[qo] + (size_t)k * ba.wpp;
-            const uint32_t *chat_q = ba.chat + (size_t)qo * 2 * L * N;
-            uint32_t a1[1][Gm::V];
-            uint4 pre[4];
-            {
-                const uint32_t *pn = phat + (size_t)(L - 1) * 2 * N + 4 * g;
-                pre[0] = ldg_op<WALLY_OPLD_P8>(pn);
-                pre[1] = ldg_op<WALLY_OPLD_P8>(pn + N);
-                pre[2] = ldg_op<WALLY_OPLD_P8>(chat_q + (size_t)(L - 1) * N + 4 * g);
-                pre[3] = ldg_op<WALLY_OPLD_P8>(chat_q + (2 * (size_t)L - 1) * N + 4 * g);
-            }
-            LimbLoopP8M<L, L - 1>::run(a1, s_ba, chat_q, phat, g, cx, tcol, s_ybuf, par, s_cst, mu, s_mrg, pre);
-            if (g < 32) c0_write_results<N>(s_ba, out_q, s_ybuf + (par ^ 1u) * Gm::T, g, mu);
-            write_component<N, FMT>(s_ba, out_q, a1[0], 1, g, s_rmap);
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(s_taddr) : "memory");
-}
-
-template <int L, int FMT>
-static cudaError_t launch_eval_p8(const BatchArgs &a, cudaStream_t s, int num_sms) {
-    static DeviceOnce once;
-    const size_t smem = chain_smem<8192>(1);
-    cudaError_t e = device_once(once, [&](int *) { return allow_smem(eval_kernel_p8<L, FMT>, smem); });
-    if (e != cudaSuccess) return e;
-    eval_kernel_p8<L, FMT><<<num_sms * 2, NttGeom<8192>::T, smem, s>>>(a);   // two CTAs per SM
-    return cudaGetLastError();
-}
-
 // ---------------------------------------------------------------------------
 // n = 8192, compact responses, 32 | d (c4), v5: operands staged by bulk
 // asynchronous copies (cp.async.bulk + mbarrier, "TMA or cp.async staging of
@@ -1618,12 +1432,6 @@ static cudaError_t launch_eval_p8(const BatchArgs &a, cudaStream_t s, int num_sm
 // stages and warp-0 tail as in v3; c1's switch state in tensor memory.  No
 // register holds a prefetched operand.
 // ---------------------------------------------------------------------------
-#ifndef WALLY_P8T_HINT
-#define WALLY_P8T_HINT 0
-#endif
-#ifndef WALLY_P8T_PRODUCER_WARP
-#define WALLY_P8T_PRODUCER_WARP -1
-#endif
 namespace p8t {
 constexpr int N = 8192;
 constexpr int T = NttGeom<N>::T;                 // 256 threads per group
@@ -1662,15 +1470,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                  "l"(src), "r"(bytes), "r"(mbar)
                  : "memory");
-}
-// the same with an L2 cache-eviction policy (createpolicy)
-__device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void *src, uint32_t bytes, uint32_t mbar,
-                                              uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-            dst),
-        "l"(src), "r"(bytes), "r"(mbar), "l"(pol)
-        : "memory");
 }
 
 // c1's passes 1 and 2 for one group (pass 0 done), tables in shared memory,
@@ -1796,83 +1595,80 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
     const int mu = min(__ffs((int)ba.d) - 1, 13);
     const uint32_t total = ba.misc[kMiscTotalItems];
     const uint32_t slots_s = (uint32_t)__cvta_generic_to_shared(slots);
-    constexpr int PRODUCER_WARP = WALLY_P8T_PRODUCER_WARP;
-    const uint64_t pol_keep = l2_evict_last_policy();
+#ifndef WALLY_P8T_TAIL_WARP
+#define WALLY_P8T_TAIL_WARP 1
+#endif
+    constexpr int TAIL_WARP = WALLY_P8T_TAIL_WARP;
     uint32_t seq = 0;      // chunk slots consumed by this CTA so far (ring position and phases)
     uint32_t par = 0;
-    ItemCursor cur;
+    ItemCursor cur, ncur;
+    // A work item's operand stream: (query, limb L-1..0, chunk); its description, computed by
+    // every thread for the current item and by the producer (thread 0) for the next one.
+    struct Desc {
+        const uint32_t *phat0;
+        uint32_t qb, qe, np, k0, nchunks;
+    };
+    auto describe = [&](ItemCursor &cu, uint32_t item) -> Desc {
+        Desc d{};
+        if (item >= total) return d;                            // nchunks = 0: no item
+        cu.seek(s_ba, item);
+        const uint32_t li = cu.li;
+        const uint32_t P = s_ba.n_pt[li], PP = (P + 1) / 2;
+        const uint32_t ch = (item - cu.b) / PP;
+        d.k0 = 2 * ((item - cu.b) % PP);
+        d.np = min(2u, P - d.k0);                               // plaintexts of the item (1 only for odd P_c)
+        d.qb = s_ba.seg[li] + ch * s_ba.chunk;
+        d.qe = min(d.qb + s_ba.chunk, s_ba.seg[li] + s_ba.counts[li]);
+        d.phat0 = s_ba.store + (size_t)(s_ba.pt_base[li] + d.k0) * L * 2 * N;
+        d.nchunks = (d.qe - d.qb) * L * CHUNKS;
+        return d;
+    };
+    // producer (thread 0): element j of item description d into ring position sq: wait for the slot
+    // to drain (one arrival per warp on its empty barrier), post the byte count on its full barrier,
+    // issue the eight 4 KB copies
+    auto produce = [&](const Desc &d, uint32_t j, uint32_t sq) {
+        const uint32_t sl = sq % NSLOT;
+        if (sq >= NSLOT) mbar_wait(empty_b(sl), ((sq / NSLOT) + 1) & 1u);
+        mbar_expect_tx(full_b(sl), (4 + 2 * d.np) * CHUNK_BYTES);
+        const uint32_t r = j / (L * CHUNKS), J = L - 1 - (j / CHUNKS) % L, c = j % CHUNKS;
+        const uint32_t dst = slots_s + sl * SLOT_BYTES;
+        for (uint32_t u = 0; u < d.np; u++) {
+            const uint32_t *pj = d.phat0 + ((size_t)u * L + J) * 2 * N + (size_t)c * 4 * T;
+            bulk_g2s(dst + (2 * u) * CHUNK_BYTES, pj, CHUNK_BYTES, full_b(sl));
+            bulk_g2s(dst + (2 * u + 1) * CHUNK_BYTES, pj + N, CHUNK_BYTES, full_b(sl));
+        }
+        const uint4 *twJ = reinterpret_cast<const uint4 *>(s_ba.tw_inv + (size_t)J * Gm::TW_LIMB);
+        bulk_g2s(dst + 4 * CHUNK_BYTES, twJ + c * T, CHUNK_BYTES, full_b(sl));
+        bulk_g2s(dst + 5 * CHUNK_BYTES, twJ + aux_block(c) * T, CHUNK_BYTES, full_b(sl));
+        const uint32_t *cq = s_ba.chat + (size_t)s_ba.perm[d.qb + r] * 2 * L * N + (size_t)c * 4 * T;
+        bulk_g2s(dst + 6 * CHUNK_BYTES, cq + (size_t)J * N, CHUNK_BYTES, full_b(sl));
+        bulk_g2s(dst + 7 * CHUNK_BYTES, cq + ((size_t)L + J) * N, CHUNK_BYTES, full_b(sl));
+    };
+    uint32_t pre_issued = 0;   // thread 0: elements of the current item issued while the previous one ran
+    if (threadIdx.x == 0) s_item[0] = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
     for (uint32_t it = 0;; it++) {
-        if (threadIdx.x == 0) s_item[it & 1] = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
         __syncthreads();
         const uint32_t item = s_item[it & 1];
         if (item >= total) break;
-        cur.seek(s_ba, item);
-        const uint32_t li = cur.li;
-        const uint32_t cnt = s_ba.counts[li];
-        const uint32_t P = s_ba.n_pt[li], PP = (P + 1) / 2;
-        const uint32_t ch = (item - cur.b) / PP, k0 = 2 * ((item - cur.b) % PP);
-        const uint32_t np = min(2u, P - k0);                    // plaintexts of this item (1 only for odd P_c)
-        const uint32_t k = k0 + grp;
+        // the next item is claimed now, so the producer can stream its first chunks while this one ends
+        if (threadIdx.x == 0) s_item[(it + 1) & 1] = atomicAdd(&ba.misc[kMiscWorkCounter], 1u);
+        const Desc d = describe(cur, item);
+        Desc dn{};
+        if (threadIdx.x == 0) dn = describe(ncur, s_item[(it + 1) & 1]);
+        const uint32_t qb = d.qb, qe = d.qe, np = d.np, nchunks = d.nchunks;
+        const uint32_t k = d.k0 + grp;
         const bool active = (uint32_t)grp < np;
-        const uint32_t qb = s_ba.seg[li] + ch * s_ba.chunk;
-        const uint32_t qe = min(qb + s_ba.chunk, s_ba.seg[li] + cnt);
-        const uint32_t *phat0 = s_ba.store + (size_t)(s_ba.pt_base[li] + k0) * L * 2 * N;
-        const uint32_t nchunks = (qe - qb) * L * CHUNKS;         // the item's chunk stream: query, limb L-1..0, chunk
         const uint32_t seq0 = seq;
-        // producer: stream element j -> slot (seq0 + j) % NSLOT.  Thread 0 waits for the slot to drain,
-        // posts the byte count and issues the eight 4 KB copies (WALLY_P8T_PRODUCER_WARP = w >= 0: warp w,
-        // lanes 0..7 one copy each, measured 1.5% slower; WALLY_P8T_HINT = 1: L2 evict_last on the
-        // plaintexts and twiddles, no change)
-        auto produce = [&](uint32_t j) {
-            const uint32_t sq = seq0 + j, sl = sq % NSLOT;
-            if (lane == 0) {
-                if (sq >= NSLOT) mbar_wait(empty_b(sl), ((sq / NSLOT) + 1) & 1u);   // consumers of sq - NSLOT done
-                mbar_expect_tx(full_b(sl), (4 + 2 * np) * CHUNK_BYTES);
-            }
-            if (PRODUCER_WARP < 0) {     // single-thread producer (thread 0): issue all eight copies itself
-                if (lane == 0) {
-                    const uint32_t r = j / (L * CHUNKS), J = L - 1 - (j / CHUNKS) % L, c = j % CHUNKS;
-                    const uint32_t dst = slots_s + sl * SLOT_BYTES;
-                    for (uint32_t u = 0; u < np; u++) {
-                        const uint32_t *pj = phat0 + ((size_t)u * L + J) * 2 * N + (size_t)c * 4 * T;
-                        bulk_g2s(dst + (2 * u) * CHUNK_BYTES, pj, CHUNK_BYTES, full_b(sl));
-                        bulk_g2s(dst + (2 * u + 1) * CHUNK_BYTES, pj + N, CHUNK_BYTES, full_b(sl));
-                    }
-                    const uint4 *twJ = reinterpret_cast<const uint4 *>(s_ba.tw_inv + (size_t)J * Gm::TW_LIMB);
-                    bulk_g2s(dst + 4 * CHUNK_BYTES, twJ + c * T, CHUNK_BYTES, full_b(sl));
-                    bulk_g2s(dst + 5 * CHUNK_BYTES, twJ + aux_block(c) * T, CHUNK_BYTES, full_b(sl));
-                    const uint32_t *cq = s_ba.chat + (size_t)s_ba.perm[qb + r] * 2 * L * N + (size_t)c * 4 * T;
-                    bulk_g2s(dst + 6 * CHUNK_BYTES, cq + (size_t)J * N, CHUNK_BYTES, full_b(sl));
-                    bulk_g2s(dst + 7 * CHUNK_BYTES, cq + ((size_t)L + J) * N, CHUNK_BYTES, full_b(sl));
-                }
-                return;
-            }
-            __syncwarp();
-            const uint32_t r = j / (L * CHUNKS), J = L - 1 - (j / CHUNKS) % L, c = j % CHUNKS;
-            const uint32_t dst = slots_s + sl * SLOT_BYTES + lane * CHUNK_BYTES;
-            const uint4 *twJ = reinterpret_cast<const uint4 *>(s_ba.tw_inv + (size_t)J * Gm::TW_LIMB);
-            if (lane < 4) {
-                if ((uint32_t)(lane / 2) < np) {
-                    const uint32_t *src = phat0 + ((size_t)(lane / 2) * L + J) * 2 * N + (lane % 2) * N + (size_t)c * 4 * T;
-                    if (WALLY_P8T_HINT) bulk_g2s_hint(dst, src, CHUNK_BYTES, full_b(sl), pol_keep);
-                    else bulk_g2s(dst, src, CHUNK_BYTES, full_b(sl));
-                }
-            } else if (lane < 6) {
-                const uint4 *src = twJ + (lane == 4 ? c : aux_block(c)) * T;
-                if (WALLY_P8T_HINT) bulk_g2s_hint(dst, src, CHUNK_BYTES, full_b(sl), pol_keep);
-                else bulk_g2s(dst, src, CHUNK_BYTES, full_b(sl));
-            } else if (lane < 8) {
-                const uint32_t *cq = s_ba.chat + (size_t)s_ba.perm[qb + r] * 2 * L * N + (size_t)c * 4 * T;
-                bulk_g2s(dst, cq + ((size_t)(lane - 6) * L + J) * N, CHUNK_BYTES, full_b(sl));
-            }
+        // elements are issued NSLOT - 1 ahead of the chunk being consumed, across the item boundary
+        // (issuing one more into the slot a limb's last chunk frees, so that the next limb's first NSLOT
+        // chunks load during the transform, measured slower: 93.6 vs 88.3 ms -- the producer then waits
+        // for every warp before its own transform)
+        auto issue = [&](uint32_t j) {
+            if (j < nchunks) produce(d, j, seq0 + j);
+            else if (j - nchunks < dn.nchunks) produce(dn, j - nchunks, seq0 + j);
         };
-        // elements are issued NSLOT - 1 ahead of the chunk being consumed.  (Issuing one more into the
-        // slot a limb's last chunk frees, so that the next limb's first NSLOT chunks load during the
-        // transform, measured slower: 93.6 vs 88.3 ms -- the producer then waits for every warp
-        // before its own transform.)
-        const bool producer = warp == (PRODUCER_WARP < 0 ? 0 : PRODUCER_WARP);
-        if (producer)
-            for (uint32_t j = 0; j + 1 < NSLOT && j < nchunks; j++) produce(j);
+        if (threadIdx.x == 0)
+            for (uint32_t j = pre_issued; j + 1 < NSLOT; j++) issue(j);
         for (uint32_t r = 0; qb + r < qe; r++) {
             const uint32_t qo = s_ba.perm[qb + r];
             uint32_t a[1][V];
@@ -1887,7 +1683,7 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
 #pragma unroll
                 for (int c = 0; c < CHUNKS; c++) {
                     const uint32_t j = (r * L + Jr) * CHUNKS + c;   // stream element
-                    if (producer && j + NSLOT - 1 < nchunks) produce(j + NSLOT - 1);
+                    if (threadIdx.x == 0) issue(j + NSLOT - 1);
                     const uint32_t sq = seq0 + j, sl = sq % NSLOT;
                     mbar_wait(full_b(sl), (sq / NSLOT) & 1u);
                     const uint4 *sp = reinterpret_cast<const uint4 *>(slots + sl * SLOT_BYTES);
@@ -1964,11 +1760,12 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
                 uint32_t *z = s_ybuf[grp] + par * T;
                 z[g] = c0_mid<N>(y, g, mu, s_mrg + J * 256, q, q2);
                 p8t_intt_tail(a, s_tw12 + (size_t)J * TW12, g, q, q2, xb, bar);
-                if (g < 32) {
+                // c0's tail on the group's warp TAIL_WARP (not warp 0, whose thread 0 is the producer)
+                if (g / 32 == TAIL_WARP) {
                     limb_dispatch<L>(J, [&](auto JC) {
                         constexpr int JJ = decltype(JC)::value;
-                        if (mu == 9) c0_tail_fast8<L, JJ>(z, s_cst[grp], s_mrg + JJ * 256, g, s_ba.kp);
-                        else c0_tail<N, L, JJ>(z, s_cst[grp], s_mrg + JJ * 256, g, mu, s_ba.kp);
+                        if (mu == 9) c0_tail_fast8<L, JJ>(z, s_cst[grp], s_mrg + JJ * 256, lane, s_ba.kp);
+                        else c0_tail<N, L, JJ>(z, s_cst[grp], s_mrg + JJ * 256, lane, mu, s_ba.kp);
                     });
                 }
                 par ^= 1u;
@@ -1976,11 +1773,12 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
             }
             if (active) {
                 uint32_t *out_q = s_ba.resp + s_ba.resp_off[qo] + (size_t)k * s_ba.wpp;
-                if (g < 32) c0_write_results<N>(s_ba, out_q, s_ybuf[grp] + (par ^ 1u) * T, g, mu);
+                if (g / 32 == TAIL_WARP) c0_write_results<N>(s_ba, out_q, s_ybuf[grp] + (par ^ 1u) * T, lane, mu);
                 write_component<N, FMT>(s_ba, out_q, a[0], 1, g, s_rmap);
             }
         }
         seq = seq0 + nchunks;
+        pre_issued = (nchunks + NSLOT - 1 > nchunks) ? min(NSLOT - 1, dn.nchunks) : 0u;   // thread 0 only
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -2044,10 +1842,7 @@ static cudaError_t launch_eval_nl(const BatchArgs &a, cudaStream_t s, int num_sm
         eval_kernel_grp<N, L><<<num_sms * blocks_per_sm, kEvalGroups * Gm::T, smem, s>>>(a);
     } else {
         if constexpr (N == 8192 && WALLY_EVAL_TMEM) {
-            if (pruned_c0_path(N, L, a.d, a.compact)) {
-                if (WALLY_P8_V == 5) return launch_eval_p8t<L, (int)WALLY_RESP_COMPACT>(a, s, num_sms);
-                return launch_eval_p8<L, (int)WALLY_RESP_COMPACT>(a, s, num_sms);
-            }
+            if (pruned_c0_path(N, L, a.d, a.compact)) return launch_eval_p8t<L, (int)WALLY_RESP_COMPACT>(a, s, num_sms);
         }
         const size_t smem = chain_smem<N>(EvalCfg<N>::NC);
         cudaError_t e = device_once(once, [&](int *v) {

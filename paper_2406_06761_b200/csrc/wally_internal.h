@@ -21,6 +21,15 @@ constexpr int kMaxLimbs = WALLY_MAX_LIMBS;
 #define WALLY_QUERY_CHUNK 32
 #endif
 constexpr uint32_t kQueryChunk = WALLY_QUERY_CHUNK;
+// Queries per work item of the n = 8192 kernel v5: its work items are short
+// (a query chunk x two plaintexts) and consecutive items share the query
+// chunk, so the SMs working at one time read each plaintext pair for
+// different queries at nearly the same time (L2 hits instead of re-reads
+// from DRAM); the operand stream runs on across items.
+#ifndef WALLY_P8_CHUNK
+#define WALLY_P8_CHUNK 1
+#endif
+constexpr uint32_t kP8QueryChunk = WALLY_P8_CHUNK;
 
 // Per-limb constants, passed by value to every kernel (kernel parameter
 // space -> constant bank, uniform across the grid).
@@ -105,19 +114,12 @@ inline bool pruned_c0_path(uint32_t n, uint32_t L, uint32_t d, bool compact) {
     return false;
 }
 
-// The n = 8192 pruned-c0 fused kernel: v3 (register prefetch, two CTAs per
-// SM) or v5 (bulk-copy staging, two groups per CTA on two plaintexts of one
-// work item; kernels.cu).
-#ifndef WALLY_P8_V
-#define WALLY_P8_V 5
-#endif
-
 // Plaintexts per work item of the fused kernel a batch runs: 2 for the v5
 // n = 8192 kernel (its two thread groups take plaintexts k and k + 1 of the
 // item's cluster for the same queries), 1 otherwise.  Shared by the batcher
 // (item count) and the kernel (item decode).
 inline uint32_t eval_plaintexts_per_item(uint32_t n, uint32_t L, uint32_t d, bool compact) {
-    return (n == 8192 && WALLY_P8_V == 5 && pruned_c0_path(n, L, d, compact)) ? 2u : 1u;
+    return (n == 8192 && pruned_c0_path(n, L, d, compact)) ? 2u : 1u;
 }
 
 // Algorithmic modular multiplications per (query, plaintext) pair of the
