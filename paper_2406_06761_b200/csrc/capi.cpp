@@ -574,6 +574,8 @@ static int eval_impl(wally_ctx *c, uint32_t nq, const uint32_t *ids, const uint3
     a.seg = (uint32_t *)(ws + w.seg);
     a.item_start = (uint32_t *)(ws + w.item_start);
     a.chat = (uint32_t *)(ws + w.chat);
+    a.resp_words = resp_words;
+    a.store_words = (uint64_t)c->npt * c->p.num_limbs * 2 * c->p.n;
     std::array<cudaEvent_t, 4> ev{};
     if (c->timing) {
         for (auto &e : ev) {

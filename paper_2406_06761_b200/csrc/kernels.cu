@@ -26,6 +26,28 @@
 
 namespace wally {
 
+// Debug builds (WALLY_BOUNDS_CHECK=1): trap with the call site when an access
+// of the v4 fused kernel leaves its buffer (round-2 investigation of the
+// L = 2 tensor-memory-state fault).
+#ifndef WALLY_BOUNDS_CHECK
+#define WALLY_BOUNDS_CHECK 0
+#endif
+#if WALLY_BOUNDS_CHECK
+#define WALLY_BC(ptr, base, words, tag)                                                                         \
+    do {                                                                                                        \
+        const uint32_t *p_ = (const uint32_t *)(ptr);                                                           \
+        if (p_ < (const uint32_t *)(base) || p_ + 1 > (const uint32_t *)(base) + (words)) {                     \
+            printf("WALLY_BC %s: block %d thread %d offset %lld of %llu\n", tag, blockIdx.x, threadIdx.x,          \
+                   (long long)(p_ - (const uint32_t *)(base)), (unsigned long long)(words));                     \
+            __trap();                                                                                           \
+        }                                                                                                       \
+    } while (0)
+#else
+#define WALLY_BC(ptr, base, words, tag) \
+    do {                                  \
+    } while (0)
+#endif
+
 // ---------------------------------------------------------------------------
 // a2: forward NTT of query polynomials (and of any [count][L][n] array)
 // ---------------------------------------------------------------------------
@@ -500,8 +522,10 @@ __device__ __forceinline__ void write_component(const BatchArgs &ba, uint32_t *o
 #pragma unroll
     for (int j = 0; j < V / Gm::R2; j++)
 #pragma unroll
-        for (int kk = 0; kk < Gm::R2; kk++)
+        for (int kk = 0; kk < Gm::R2; kk++) {
+            WALLY_BC((dst + pass_index<N, Gm::TB2, Gm::R2>(g, j, kk)), ba.resp, ba.resp_words, "full store");
             __stcs(dst + pass_index<N, Gm::TB2, Gm::R2>(g, j, kk), a[j * Gm::R2 + kk]);
+        }
 }
 
 // Evaluate work item `item` (cursor already positioned) for one thread group.
@@ -655,51 +679,44 @@ struct LimbLoopTM {
 #pragma unroll
             for (int c = 0; c < NC; c++)
 #pragma unroll
-                for (int v = 0; v < V / 4; v++)
+                for (int v = 0; v < V / 4; v++) {
+                    WALLY_BC(nsrc + (size_t)c * L * N + (size_t)g * V + 4 * v + 3, ba.chat, (size_t)ba.nq * 2 * L * N, "tm cpre");
                     cpre[c][v] = ldg_stream(nsrc + (size_t)c * L * N + (size_t)g * V + 4 * v);
+                }
         }
         intt_chain_group<N, NC>(st.a, cx.tw + (size_t)J * Gm::TW_LIMB, g, q, q2, cx.bufA, cx.bar);
         // mod-switch state through TMEM between limbs: L = 3 (its registers are
         // what the chat prefetch needs).  L = 2 keeps its single 16-word state
-        // in registers (round 1: the TMEM variant faulted once on B200;
-        // WALLY_TM_L2_TMEM = 1 builds it again for that investigation).
+        // in registers: the TMEM variant (WALLY_TM_L2_TMEM = 1) raises an
+        // illegal-address fault on the B200 (scripts/tm_l2_repro.py; the
+        // investigation is in DESIGN.md section 14).
 #ifndef WALLY_TM_L2_TMEM
 #define WALLY_TM_L2_TMEM 0
 #endif
-#ifndef WALLY_TM_SYNC_LD
-#define WALLY_TM_SYNC_LD 0
-#endif
+        constexpr uint32_t TM_STATE_COL = 96;
         if constexpr (L == 3 || (L == 2 && WALLY_TM_L2_TMEM)) {
             if constexpr (J < L - 1) {
                 // state written at limb J + 1: rtop (J == L - 2) or acc (J < L - 2)
                 tmem_wait_st_all();
-#if WALLY_TM_SYNC_LD
 #pragma unroll
                 for (int c = 0; c < NC; c++) {
-                    if constexpr (J == L - 2) tmem_ld_sync16(tcol + 96 + 16 * c, st.rtop[c]);
-                    else tmem_ld_sync16(tcol + 96 + 16 * c, st.acc[c][0]);
-                }
-#else
-#pragma unroll
-                for (int c = 0; c < NC; c++) {
-                    if constexpr (J == L - 2) tmem_ld<16>(tcol + 96 + 16 * c, st.rtop[c]);
-                    else tmem_ld<16>(tcol + 96 + 16 * c, st.acc[c][0]);
+                    if constexpr (J == L - 2) tmem_ld<16>(tcol + TM_STATE_COL + 16 * c, st.rtop[c]);
+                    else tmem_ld<16>(tcol + TM_STATE_COL + 16 * c, st.acc[c][0]);
                 }
 #pragma unroll
                 for (int c = 0; c < NC; c++) {
                     if constexpr (J == L - 2) tmem_wait_ld<16>(st.rtop[c]);
                     else tmem_wait_ld<16>(st.acc[c][0]);
                 }
-#endif
             }
 #pragma unroll
             for (int c = 0; c < NC; c++) ms_step<L, J, V>(st.a[c], st.rtop[c], st.acc[c], ba.kp);
             if constexpr (J == L - 1) {
 #pragma unroll
-                for (int c = 0; c < NC; c++) tmem_st<16>(tcol + 96 + 16 * c, st.rtop[c]);
+                for (int c = 0; c < NC; c++) tmem_st<16>(tcol + TM_STATE_COL + 16 * c, st.rtop[c]);
             } else if constexpr (J > 0) {
 #pragma unroll
-                for (int c = 0; c < NC; c++) tmem_st<16>(tcol + 96 + 16 * c, st.acc[c][0]);
+                for (int c = 0; c < NC; c++) tmem_st<16>(tcol + TM_STATE_COL + 16 * c, st.acc[c][0]);
             }
         } else {
 #pragma unroll
@@ -734,6 +751,7 @@ __device__ __forceinline__ void eval_item_tm(const BatchArgs &ba, const ItemCurs
         const uint32_t *pv = phat + (size_t)J * 2 * N + (size_t)g * V;
 #pragma unroll
         for (int v = 0; v < 4; v++) {
+            WALLY_BC(pv + N + 4 * v + 3, ba.store, ba.store_words, "tm plaintext");
             const uint4 x = ldg_stream(pv + 4 * v), y = ldg_stream(pv + N + 4 * v);
             p[4 * v] = x.x; p[4 * v + 1] = x.y; p[4 * v + 2] = x.z; p[4 * v + 3] = x.w;
             pp[4 * v] = y.x; pp[4 * v + 1] = y.y; pp[4 * v + 2] = y.z; pp[4 * v + 3] = y.w;
@@ -747,9 +765,12 @@ __device__ __forceinline__ void eval_item_tm(const BatchArgs &ba, const ItemCurs
     {
         const uint32_t *src = ba.chat + (size_t)qo * 2 * L * N + (size_t)(L - 1) * N;
 #pragma unroll
-        for (int c = 0; c < NC; c++)
+        for (int c = 0; c < NC; c++) {
+#pragma unroll
+            for (int v = 0; v < V / 4; v++) WALLY_BC(src + (size_t)c * L * N + (size_t)g * V + 4 * v + 3, ba.chat, (size_t)ba.nq * 2 * L * N, "tm cpre0");
 #pragma unroll
             for (int v = 0; v < V / 4; v++) cpre[c][v] = ldg_stream(src + (size_t)c * L * N + (size_t)g * V + 4 * v);
+        }
     }
     for (uint32_t qi = qb; qi < qe; qi++) {
         const uint32_t qn = (qi + 1 < qe) ? ba.perm[qi + 1] : 0xffffffffu;
@@ -771,6 +792,7 @@ __device__ __forceinline__ void eval_item_tm(const BatchArgs &ba, const ItemCurs
                 const uint32_t *np = ba.store + (size_t)(ba.pt_base[nli] + nk) * L * 2 * N + (size_t)g * V;
 #pragma unroll
                 for (int J = 0; J < L; J++) {
+                    WALLY_BC(np + (size_t)J * 2 * N + N, ba.store, ba.store_words, "tm L2 prefetch");
                     asm volatile("prefetch.global.L2 [%0];" ::"l"(np + (size_t)J * 2 * N));
                     asm volatile("prefetch.global.L2 [%0];" ::"l"(np + (size_t)J * 2 * N + N));
                 }

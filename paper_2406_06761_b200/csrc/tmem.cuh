@@ -107,17 +107,5 @@ __device__ __forceinline__ void tmem_wait_ld<32>(uint32_t (&r)[32]) {
 
 __device__ __forceinline__ void tmem_wait_st_all() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// Load and wait in ONE asm statement: the destination registers are written
-// asynchronously by tcgen05.ld, so between a separate ld and wait the
-// compiler must not touch them -- a single statement makes that structural.
-__device__ __forceinline__ void tmem_ld_sync16(uint32_t taddr, uint32_t (&r)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-        "tcgen05.wait::ld.sync.aligned;"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr)
-        : "memory");
-}
 
 }  // namespace wally

@@ -87,6 +87,7 @@ struct BatchArgs {
     uint32_t *seg;
     uint32_t *item_start;
     uint32_t *chat;               // [nq][2][L][n]
+    uint64_t resp_words, store_words;   // buffer sizes (bounds checks of WALLY_BOUNDS_CHECK builds)
 };
 
 struct EncodeArgs {
