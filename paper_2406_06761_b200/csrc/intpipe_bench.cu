@@ -90,6 +90,61 @@ __global__ void __launch_bounds__(1024) bench_kernel(uint32_t iters, uint32_t a,
     }
 }
 
+// FP64 pipe (round 2: could a second, double-precision modular multiplier
+// run beside the IMAD pipe?):
+//   10 dfma      x = fma(x, a, b)                    (DFMA)
+//   11 cvt       x = (double)(uint32)x round trip     (F2I.F64 + I2F.F64)
+//   12 fp64_mod  exact x * w mod q in doubles: h = x w, l = fma(x, w, -h),
+//                t = rint(h / q), r = fma(-t, q, h) + l   (6 FP64 ops)
+//   13 mixed     one Shoup modmul (IMAD pipe) and one fp64_mod per step, independent
+template <int OP>
+__global__ void __launch_bounds__(1024) fp64_kernel(uint32_t iters, uint32_t a, uint32_t b, uint32_t q,
+                                                    uint32_t *sink, unsigned long long *rec) {
+    double x[CHAINS];
+    uint32_t u[CHAINS];
+#pragma unroll
+    for (int c = 0; c < CHAINS; c++) {
+        u[c] = (threadIdx.x * 7919u + c * 104729u + blockIdx.x) % q;
+        x[c] = (double)u[c];
+    }
+    const double ad = (double)a, bd = (double)b, qd = (double)q, qinv = 1.0 / (double)q;
+    const uint32_t wp = (uint32_t)(((uint64_t)a << 32) / q);
+    __syncthreads();
+    const long long t0 = clock64();
+    const uint64_t g0 = gtimer();
+    for (uint32_t i = 0; i < iters; i++) {
+#pragma unroll
+        for (int rep = 0; rep < REP; rep++)
+#pragma unroll
+        for (int c = 0; c < CHAINS; c++) {
+            if (OP == 10) asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(x[c]) : "d"(ad), "d"(bd));
+            if (OP == 11) {
+                uint32_t t;
+                asm volatile("cvt.rzi.u32.f64 %0, %1;" : "=r"(t) : "d"(x[c]));
+                asm volatile("cvt.rn.f64.u32 %0, %1;" : "=d"(x[c]) : "r"(t + 1u));
+            }
+            if (OP == 12 || OP == 13) {
+                const double h = x[c] * ad;
+                const double l = fma(x[c], ad, -h);
+                const double t = rint(h * qinv);
+                x[c] = fma(-t, qd, h) + l;
+            }
+            if (OP == 13) u[c] = shoup_mul(u[c], a, wp, q);
+        }
+    }
+    __syncthreads();
+    const long long t1 = clock64();
+    const uint64_t g1 = gtimer();
+    uint32_t s = 0;
+#pragma unroll
+    for (int c = 0; c < CHAINS; c++) s ^= (uint32_t)(int64_t)x[c] ^ u[c];
+    if (s == 0x12345678u) sink[0] = s;
+    if (threadIdx.x == 0) {
+        rec[2 * blockIdx.x] = (unsigned long long)(t1 - t0);
+        rec[2 * blockIdx.x + 1] = (unsigned long long)(g1 - g0);
+    }
+}
+
 // TMEM read bandwidth: 512 threads (16 warps), one CTA per SM, 512 columns
 // allocated; warp w reads its lane quadrant (w % 4), columns (w / 4) * 128 + ...
 __global__ void __launch_bounds__(512, 1) tmem_kernel(uint32_t iters, uint32_t *sink, unsigned long long *rec) {
@@ -161,10 +216,17 @@ static void report(const char *name, double ops_per_block, int blocks, int block
 }
 
 template <int OP>
+static auto kernel_of() {
+    if constexpr (OP >= 10) return fp64_kernel<OP>;
+    else return bench_kernel<OP>;
+}
+
+template <int OP>
 static void run(const char *name, int num_sms, int ops_per_step = 1) {
     const int threads = 1024;
     int bps = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, bench_kernel<OP>, threads, 0);
+    auto kern = kernel_of<OP>();
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, threads, 0);
     if (bps < 1) bps = 1;
     const int blocks = num_sms * bps;
     const uint32_t iters = g_iters;
@@ -173,12 +235,12 @@ static void run(const char *name, int num_sms, int ops_per_step = 1) {
     cudaMalloc(&sink, 4);
     cudaMalloc(&rec, sizeof(unsigned long long) * 2 * blocks);
     const uint32_t q = 1073651713u, a = 123456789u, b = 987654321u;
-    bench_kernel<OP><<<blocks, threads>>>(1024, a, b, q, sink, rec);  // warm-up
+    kern<<<blocks, threads>>>(1024, a, b, q, sink, rec);  // warm-up
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    bench_kernel<OP><<<blocks, threads>>>(iters, a, b, q, sink, rec);
+    kern<<<blocks, threads>>>(iters, a, b, q, sink, rec);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms = 0;
@@ -228,6 +290,10 @@ int main(int argc, char **argv) {
     run<5>("imad_hi_plus_imad_1to1", num_sms, 2);
     run<6>("imad_plus_iadd3_1to1", num_sms, 2);
     run<7>("imad_wide_plus_lop3", num_sms, 1);
+    run<10>("dfma", num_sms);
+    run<11>("cvt_f64_u32_round_trip", num_sms);
+    run<12>("fp64_modmul", num_sms);
+    run<13>("shoup_plus_fp64_modmul_1to1", num_sms, 2);
     run_tmem(num_sms);
     return 0;
 }
