@@ -786,7 +786,11 @@ def main():
     import torch
     import torch.distributed as dist
     if args.dry_run:
-        if world > 1:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(_free_port()))
+            dist.init_process_group("gloo", rank=0, world_size=1)
+        else:
             dist.init_process_group("gloo")
         out = run_dry(args, rank, world)
     else:
@@ -798,7 +802,7 @@ def main():
                                                                                             local_rank)
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
 
