@@ -181,6 +181,7 @@ extern "C" void wally_destroy(wally_ctx *c) {
     cudaFree(c->d_tw_fwd);
     cudaFree(c->d_tw_inv);
     cudaFree(c->d_tw_mrg);
+    cudaFree(c->d_tw_slot);
     cudaFree(c->d_local_of_cluster);
     cudaFree(c->d_pt_base);
     cudaFree(c->d_n_pt);
@@ -260,6 +261,11 @@ extern "C" int wally_create(const wally_params *pp, int device, wally_ctx **out)
         kp.h[l] = (uint32_t)(q / 2);
         kp.ninv[l] = (uint32_t)invm(n, q);
         kp.ninvp[l] = shoup_companion(kp.ninv[l], (uint32_t)q);
+        {   // -q^{-1} mod 2^32 by Newton iteration (q odd: x = q is q^{-1} mod 2^3)
+            uint32_t x = (uint32_t)q;
+            for (int it = 0; it < 5; it++) x *= 2u - (uint32_t)q * x;
+            kp.mqinv[l] = 0u - x;
+        }
         // fold F_l = n^{-1} prod_{k>l} q_k^{-1} mod q_l
         uint64_t f = invm(n, q);
         for (uint32_t k = l + 1; k < L; k++) f = mulm(f, invm(p.moduli[k] % q, q), q);
@@ -293,6 +299,15 @@ extern "C" int wally_create(const wally_params *pp, int device, wally_ctx **out)
     cudaMemcpy(c->d_tw_fwd, twf.data(), tb, cudaMemcpyHostToDevice);
     cudaMemcpy(c->d_tw_inv, twi.data(), tb, cudaMemcpyHostToDevice);
     cudaMemcpy(c->d_tw_mrg, twm.data(), sizeof(uint2) * twm.size(), cudaMemcpyHostToDevice);
+    if (n == 8192) {
+        std::vector<uint2> tws((size_t)L * kP8tSlotTwEntries);
+        p8t_slot_twiddles(twi.data(), L, tw_limb, tws.data());
+        if (cudaMalloc(&c->d_tw_slot, sizeof(uint2) * tws.size()) != cudaSuccess) {
+            wally_destroy(c);
+            return fail(nullptr, WALLY_E_OOM, "twiddle table allocation failed");
+        }
+        cudaMemcpy(c->d_tw_slot, tws.data(), sizeof(uint2) * tws.size(), cudaMemcpyHostToDevice);
+    }
     for (auto &s : c->slot) cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming);
     cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
     if (cudaGetLastError() != cudaSuccess) {
@@ -559,6 +574,7 @@ static int eval_impl(wally_ctx *c, uint32_t nq, const uint32_t *ids, const uint3
     a.tw_fwd = c->d_tw_fwd;
     a.tw_inv = c->d_tw_inv;
     a.tw_mrg = c->d_tw_mrg;
+    a.tw_slot = c->d_tw_slot;
     a.local_of_cluster = c->d_local_of_cluster;
     a.pt_base = c->d_pt_base;
     a.n_pt = c->d_n_pt;

@@ -51,7 +51,24 @@ namespace wally {
 // ---------------------------------------------------------------------------
 // a2: forward NTT of query polynomials (and of any [count][L][n] array)
 // ---------------------------------------------------------------------------
+// Query-NTT storage in the batch workspace (chat, [nq][2][L][n] words): at
+// n = 8192 the two components of a limb are interleaved by 16-byte chunk --
+// chunk v of component c of limb J at ((J * 8 + v) * 2 + c) * 4T (+ 4g + i,
+// ntt_word's chunk-major order) -- so one bulk copy stages both chunks a ring
+// slot of the v5 kernel needs; otherwise (c L + J) n + ntt_word.
 template <int N>
+__host__ __device__ constexpr size_t chat_word(uint32_t L, int comp, int J, int g, int v) {
+    if constexpr (N == 8192) {
+        constexpr int T = NttGeom<N>::T, CH = NttGeom<N>::V / 4;
+        return (((size_t)J * CH + v) * 2 + comp) * 4 * T + 4 * (size_t)g;
+    } else {
+        return ((size_t)comp * L + J) * N + ntt_word<N>(g, v);
+    }
+}
+
+// CHAT: write the query-NTT workspace order (chat_word) instead of one
+// polynomial after another (ntt_word).
+template <int N, bool CHAT>
 __global__ void __launch_bounds__(NttGeom<N>::T) ntt_forward_kernel(KParams kp, uint32_t L, const uint2 *__restrict__ tw,
                                                                     const uint32_t *__restrict__ in,
                                                                     uint32_t *__restrict__ out, uint32_t *err) {
@@ -77,11 +94,20 @@ __global__ void __launch_bounds__(NttGeom<N>::T) ntt_forward_kernel(KParams kp, 
         }
     if (bad && err) atomicOr(err, (uint32_t)kErrResidue);
     ntt_chain<N, 1>(a, tw + (size_t)limb * Gm::TW_LIMB, g, q, q2, bufA, bufB);
-    uint32_t *dst = out + poly * N;
+    if constexpr (CHAT) {
+        const uint32_t comp = (uint32_t)((poly / L) % 2);
+        uint32_t *dst = out + (poly / (2 * L)) * 2 * L * N;
 #pragma unroll
-    for (int v = 0; v < V / 4; v++)
-        *reinterpret_cast<uint4 *>(dst + ntt_word<N>(g, v)) =
-            make_uint4(a[0][4 * v], a[0][4 * v + 1], a[0][4 * v + 2], a[0][4 * v + 3]);
+        for (int v = 0; v < V / 4; v++)
+            *reinterpret_cast<uint4 *>(dst + chat_word<N>(L, comp, limb, g, v)) =
+                make_uint4(a[0][4 * v], a[0][4 * v + 1], a[0][4 * v + 2], a[0][4 * v + 3]);
+    } else {
+        uint32_t *dst = out + poly * N;
+#pragma unroll
+        for (int v = 0; v < V / 4; v++)
+            *reinterpret_cast<uint4 *>(dst + ntt_word<N>(g, v)) =
+                make_uint4(a[0][4 * v], a[0][4 * v + 1], a[0][4 * v + 2], a[0][4 * v + 3]);
+    }
 }
 
 // Debug/test inverse NTT: out = n^{-1} INTT(in), canonical.
@@ -154,7 +180,10 @@ __global__ void __launch_bounds__(NttGeom<N>::T) encode_kernel(EncodeArgs ea) {
 #pragma unroll
         for (int i = 0; i < 4; i++) {
             y[i] = csub(shoup_mul(a[0][4 * v + i], ea.kp.fold[limb], ea.kp.foldp[limb], q), q);  // canonical
-            yp[i] = (uint32_t)(((uint64_t)y[i] << 32) / q);                                    // Shoup companion
+            if constexpr (PtStore<N>::MONT)
+                yp[i] = (uint32_t)(((uint64_t)y[i] << 32) % q);                                // Montgomery form
+            else
+                yp[i] = (uint32_t)(((uint64_t)y[i] << 32) / q);                                // Shoup companion
         }
         *reinterpret_cast<uint4 *>(dst + ntt_word<N>(g, v)) = make_uint4(y[0], y[1], y[2], y[3]);
         *reinterpret_cast<uint4 *>(dst + N + ntt_word<N>(g, v)) = make_uint4(yp[0], yp[1], yp[2], yp[3]);
@@ -363,14 +392,27 @@ __device__ __forceinline__ void eval_limb(EvalState<N, L, NC> &st, const BatchAr
     const uint32_t *pv = phat + (size_t)J * 2 * N;
 #pragma unroll
     for (int v = 0; v < V / 4; v++) {
-        const uint4 p = ldg_stream(pv + ntt_word<N>(g, v)), pp = ldg_stream(pv + N + ntt_word<N>(g, v));
+        if constexpr (PtStore<N>::MONT) {
+            const uint32_t qi = ba.kp.mqinv[J];
+            const uint4 pm = ldg_stream(pv + N + ntt_word<N>(g, v));
 #pragma unroll
-        for (int c = 0; c < NC; c++) {
-            const uint4 x = ldg_stream(chat_q + ((size_t)(comp0 + c) * L + J) * N + ntt_word<N>(g, v));
-            st.a[c][4 * v + 0] = shoup_mul(x.x, p.x, pp.x, q);
-            st.a[c][4 * v + 1] = shoup_mul(x.y, p.y, pp.y, q);
-            st.a[c][4 * v + 2] = shoup_mul(x.z, p.z, pp.z, q);
-            st.a[c][4 * v + 3] = shoup_mul(x.w, p.w, pp.w, q);
+            for (int c = 0; c < NC; c++) {
+                const uint4 x = ldg_stream(chat_q + chat_word<N>(L, comp0 + c, J, g, v));
+                st.a[c][4 * v + 0] = mont_mul(x.x, pm.x, q, qi);
+                st.a[c][4 * v + 1] = mont_mul(x.y, pm.y, q, qi);
+                st.a[c][4 * v + 2] = mont_mul(x.z, pm.z, q, qi);
+                st.a[c][4 * v + 3] = mont_mul(x.w, pm.w, q, qi);
+            }
+        } else {
+            const uint4 p = ldg_stream(pv + ntt_word<N>(g, v)), pp = ldg_stream(pv + N + ntt_word<N>(g, v));
+#pragma unroll
+            for (int c = 0; c < NC; c++) {
+                const uint4 x = ldg_stream(chat_q + chat_word<N>(L, comp0 + c, J, g, v));
+                st.a[c][4 * v + 0] = shoup_mul(x.x, p.x, pp.x, q);
+                st.a[c][4 * v + 1] = shoup_mul(x.y, p.y, pp.y, q);
+                st.a[c][4 * v + 2] = shoup_mul(x.z, p.z, pp.z, q);
+                st.a[c][4 * v + 3] = shoup_mul(x.w, p.w, pp.w, q);
+            }
         }
     }
     if constexpr (GRP)
@@ -885,22 +927,29 @@ cudaError_t launch_encode(const EncodeArgs &a, cudaStream_t s, uint64_t *launche
 
 template <int N>
 static cudaError_t launch_fwd_n(const KParams &kp, uint32_t L, const uint2 *tw, const uint32_t *in, uint32_t *out,
-                                uint32_t count, uint32_t *err, cudaStream_t s) {
-    cudaError_t e = allow_smem(ntt_forward_kernel<N>, chain_smem<N>());
-    if (e != cudaSuccess) return e;
-    ntt_forward_kernel<N><<<(unsigned)(count * L), NttGeom<N>::T, chain_smem<N>(), s>>>(kp, L, tw, in, out, err);
+                                uint32_t count, uint32_t *err, cudaStream_t s, bool chat) {
+    if (chat) {
+        cudaError_t e = allow_smem(ntt_forward_kernel<N, true>, chain_smem<N>());
+        if (e != cudaSuccess) return e;
+        ntt_forward_kernel<N, true><<<(unsigned)(count * L), NttGeom<N>::T, chain_smem<N>(), s>>>(kp, L, tw, in, out, err);
+    } else {
+        cudaError_t e = allow_smem(ntt_forward_kernel<N, false>, chain_smem<N>());
+        if (e != cudaSuccess) return e;
+        ntt_forward_kernel<N, false><<<(unsigned)(count * L), NttGeom<N>::T, chain_smem<N>(), s>>>(kp, L, tw, in, out, err);
+    }
     return cudaGetLastError();
 }
 
 cudaError_t launch_ntt_forward(const KParams &kp, uint32_t n, uint32_t L, const uint2 *tw_fwd, const uint32_t *in,
-                               uint32_t *out, uint32_t count, uint32_t *err, cudaStream_t s, uint64_t *launches) {
+                               uint32_t *out, uint32_t count, uint32_t *err, cudaStream_t s, uint64_t *launches,
+                               bool chat) {
     if (count == 0) return cudaSuccess;
     *launches += 1;
     switch (n) {
-        case 1024: return launch_fwd_n<1024>(kp, L, tw_fwd, in, out, count, err, s);
-        case 2048: return launch_fwd_n<2048>(kp, L, tw_fwd, in, out, count, err, s);
-        case 4096: return launch_fwd_n<4096>(kp, L, tw_fwd, in, out, count, err, s);
-        case 8192: return launch_fwd_n<8192>(kp, L, tw_fwd, in, out, count, err, s);
+        case 1024: return launch_fwd_n<1024>(kp, L, tw_fwd, in, out, count, err, s, chat);
+        case 2048: return launch_fwd_n<2048>(kp, L, tw_fwd, in, out, count, err, s, chat);
+        case 4096: return launch_fwd_n<4096>(kp, L, tw_fwd, in, out, count, err, s, chat);
+        case 8192: return launch_fwd_n<8192>(kp, L, tw_fwd, in, out, count, err, s, chat);
     }
     return cudaErrorInvalidValue;
 }
@@ -1453,8 +1502,10 @@ __device__ __forceinline__ void c0_tail_fast8(uint32_t *z, uint32_t *cst, const 
 // The operands of one (query, limb) stream through a ring of NSLOT shared-
 // memory slots, one per 4-value chunk c of every thread (chunk-major
 // NTT-domain storage, ntt_word: chunk c of all threads is one 4 KB block):
-//   [p, p' of k0][p, p' of k1][pass-0 stage-0 twiddle block c]
-//   [pass-0 twiddle block B(c)][c0 chunk][c1 chunk]          (32 KB per slot)
+//   [y 2^32 of k0][y 2^32 of k1][pass-0 stage-0 twiddle block c]
+//   [pass-0 twiddle block B(c)][c0 chunk][c1 chunk]          (24 KB per slot)
+// (the plaintext's Montgomery plane only, PtStore: the pointwise products are
+// Montgomery products, so no Shoup companion is staged)
 // B(c) = 8, 12, 9, 14, 10, 13, 11, 15 delivers each later-stage twiddle block
 // with the first chunk that needs it (a thread keeps the half it needs again
 // in a register).  A producer thread (thread 0) keeps the ring NSLOT - 1
@@ -1469,9 +1520,12 @@ __device__ __forceinline__ void c0_tail_fast8(uint32_t *z, uint32_t *cst, const 
 namespace p8t {
 constexpr int N = 8192;
 constexpr int T = NttGeom<N>::T;                 // 256 threads per group
-constexpr int NSLOT = 4;
+#ifndef WALLY_P8T_NSLOT
+#define WALLY_P8T_NSLOT 4
+#endif
+constexpr int NSLOT = WALLY_P8T_NSLOT;
 constexpr int CHUNK_BYTES = T * 16;              // one 16-byte chunk of every thread: 4 KB
-constexpr int SLOT_BYTES = 8 * CHUNK_BYTES;      // 2 x (p, p'), 2 twiddle blocks, c0, c1
+constexpr int SLOT_BYTES = 6 * CHUNK_BYTES;      // 2 Montgomery plaintext chunks, 2 twiddle blocks, c0, c1
 constexpr int TW12 = NttGeom<N>::TW_LIMB - NttGeom<N>::TW1;   // pass-1/2 table entries per limb
 constexpr int XB_WORDS = NttGeom<N>::SMEM_WORDS;
 __host__ __device__ constexpr size_t smem_bytes(int L) {
@@ -1482,6 +1536,18 @@ __host__ __device__ constexpr int aux_block(int c) {
     return c == 0 ? 8 : c == 1 ? 12 : c == 2 ? 9 : c == 3 ? 14 : c == 4 ? 10 : c == 5 ? 13 : c == 6 ? 11 : 15;
 }
 }  // namespace p8t
+
+void p8t_slot_twiddles(const uint2 *twi, uint32_t L, size_t tw_limb, uint2 *out) {
+    using namespace p8t;
+    static_assert(kP8tSlotTwEntries == (size_t)8 * 2 * T * 2, "slot twiddle table size");
+    for (uint32_t J = 0; J < L; J++)
+        for (int c = 0; c < 8; c++)
+            for (int h = 0; h < 2; h++) {
+                const int blk = h ? aux_block(c) : c;   // uint4 block of T entries = 2 T uint2 entries
+                const uint2 *src = twi + (size_t)J * tw_limb + (size_t)blk * 2 * T;
+                std::copy(src, src + 2 * T, out + (size_t)J * kP8tSlotTwEntries + ((size_t)c * 2 + h) * 2 * T);
+            }
+}
 
 __device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
@@ -1663,20 +1729,18 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
     auto produce = [&](const Desc &d, uint32_t j, uint32_t sq) {
         const uint32_t sl = sq % NSLOT;
         if (sq >= NSLOT) mbar_wait(empty_b(sl), ((sq / NSLOT) + 1) & 1u);
-        mbar_expect_tx(full_b(sl), (4 + 2 * d.np) * CHUNK_BYTES);
+        mbar_expect_tx(full_b(sl), (4 + d.np) * CHUNK_BYTES);
         const uint32_t r = j / (L * CHUNKS), J = L - 1 - (j / CHUNKS) % L, c = j % CHUNKS;
         const uint32_t dst = slots_s + sl * SLOT_BYTES;
+        static_assert(PtStore<N>::MONT, "v5 stages the Montgomery plane of the plaintext store only");
         for (uint32_t u = 0; u < d.np; u++) {
-            const uint32_t *pj = d.phat0 + ((size_t)u * L + J) * 2 * N + (size_t)c * 4 * T;
-            bulk_g2s(dst + (2 * u) * CHUNK_BYTES, pj, CHUNK_BYTES, full_b(sl));
-            bulk_g2s(dst + (2 * u + 1) * CHUNK_BYTES, pj + N, CHUNK_BYTES, full_b(sl));
+            const uint32_t *pj = d.phat0 + ((size_t)u * L + J) * 2 * N + N + (size_t)c * 4 * T;
+            bulk_g2s(dst + u * CHUNK_BYTES, pj, CHUNK_BYTES, full_b(sl));
         }
-        const uint4 *twJ = reinterpret_cast<const uint4 *>(s_ba.tw_inv + (size_t)J * Gm::TW_LIMB);
-        bulk_g2s(dst + 4 * CHUNK_BYTES, twJ + c * T, CHUNK_BYTES, full_b(sl));
-        bulk_g2s(dst + 5 * CHUNK_BYTES, twJ + aux_block(c) * T, CHUNK_BYTES, full_b(sl));
-        const uint32_t *cq = s_ba.chat + (size_t)s_ba.perm[d.qb + r] * 2 * L * N + (size_t)c * 4 * T;
-        bulk_g2s(dst + 6 * CHUNK_BYTES, cq + (size_t)J * N, CHUNK_BYTES, full_b(sl));
-        bulk_g2s(dst + 7 * CHUNK_BYTES, cq + ((size_t)L + J) * N, CHUNK_BYTES, full_b(sl));
+        bulk_g2s(dst + 2 * CHUNK_BYTES, s_ba.tw_slot + (size_t)J * kP8tSlotTwEntries + (size_t)c * 4 * T,
+                 2 * CHUNK_BYTES, full_b(sl));
+        const uint32_t *cq = s_ba.chat + (size_t)s_ba.perm[d.qb + r] * 2 * L * N;
+        bulk_g2s(dst + 4 * CHUNK_BYTES, cq + chat_word<N>(L, 0, J, 0, c), 2 * CHUNK_BYTES, full_b(sl));   // c0, c1
     };
     uint32_t pre_issued = 0;   // thread 0: elements of the current item issued while the previous one ran
     // items are claimed in blocks of `ib` consecutive ones (thread 0 keeps the current block's end and
@@ -1739,15 +1803,16 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
                     mbar_wait(full_b(sl), (sq / NSLOT) & 1u);
                     const uint4 *sp = reinterpret_cast<const uint4 *>(slots + sl * SLOT_BYTES);
                     if (active) {
-                        const uint4 p = sp[2 * grp * T + g], pp = sp[(2 * grp + 1) * T + g];
-                        const uint4 w0 = sp[4 * T + g], ta = sp[5 * T + g];
-                        const uint4 x0 = sp[6 * T + g], x1 = sp[7 * T + g];
-                        a[0][4 * c + 0] = shoup_mul(x1.x, p.x, pp.x, q);
-                        a[0][4 * c + 1] = shoup_mul(x1.y, p.y, pp.y, q);
-                        a[0][4 * c + 2] = shoup_mul(x1.z, p.z, pp.z, q);
-                        a[0][4 * c + 3] = shoup_mul(x1.w, p.w, pp.w, q);
-                        const uint32_t y0 = shoup_mul(x0.x, p.x, pp.x, q), y1 = shoup_mul(x0.y, p.y, pp.y, q);
-                        const uint32_t y2 = shoup_mul(x0.z, p.z, pp.z, q), y3 = shoup_mul(x0.w, p.w, pp.w, q);
+                        const uint32_t qi = s_ba.kp.mqinv[J];
+                        const uint4 pm = sp[grp * T + g];
+                        const uint4 w0 = sp[2 * T + g], ta = sp[3 * T + g];
+                        const uint4 x0 = sp[4 * T + g], x1 = sp[5 * T + g];
+                        a[0][4 * c + 0] = mont_mul(x1.x, pm.x, q, qi);
+                        a[0][4 * c + 1] = mont_mul(x1.y, pm.y, q, qi);
+                        a[0][4 * c + 2] = mont_mul(x1.z, pm.z, q, qi);
+                        a[0][4 * c + 3] = mont_mul(x1.w, pm.w, q, qi);
+                        const uint32_t y0 = mont_mul(x0.x, pm.x, q, qi), y1 = mont_mul(x0.y, pm.y, q, qi);
+                        const uint32_t y2 = mont_mul(x0.z, pm.z, q, qi), y3 = mont_mul(x0.w, pm.w, q, qi);
                         // pass-0 stages of this chunk: c1 in full, c0 the last Y output of each block
                         const uint2 wa = make_uint2(w0.x, w0.y), wb = make_uint2(w0.z, w0.w);
                         bf(4 * c, 4 * c + 1, wa);
@@ -1966,7 +2031,8 @@ cudaError_t launch_batcher(const BatchArgs &a, cudaStream_t s, uint64_t *launche
 }
 
 cudaError_t launch_query_ntt(const BatchArgs &a, cudaStream_t s, uint64_t *launches) {
-    return launch_ntt_forward(a.kp, a.n, a.L, a.tw_fwd, a.query_ct, a.chat, 2 * a.nq, a.misc + kMiscErr, s, launches);
+    return launch_ntt_forward(a.kp, a.n, a.L, a.tw_fwd, a.query_ct, a.chat, 2 * a.nq, a.misc + kMiscErr, s, launches,
+                              true);
 }
 
 cudaError_t launch_eval(const BatchArgs &a, cudaStream_t s, int num_sms, uint64_t *launches) {

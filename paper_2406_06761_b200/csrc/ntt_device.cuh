@@ -26,6 +26,15 @@ __device__ __forceinline__ uint32_t shoup_mul(uint32_t x, uint32_t w, uint32_t w
     return x * w - hi * q;
 }
 
+// Montgomery multiplication x * ym * 2^-32 mod q (ym = y 2^32 mod q, qi =
+// -q^{-1} mod 2^32): for x < 4q returns x y mod q in [0, 2q), the range of
+// shoup_mul, without a companion operand.  2 IMAD.WIDE + 1 IMAD.
+__device__ __forceinline__ uint32_t mont_mul(uint32_t x, uint32_t ym, uint32_t q, uint32_t qi) {
+    const uint64_t t = (uint64_t)x * ym;                       // < 4 q^2 < 2^62
+    const uint32_t m = (uint32_t)t * qi;
+    return (uint32_t)((t + (uint64_t)m * q) >> 32);           // (t + m q) / 2^32 < 2q
+}
+
 // Gentleman-Sande (inverse) butterfly, Harvey lazy form.
 // In: X, Y in [0, 2q).  Out: X' = X + Y in [0, 2q), Y' = (X - Y) w in [0, 2q).
 __device__ __forceinline__ void gs_bfly(uint32_t &X, uint32_t &Y, uint32_t w, uint32_t wp, uint32_t q, uint32_t q2) {

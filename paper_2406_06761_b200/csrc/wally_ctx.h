@@ -29,6 +29,7 @@ struct wally_ctx {
     wally::KParams kp{};
     uint2 *d_tw_fwd = nullptr, *d_tw_inv = nullptr;
     uint2 *d_tw_mrg = nullptr;  // [L][n] merged inverse table psi^{-brev(i)} (pruned c0 transform)
+    uint2 *d_tw_slot = nullptr; // n = 8192: [L][8][2][T] uint4 pass-0 twiddle blocks in ring-slot order (v5)
     // cluster layout
     bool loaded = false;
     uint32_t total_clusters = 0, n_local = 0, npt = 0, max_pt = 0;

@@ -43,7 +43,17 @@ struct KParams {
     uint32_t foldp[kMaxLimbs];    //   Shoup companion
     uint32_t C[kMaxLimbs][kMaxLimbs];   // C[l][m] = prod_{k=l+1..m} q_k^{-1} mod q_l, l < m
     uint32_t Cp[kMaxLimbs][kMaxLimbs];  //   Shoup companions
+    uint32_t mqinv[kMaxLimbs];    // -q^{-1} mod 2^32 (Montgomery products with the n = 8192 plaintexts)
 };
+
+// Plaintext store planes ([npt][L][2][n] uint32): plane 0 holds the folded
+// NTT-domain value y = NTT(p) F_l (canonical).  Plane 1 holds, at n <= 4096,
+// y's Shoup companion floor(y 2^32 / q) and, at n = 8192, y's Montgomery form
+// y 2^32 mod q: the n = 8192 kernels multiply with one plane only (a
+// Montgomery product, mont_mul), so the v5 kernel stages half the plaintext
+// bytes per chunk.
+template <int N>
+struct PtStore { static constexpr bool MONT = (N == 8192); };
 
 // Workspace layout of one batch (device), offsets in bytes.
 struct WsLayout {
@@ -71,10 +81,11 @@ struct BatchArgs {
     const uint2 *tw_fwd;          // [L][n] (w, w') psi^{brev(i)}
     const uint2 *tw_inv;          // [L] pass-major inverse tables (ntt_device.cuh)
     const uint2 *tw_mrg;          // [L][n] (w, w') psi^{-brev(i)}, plain merged order
+    const uint2 *tw_slot;         // n = 8192: pass-0 twiddle blocks per ring slot (p8t_slot_twiddles)
     const int32_t *local_of_cluster;  // [total_clusters]
     const uint32_t *pt_base;      // [n_local]
     const uint32_t *n_pt;         // [n_local]
-    const uint32_t *store;        // [npt][L][2][n]
+    const uint32_t *store;        // [npt][L][2][n] (planes: PtStore)
     const uint32_t *query_ct;     // [nq][2][L][n]
     uint32_t *resp;
     // workspace pieces
@@ -175,14 +186,23 @@ inline cudaError_t device_once(DeviceOnce &o, F &&f, int *value_out = nullptr) {
     return cudaSuccess;
 }
 
+// n = 8192 kernel v5: the two pass-0 twiddle blocks a ring slot of chunk c
+// carries (block c and the later-stage block B(c)), adjacent so that one bulk
+// copy moves both: out[L][8][2][T] uint4 from the pass-major inverse table twi
+// (host arrays, uint2 entries).
+void p8t_slot_twiddles(const uint2 *twi, uint32_t L, size_t tw_limb, uint2 *out);
+constexpr size_t kP8tSlotTwEntries = 8 * 2 * 256 * 2;   // uint2 entries per limb
+
 // Kernel launchers (kernels.cu).  Each returns the cudaError_t of the launch
 // and adds the number of kernels launched to *launches.
 cudaError_t launch_encode(const EncodeArgs &a, cudaStream_t s, uint64_t *launches);
 cudaError_t launch_batcher(const BatchArgs &a, cudaStream_t s, uint64_t *launches);
 cudaError_t launch_query_ntt(const BatchArgs &a, cudaStream_t s, uint64_t *launches);
 cudaError_t launch_eval(const BatchArgs &a, cudaStream_t s, int num_sms, uint64_t *launches);
+// chat: write the batch workspace's query-NTT order (kernels.cu chat_word) instead of polynomial order
 cudaError_t launch_ntt_forward(const KParams &kp, uint32_t n, uint32_t L, const uint2 *tw_fwd, const uint32_t *in,
-                               uint32_t *out, uint32_t count, uint32_t *err, cudaStream_t s, uint64_t *launches);
+                               uint32_t *out, uint32_t count, uint32_t *err, cudaStream_t s, uint64_t *launches,
+                               bool chat = false);
 cudaError_t launch_pack_rows(const uint32_t *index, const uint32_t *src, uint32_t *dst, uint32_t count,
                              uint32_t row_words, cudaStream_t s, uint64_t *launches);
 cudaError_t launch_ntt_inverse(const KParams &kp, uint32_t n, uint32_t L, const uint2 *tw_inv, const uint32_t *in,
