@@ -149,14 +149,17 @@ int wally_load_clusters(wally_ctx *ctx, uint32_t total_clusters, const uint32_t 
                         const int32_t *owner_host, int32_t rank);
 
 /* Bytes of the device plaintext store for the local clusters:
- * sum_c P_c * L * 2 * n * 4 (NTT-domain values plus Shoup companions). */
+ * n <= 4096: sum_c P_c * L * 2 * n * 4 (NTT-domain values plus Shoup
+ * companions); n = 8192: sum_c P'_c * L * n * 4 with P'_c = P_c rounded up to
+ * even (the values in Montgomery form, plaintexts stored in pairs). */
 int wally_plaintext_store_bytes(const wally_ctx *ctx, size_t *bytes_out);
 /* Number of local entries (rows of the entries array wally_encode_plaintexts_ntt reads). */
 int wally_local_entry_count(const wally_ctx *ctx, uint64_t *count_out);
 
 /* ServerInit, part 2: pack every local plaintext (entries reversed at offsets
  * j*d, reading S1), lift each signed entry x to x mod q_i (S8), forward-NTT
- * per limb and keep the result, with its Shoup companion, in store_dev.
+ * per limb and keep the result, with its Shoup companion (n <= 4096) or in
+ * Montgomery form (n = 8192), in store_dev.
  *   entries_dev  int8 [local_entry_count][d] row-major, local clusters in
  *                ascending cluster-id order, each cluster's entries contiguous
  *   store_dev    device buffer of wally_plaintext_store_bytes bytes; the

@@ -346,12 +346,15 @@ static int load_clusters_impl(wally_ctx *c, uint32_t total_clusters, const uint3
         const uint32_t li = (uint32_t)pt_base.size();
         const uint32_t P = (sizes[cl] + c->E - 1) / c->E;
         local[cl] = (int32_t)li;
+        // store slots: P rounded up to the store's alignment (n = 8192: plaintext pairs; the
+        // pad plaintext k = P encodes no entry, i.e. zero)
+        const uint32_t al = pt_store_align(c->p.n), Ps = (P + al - 1) / al * al;
         pt_base.push_back(npt);
         n_pt.push_back(P);
         size.push_back(sizes[cl]);
         entry_base.push_back(entries);
-        for (uint32_t k = 0; k < P; k++) { pt_li.push_back(li); pt_k.push_back(k); }
-        npt += P;
+        for (uint32_t k = 0; k < Ps; k++) { pt_li.push_back(li); pt_k.push_back(k); }
+        npt += Ps;
         max_pt = std::max(max_pt, P);
         entries += sizes[cl];
     }
@@ -418,7 +421,7 @@ extern "C" int wally_plaintext_store_bytes(const wally_ctx *c, size_t *bytes) {
     WALLY_NVTX("wally_plaintext_store_bytes");
     if (!c || !bytes) return WALLY_E_ARG;
     if (!c->loaded) return fail(const_cast<wally_ctx *>(c), WALLY_E_STATE, "load_clusters first");
-    *bytes = (size_t)c->npt * c->p.num_limbs * 2 * c->p.n * sizeof(uint32_t);
+    *bytes = (size_t)c->npt * c->p.num_limbs * pt_store_planes(c->p.n) * c->p.n * sizeof(uint32_t);
     return WALLY_OK;
 }
 
@@ -591,7 +594,7 @@ static int eval_impl(wally_ctx *c, uint32_t nq, const uint32_t *ids, const uint3
     a.item_start = (uint32_t *)(ws + w.item_start);
     a.chat = (uint32_t *)(ws + w.chat);
     a.resp_words = resp_words;
-    a.store_words = (uint64_t)c->npt * c->p.num_limbs * 2 * c->p.n;
+    a.store_words = (uint64_t)c->npt * c->p.num_limbs * pt_store_planes(c->p.n) * c->p.n;
     std::array<cudaEvent_t, 4> ev{};
     if (c->timing) {
         for (auto &e : ev) {

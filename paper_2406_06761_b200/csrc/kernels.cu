@@ -66,6 +66,14 @@ __host__ __device__ constexpr size_t chat_word(uint32_t L, int comp, int J, int 
     }
 }
 
+// Word of value 4v of thread g (a 16-byte chunk) of plaintext pt, limb J, in
+// the n = 8192 store (PtStore::MONT: pairs interleaved by chunk).
+template <int N>
+__host__ __device__ constexpr size_t pt_mont_word(size_t pt, uint32_t L, int J, int g, int v) {
+    constexpr int T = NttGeom<N>::T, CH = NttGeom<N>::V / 4;
+    return (pt >> 1) * 2 * L * N + (((size_t)J * CH + v) * 2 + (pt & 1)) * 4 * T + 4 * (size_t)g;
+}
+
 // CHAT: write the query-NTT workspace order (chat_word) instead of one
 // polynomial after another (ntt_word).
 template <int N, bool CHAT>
@@ -158,7 +166,7 @@ __global__ void __launch_bounds__(NttGeom<N>::T) encode_kernel(EncodeArgs ea) {
     const uint32_t li = ea.pt_li[pt], k = ea.pt_k[pt];
     const uint32_t first = k * ea.E;  // first entry of this plaintext inside the cluster
     const uint32_t size = ea.size[li];
-    const uint32_t count = min(ea.E, size - first);
+    const uint32_t count = first < size ? min(ea.E, size - first) : 0u;   // 0: pad plaintext (PtStore)
     const int8_t *ent = ea.entries + (ea.entry_base[li] + first) * (uint64_t)ea.d;
     uint32_t a[1][V];
 #pragma unroll
@@ -173,7 +181,6 @@ __global__ void __launch_bounds__(NttGeom<N>::T) encode_kernel(EncodeArgs ea) {
             a[0][j * Gm::R2 + kk] = (x < 0) ? (uint32_t)((int64_t)q + x) : (uint32_t)x;  // x mod q (reading S8)
         }
     ntt_chain<N, 1>(a, ea.tw_fwd + (size_t)limb * Gm::TW_LIMB, g, q, q2, bufA, bufB);
-    uint32_t *dst = ea.store + ((size_t)pt * ea.L + limb) * 2 * N;
 #pragma unroll
     for (int v = 0; v < V / 4; v++) {
         uint32_t y[4], yp[4];
@@ -185,8 +192,14 @@ __global__ void __launch_bounds__(NttGeom<N>::T) encode_kernel(EncodeArgs ea) {
             else
                 yp[i] = (uint32_t)(((uint64_t)y[i] << 32) / q);                                // Shoup companion
         }
-        *reinterpret_cast<uint4 *>(dst + ntt_word<N>(g, v)) = make_uint4(y[0], y[1], y[2], y[3]);
-        *reinterpret_cast<uint4 *>(dst + N + ntt_word<N>(g, v)) = make_uint4(yp[0], yp[1], yp[2], yp[3]);
+        if constexpr (PtStore<N>::MONT) {
+            *reinterpret_cast<uint4 *>(ea.store + pt_mont_word<N>(pt, ea.L, limb, g, v)) =
+                make_uint4(yp[0], yp[1], yp[2], yp[3]);
+        } else {
+            uint32_t *dst = ea.store + ((size_t)pt * ea.L + limb) * 2 * N;
+            *reinterpret_cast<uint4 *>(dst + ntt_word<N>(g, v)) = make_uint4(y[0], y[1], y[2], y[3]);
+            *reinterpret_cast<uint4 *>(dst + N + ntt_word<N>(g, v)) = make_uint4(yp[0], yp[1], yp[2], yp[3]);
+        }
     }
 }
 
@@ -394,7 +407,7 @@ __device__ __forceinline__ void eval_limb(EvalState<N, L, NC> &st, const BatchAr
     for (int v = 0; v < V / 4; v++) {
         if constexpr (PtStore<N>::MONT) {
             const uint32_t qi = ba.kp.mqinv[J];
-            const uint4 pm = ldg_stream(pv + N + ntt_word<N>(g, v));
+            const uint4 pm = ldg_stream(phat + pt_mont_word<N>(0, L, J, g, v));   // phat: pair base + parity
 #pragma unroll
             for (int c = 0; c < NC; c++) {
                 const uint4 x = ldg_stream(chat_q + chat_word<N>(L, comp0 + c, J, g, v));
@@ -585,7 +598,8 @@ __device__ __forceinline__ void eval_item(const BatchArgs &ba, const ItemCursor 
     const uint32_t ch = local / P, k = local % P;
     const uint32_t qb = ba.seg[li] + ch * ba.chunk;
     const uint32_t qe = min(qb + ba.chunk, ba.seg[li] + cnt);
-    const uint32_t *phat = ba.store + (size_t)(ba.pt_base[li] + k) * L * 2 * N;
+    const size_t pt = (size_t)ba.pt_base[li] + k;
+    const uint32_t *phat = PtStore<N>::MONT ? ba.store + pt_mont_word<N>(pt, L, 0, 0, 0) : ba.store + pt * L * 2 * N;
     for (uint32_t qi = qb; qi < qe; qi++) {
         const uint32_t qo = ba.perm[qi];
         uint32_t *out_q = ba.resp + ba.resp_off[qo] + (size_t)k * ba.wpp;
@@ -1719,7 +1733,7 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
         d.np = min(2u, P - d.k0);                               // plaintexts of the item (1 only for odd P_c)
         d.qb = s_ba.seg[li] + ch * s_ba.chunk;
         d.qe = min(d.qb + s_ba.chunk, s_ba.seg[li] + s_ba.counts[li]);
-        d.phat0 = s_ba.store + (size_t)(s_ba.pt_base[li] + d.k0) * L * 2 * N;
+        d.phat0 = s_ba.store + pt_mont_word<N>((size_t)s_ba.pt_base[li] + d.k0, L, 0, 0, 0);   // an even index
         d.nchunks = (d.qe - d.qb) * L * CHUNKS;
         return d;
     };
@@ -1729,14 +1743,12 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
     auto produce = [&](const Desc &d, uint32_t j, uint32_t sq) {
         const uint32_t sl = sq % NSLOT;
         if (sq >= NSLOT) mbar_wait(empty_b(sl), ((sq / NSLOT) + 1) & 1u);
-        mbar_expect_tx(full_b(sl), (4 + d.np) * CHUNK_BYTES);
+        mbar_expect_tx(full_b(sl), 6 * CHUNK_BYTES);
         const uint32_t r = j / (L * CHUNKS), J = L - 1 - (j / CHUNKS) % L, c = j % CHUNKS;
         const uint32_t dst = slots_s + sl * SLOT_BYTES;
-        static_assert(PtStore<N>::MONT, "v5 stages the Montgomery plane of the plaintext store only");
-        for (uint32_t u = 0; u < d.np; u++) {
-            const uint32_t *pj = d.phat0 + ((size_t)u * L + J) * 2 * N + N + (size_t)c * 4 * T;
-            bulk_g2s(dst + u * CHUNK_BYTES, pj, CHUNK_BYTES, full_b(sl));
-        }
+        // chunk c of both plaintexts of the pair (the second is the pad plaintext when P_c is odd)
+        static_assert(PtStore<N>::MONT, "v6 stages the pair-interleaved Montgomery store");
+        bulk_g2s(dst, d.phat0 + pt_mont_word<N>(0, L, J, 0, c), 2 * CHUNK_BYTES, full_b(sl));
         bulk_g2s(dst + 2 * CHUNK_BYTES, s_ba.tw_slot + (size_t)J * kP8tSlotTwEntries + (size_t)c * 4 * T,
                  2 * CHUNK_BYTES, full_b(sl));
         const uint32_t *cq = s_ba.chat + (size_t)s_ba.perm[d.qb + r] * 2 * L * N;

@@ -46,14 +46,22 @@ struct KParams {
     uint32_t mqinv[kMaxLimbs];    // -q^{-1} mod 2^32 (Montgomery products with the n = 8192 plaintexts)
 };
 
-// Plaintext store planes ([npt][L][2][n] uint32): plane 0 holds the folded
-// NTT-domain value y = NTT(p) F_l (canonical).  Plane 1 holds, at n <= 4096,
-// y's Shoup companion floor(y 2^32 / q) and, at n = 8192, y's Montgomery form
-// y 2^32 mod q: the n = 8192 kernels multiply with one plane only (a
-// Montgomery product, mont_mul), so the v5 kernel stages half the plaintext
-// bytes per chunk.
+// Plaintext store.  n <= 4096: [npt][L][2][n] uint32, per limb the folded
+// NTT-domain value y = NTT(p) F_l (canonical, ntt_word order) followed by its
+// Shoup companion floor(y 2^32 / q).  n = 8192 (MONT): one plane, y's
+// Montgomery form y 2^32 mod q, multiplied with mont_mul (no companion), and
+// plaintexts stored in pairs (2k, 2k + 1) interleaved by 16-byte chunk --
+// [npt/2][L][chunk v][2][4T] -- so one bulk copy stages chunk v of both
+// plaintexts of a v6 work item; every cluster starts at an even plaintext
+// index (a pad plaintext, all zero, after an odd P_c).  DESIGN.md §5-6.
 template <int N>
-struct PtStore { static constexpr bool MONT = (N == 8192); };
+struct PtStore {
+    static constexpr bool MONT = (N == 8192);
+    static constexpr int PLANES = MONT ? 1 : 2;
+    static constexpr uint32_t ALIGN = MONT ? 2 : 1;   // plaintext index alignment of a cluster
+};
+inline uint32_t pt_store_planes(uint32_t n) { return n == 8192 ? 1u : 2u; }
+inline uint32_t pt_store_align(uint32_t n) { return n == 8192 ? 2u : 1u; }
 
 // Workspace layout of one batch (device), offsets in bytes.
 struct WsLayout {
@@ -85,7 +93,7 @@ struct BatchArgs {
     const int32_t *local_of_cluster;  // [total_clusters]
     const uint32_t *pt_base;      // [n_local]
     const uint32_t *n_pt;         // [n_local]
-    const uint32_t *store;        // [npt][L][2][n] (planes: PtStore)
+    const uint32_t *store;        // plaintext store (layout: PtStore)
     const uint32_t *query_ct;     // [nq][2][L][n]
     uint32_t *resp;
     // workspace pieces
@@ -111,7 +119,7 @@ struct EncodeArgs {
     const uint32_t *pt_k;         // [npt] index of the plaintext in its cluster
     const uint64_t *entry_base;   // [n_local] first entry row of each local cluster
     const uint32_t *size;         // [n_local] entries of each local cluster
-    uint32_t *store;              // [npt][L][2][n]
+    uint32_t *store;              // plaintext store (layout: PtStore)
 };
 
 // Does a batch take the pruned-c0 fused kernel (kernels.cu "Fused kernel
