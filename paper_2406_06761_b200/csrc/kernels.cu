@@ -1534,12 +1534,16 @@ __device__ __forceinline__ void c0_tail_fast8(uint32_t *z, uint32_t *cst, const 
 namespace p8t {
 constexpr int N = 8192;
 constexpr int T = NttGeom<N>::T;                 // 256 threads per group
-#ifndef WALLY_P8T_NSLOT
-#define WALLY_P8T_NSLOT 4
+#ifndef WALLY_P8T_CPS
+#define WALLY_P8T_CPS 2
 #endif
+#ifndef WALLY_P8T_NSLOT
+#define WALLY_P8T_NSLOT (WALLY_P8T_CPS == 1 ? 4 : 2)
+#endif
+constexpr int CPS = WALLY_P8T_CPS;               // chunks per ring slot
 constexpr int NSLOT = WALLY_P8T_NSLOT;
 constexpr int CHUNK_BYTES = T * 16;              // one 16-byte chunk of every thread: 4 KB
-constexpr int SLOT_BYTES = 6 * CHUNK_BYTES;      // 2 Montgomery plaintext chunks, 2 twiddle blocks, c0, c1
+constexpr int SLOT_BYTES = 6 * CPS * CHUNK_BYTES;   // per chunk: 2 Montgomery plaintext chunks, 2 twiddle blocks, c0, c1
 constexpr int TW12 = NttGeom<N>::TW_LIMB - NttGeom<N>::TW1;   // pass-1/2 table entries per limb
 constexpr int XB_WORDS = NttGeom<N>::SMEM_WORDS;
 __host__ __device__ constexpr size_t smem_bytes(int L) {
@@ -1666,6 +1670,7 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
     constexpr int V = Gm::V;
     constexpr int NA = (L > 2) ? (L - 2) : 1;
     constexpr int CHUNKS = V / 4;                 // 8 chunks of 4 values per thread and limb
+    constexpr int EPL = CHUNKS / CPS;             // ring elements per limb
     extern __shared__ __align__(128) uint8_t smem8[];
     uint8_t *slots = smem8;
     uint2 *s_tw12 = reinterpret_cast<uint2 *>(smem8 + NSLOT * SLOT_BYTES);
@@ -1734,7 +1739,7 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
         d.qb = s_ba.seg[li] + ch * s_ba.chunk;
         d.qe = min(d.qb + s_ba.chunk, s_ba.seg[li] + s_ba.counts[li]);
         d.phat0 = s_ba.store + pt_mont_word<N>((size_t)s_ba.pt_base[li] + d.k0, L, 0, 0, 0);   // an even index
-        d.nchunks = (d.qe - d.qb) * L * CHUNKS;
+        d.nchunks = (d.qe - d.qb) * L * EPL;   // ring elements (CPS chunks each)
         return d;
     };
     // producer (thread 0): element j of item description d into ring position sq: wait for the slot
@@ -1743,16 +1748,17 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
     auto produce = [&](const Desc &d, uint32_t j, uint32_t sq) {
         const uint32_t sl = sq % NSLOT;
         if (sq >= NSLOT) mbar_wait(empty_b(sl), ((sq / NSLOT) + 1) & 1u);
-        mbar_expect_tx(full_b(sl), 6 * CHUNK_BYTES);
-        const uint32_t r = j / (L * CHUNKS), J = L - 1 - (j / CHUNKS) % L, c = j % CHUNKS;
+        mbar_expect_tx(full_b(sl), 6 * CPS * CHUNK_BYTES);
+        const uint32_t r = j / (L * EPL), J = L - 1 - (j / EPL) % L, c = (j % EPL) * CPS;
         const uint32_t dst = slots_s + sl * SLOT_BYTES;
         // chunk c of both plaintexts of the pair (the second is the pad plaintext when P_c is odd)
         static_assert(PtStore<N>::MONT, "v6 stages the pair-interleaved Montgomery store");
-        bulk_g2s(dst, d.phat0 + pt_mont_word<N>(0, L, J, 0, c), 2 * CHUNK_BYTES, full_b(sl));
-        bulk_g2s(dst + 2 * CHUNK_BYTES, s_ba.tw_slot + (size_t)J * kP8tSlotTwEntries + (size_t)c * 4 * T,
-                 2 * CHUNK_BYTES, full_b(sl));
+        bulk_g2s(dst, d.phat0 + pt_mont_word<N>(0, L, J, 0, c), 2 * CPS * CHUNK_BYTES, full_b(sl));
+        bulk_g2s(dst + 2 * CPS * CHUNK_BYTES, s_ba.tw_slot + (size_t)J * kP8tSlotTwEntries + (size_t)c * 4 * T,
+                 2 * CPS * CHUNK_BYTES, full_b(sl));
         const uint32_t *cq = s_ba.chat + (size_t)s_ba.perm[d.qb + r] * 2 * L * N;
-        bulk_g2s(dst + 4 * CHUNK_BYTES, cq + chat_word<N>(L, 0, J, 0, c), 2 * CHUNK_BYTES, full_b(sl));   // c0, c1
+        bulk_g2s(dst + 4 * CPS * CHUNK_BYTES, cq + chat_word<N>(L, 0, J, 0, c), 2 * CPS * CHUNK_BYTES,
+                 full_b(sl));   // c0, c1
     };
     uint32_t pre_issued = 0;   // thread 0: elements of the current item issued while the previous one ran
     // items are claimed in blocks of `ib` consecutive ones (thread 0 keeps the current block's end and
@@ -1809,16 +1815,19 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
                 uint2 k1 = make_uint2(0, 0), k2 = make_uint2(0, 0), k3 = make_uint2(0, 0);  // twiddle halves kept
 #pragma unroll
                 for (int c = 0; c < CHUNKS; c++) {
-                    const uint32_t j = (r * L + Jr) * CHUNKS + c;   // stream element
-                    if (threadIdx.x == 0) issue(j + NSLOT - 1);
+                    const uint32_t j = (r * L + Jr) * EPL + c / CPS;   // stream element
                     const uint32_t sq = seq0 + j, sl = sq % NSLOT;
-                    mbar_wait(full_b(sl), (sq / NSLOT) & 1u);
+                    const int h = c % CPS;                             // chunk inside the element (unrolled: constant)
+                    if (h == 0) {
+                        if (threadIdx.x == 0) issue(j + NSLOT - 1);
+                        mbar_wait(full_b(sl), (sq / NSLOT) & 1u);
+                    }
                     const uint4 *sp = reinterpret_cast<const uint4 *>(slots + sl * SLOT_BYTES);
                     if (active) {
                         const uint32_t qi = s_ba.kp.mqinv[J];
-                        const uint4 pm = sp[grp * T + g];
-                        const uint4 w0 = sp[2 * T + g], ta = sp[3 * T + g];
-                        const uint4 x0 = sp[4 * T + g], x1 = sp[5 * T + g];
+                        const uint4 pm = sp[(2 * h + grp) * T + g];
+                        const uint4 w0 = sp[(2 * CPS + 2 * h) * T + g], ta = sp[(2 * CPS + 2 * h + 1) * T + g];
+                        const uint4 x0 = sp[(4 * CPS + 2 * h) * T + g], x1 = sp[(4 * CPS + 2 * h + 1) * T + g];
                         a[0][4 * c + 0] = mont_mul(x1.x, pm.x, q, qi);
                         a[0][4 * c + 1] = mont_mul(x1.y, pm.y, q, qi);
                         a[0][4 * c + 2] = mont_mul(x1.z, pm.z, q, qi);
@@ -1881,8 +1890,10 @@ __global__ void __launch_bounds__(2 * NttGeom<8192>::T, 1) eval_kernel_p8t(Batch
                             }
                         }
                     }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(empty_b(sl));
+                    if (h == CPS - 1) {
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(empty_b(sl));
+                    }
                 }
                 if (!active) continue;
                 uint32_t *z = s_ybuf[grp] + par * T;
