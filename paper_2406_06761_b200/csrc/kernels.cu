@@ -313,10 +313,9 @@ __global__ void batch_scatter_kernel(const uint32_t *__restrict__ ids, uint32_t 
 // a3-a6: fused pointwise modmul + inverse NTT + modulus switch + write
 // ---------------------------------------------------------------------------
 
-// ((h_m - (r mod q_l)) * C[l][m]) mod q_l, canonical; r < q_m < 2 q_l.
+// ((h_m - (r mod q_l)) * C[l][m]) mod q_l in [0, 2 q_l) (lazy); r < q_m < 2 q_l.
 __device__ __forceinline__ uint32_t ms_term(uint32_t r, uint32_t h_m, uint32_t q_l, uint32_t C, uint32_t Cp) {
-    uint32_t rl = csub(r, q_l);
-    return csub(shoup_mul(h_m + q_l - rl, C, Cp, q_l), q_l);
+    return shoup_mul(h_m + q_l - csub(r, q_l), C, Cp, q_l);
 }
 
 // Modulus-switch bookkeeping after the inverse NTT of limb J (limbs are
@@ -327,33 +326,41 @@ __device__ __forceinline__ uint32_t ms_term(uint32_t r, uint32_t h_m, uint32_t q
 // accumulating  A_l = sum_{m>l} (h_m - r_m) prod_{k=l+1..m} q_k^{-1}  so that
 // c_l(final) = c_l F_l + A_l.  Limb 0's final value is the response word.
 // Element form of the recurrence (limb J; rtop / acc = this coefficient's
-// state, NA = max(L - 2, 1) accumulators).
+// state, NA = max(L - 2, 1) accumulators).  Ranges: the rounding residues
+// (rtop, r) and the response word are canonical; the accumulated terms stay
+// lazy in [0, 2q) (sums of two are < 4q < 2^32), so each residue costs one
+// three-input add and two conditional subtractions.  a is consumed: for
+// J > 0 only its residue r is kept.
 template <int L, int J, int NA>
 __device__ __forceinline__ void ms_elem(uint32_t &a, uint32_t &rtop, uint32_t (&acc)[NA], const KParams &kp) {
-    const uint32_t qj = kp.q[J];
-    a = csub(a, qj);
+    const uint32_t qj = kp.q[J], qj2 = kp.q2[J];
     if constexpr (L == 1) {
-        return;
+        a = csub(a, qj);
+    } else if constexpr (L == 2) {
+        // two limbs: canonical steps (measured 1% faster on c5 than the lazy form)
+        a = csub(a, qj);
+        if constexpr (J == 1) rtop = csub(a + kp.h[1], qj);
+        else a = csub(a + csub(ms_term(rtop, kp.h[1], qj, kp.C[0][1], kp.Cp[0][1]), qj), qj);
     } else if constexpr (J == L - 1) {
-        rtop = csub(a + kp.h[J], qj);
+        rtop = csub(csub(a + kp.h[J], qj2), qj);                    // a + h < 2.5 q
     } else {
-        uint32_t A;
+        uint32_t A;                                                  // [0, 2q)
         if constexpr (J == L - 2)
             A = ms_term(rtop, kp.h[L - 1], qj, kp.C[J][L - 1], kp.Cp[J][L - 1]);
         else
             A = acc[J];
-        a = csub(a + A, qj);
         if constexpr (J > 0) {
-            const uint32_t r = csub(a + kp.h[J], qj);
+            const uint32_t r = csub(csub(a + csub(A, qj) + kp.h[J], qj2), qj);   // < 2q + q + q/2
 #pragma unroll
             for (int l = 0; l < J; l++) {
                 const uint32_t ql = kp.q[l];
                 const uint32_t term = ms_term(r, kp.h[J], ql, kp.C[l][J], kp.Cp[l][J]);
-                if constexpr (J == L - 2)
-                    acc[l] = csub(ms_term(rtop, kp.h[L - 1], ql, kp.C[l][L - 1], kp.Cp[l][L - 1]) + term, ql);
-                else
-                    acc[l] = csub(acc[l] + term, ql);
+                const uint32_t prev =
+                    (J == L - 2) ? ms_term(rtop, kp.h[L - 1], ql, kp.C[l][L - 1], kp.Cp[l][L - 1]) : acc[l];
+                acc[l] = csub(prev + term, kp.q2[l]);               // < 4 q -> [0, 2q)
             }
+        } else {
+            a = csub(csub(a + A, qj2), qj);                          // < 4 q -> canonical response word
         }
     }
 }
