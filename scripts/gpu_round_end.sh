@@ -19,7 +19,7 @@ python -c "import json;d=json.load(open('gpurun_out/bench_c4_full.json'));r=d['r
 bash scripts/gpu_simd_refresh.sh
 B="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline"
 timeout 600 $B > gpurun_out/plain_launch.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv $B > gpurun_out/ncu_launch.log 2>&1; echo "ncu launch rc=$?"
-for c in c3 c4; do
+for c in c3 c4 c5; do
   P="python bench.py --config $c --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
   timeout 600 $P > gpurun_out/plain_full_$c.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k regex:eval_kernel -s 1 -c 1 -o gpurun_out/prof_final_$c $P > gpurun_out/ncu_final_$c.log 2>&1; echo "$c ncu rc=$?"
 done
@@ -27,3 +27,4 @@ done
 ./paper_2406_06761_b200/imma_bench > gpurun_out/imma.jsonl 2>&1
 ./paper_2406_06761_b200/tc_ntt_bench --reps 16 --mma-only > gpurun_out/tc_ntt.jsonl 2>&1
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err; echo "reference rc=$?"; head -c 300 gpurun_out/bench_reference.json; echo
