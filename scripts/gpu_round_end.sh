@@ -19,9 +19,16 @@ python -c "import json;d=json.load(open('gpurun_out/bench_c4_full.json'));r=d['r
 bash scripts/gpu_simd_refresh.sh
 B="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline"
 timeout 600 $B > gpurun_out/plain_launch.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv $B > gpurun_out/ncu_launch.log 2>&1; echo "ncu launch rc=$?"
+# full captures go to /tmp (an .ncu-rep is tens of MB; gpurun_out/ must stay under 64 MiB): the summaries,
+# the per-line stall table and the traffic record are written here on the box
+declare -A KN=([c3]=_ZN5wally14eval_kernel_prILi3ELi2EEEvNS_9BatchArgsE [c4]=_ZN5wally15eval_kernel_p8tILi4ELi1EEEvNS_9BatchArgsE [c5]=_ZN5wally14eval_kernel_prILi2ELi2EEEvNS_9BatchArgsE)
 for c in c3 c4 c5; do
   P="python bench.py --config $c --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
-  timeout 600 $P > gpurun_out/plain_full_$c.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k regex:eval_kernel -s 1 -c 1 -o gpurun_out/prof_final_$c $P > gpurun_out/ncu_final_$c.log 2>&1; echo "$c ncu rc=$?"
+  timeout 600 $P > gpurun_out/plain_full_$c.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k regex:eval_kernel -s 1 -c 1 -o /tmp/prof_final_$c $P > gpurun_out/ncu_final_$c.log 2>&1; echo "$c ncu rc=$?"
+  python scripts/ncu_summary.py /tmp/prof_final_$c.ncu-rep > gpurun_out/ncu_summary_$c.txt 2>&1
+  python scripts/ncu_lines.py /tmp/prof_final_$c.ncu-rep paper_2406_06761_b200/libwally.so ${KN[$c]} 30 > gpurun_out/ncu_lines_$c.txt 2>&1
+  cp profiles/ncu_fused_traffic.json gpurun_out/ncu_fused_traffic.json 2>/dev/null
+  python scripts/update_traffic.py $c /tmp/prof_final_$c.ncu-rep 2 > /dev/null 2>&1 && cp profiles/ncu_fused_traffic.json gpurun_out/ncu_fused_traffic.json
 done
 ./paper_2406_06761_b200/intpipe_bench > gpurun_out/intpipe.jsonl 2>&1
 ./paper_2406_06761_b200/imma_bench > gpurun_out/imma.jsonl 2>&1
