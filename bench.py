@@ -545,7 +545,7 @@ def run_simd(args, rank, world, local_rank):
     path shards by query like the coefficient path)."""
     import torch
     import torch.distributed as dist
-    from paper_2406_06761_b200.simd import SimdServer
+    from paper_2406_06761_b200.simd import STAGES as STAGES_SIMD, SimdServer
 
     torch.cuda.set_device(local_rank)
     dev = f"cuda:{local_rank}"
@@ -581,6 +581,8 @@ def run_simd(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     launches0 = srv.launch_count()
+    srv.stage_times()                                  # clear
+    srv.enable_stage_timing(True)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         clk.wait_first()
@@ -595,6 +597,8 @@ def run_simd(args, rank, world, local_rank):
         torch.cuda.synchronize()
         t_clk1 = clk.mark()
     ms = start.elapsed_time(end)
+    srv.enable_stage_timing(False)
+    st_ms, _ = srv.stage_times()
     launches = srv.launch_count() - launches0
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     wk = torch.tensor([dots, nq], dtype=torch.float64, device=dev)
@@ -608,16 +612,41 @@ def run_simd(args, rank, world, local_rank):
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     clocks = clk.summary(t_clk0, t_clk1)
     mm = sum(srv.modmuls_per_query(int(b)) for b in blocks)
-    achieved = mm / (ms / args.steps / 1e3) / 1e12
     peak = SM_COUNT * MODMUL_PER_CLK_PER_SM * sm_max * 1e6 / 1e12
-    roofline = {"bound": "fmaheavy", "bound_class": "alu (integer multiply-add on the FMA-heavy pipe; no "
-                                                    "tensor-core or HBM bound, DESIGN.md section 6)",
+    hbm_peak = float(peaks.get("hbm_gbs", 6556.5))
+    # per-stage roofline (include/wally_simd.h wally_simd_stage_work): each stage is bound by the larger of
+    # its modmuls on the integer pipe and its minimum HBM bytes; the step's bound is their sum
+    smm, sby = srv.stage_work(ids)
+    stages, t_bound = {}, 0.0
+    for i, name in enumerate(STAGES_SIMD):
+        sms = st_ms[i] / args.steps
+        t_int = smm[i] / (peak * 1e12) * 1e3
+        t_hbm = sby[i] / (hbm_peak * 1e9) * 1e3
+        tb = max(t_int, t_hbm)
+        t_bound += tb
+        stages[name] = {"ms": round(sms, 3), "modmuls": smm[i], "bytes": sby[i],
+                        "bound": "fmaheavy" if t_int >= t_hbm else "hbm",
+                        "achieved": round(smm[i] / (sms / 1e3) / 1e12, 4) if t_int >= t_hbm
+                        else round(sby[i] / (sms / 1e3) / 1e9, 1),
+                        "unit": "Tmodmul/s" if t_int >= t_hbm else "GB/s",
+                        "frac": round(tb / sms, 4) if sms > 0 else None}
+    rot_ms = (st_ms[1] + st_ms[3]) / args.steps
+    rot_mm = smm[1] + smm[3]
+    achieved = rot_mm / (rot_ms / 1e3) / 1e12
+    roofline = {"bound": "fmaheavy", "bound_class": "alu (integer multiply-add on the FMA-heavy pipe, DESIGN.md "
+                                                    "section 6)",
                 "achieved": round(achieved, 4), "peak": round(peak, 4), "unit": "Tmodmul/s",
                 "frac": round(achieved / peak, 4), "traffic": None,
-                "kernel": "the whole SIMD step (simd_ntt, simd_modup/moddown key switching, simd_ptmac, "
-                          "simd_switch; every kernel is bound by the same integer multiply pipe)",
-                "per_launch": f"{mm} modmul per step (wally_simd_modmuls_per_query summed over the batch)",
-                "peak_basis": f"{SM_COUNT} SMs x {MODMUL_PER_CLK_PER_SM:.0f} Shoup modmul/clk/SM x {sm_max:.0f} MHz"}
+                "kernel": "the rotations (baby and giant steps: simd_rot_chain_kernel, or simd_modup/moddown), "
+                          f"{100 * rot_ms / (ms / args.steps):.0f}% of the step, timed by the library's stage events",
+                "per_launch": f"{rot_mm} modmul per step in the rotations (wally_simd_stage_work)",
+                "peak_basis": f"{SM_COUNT} SMs x {MODMUL_PER_CLK_PER_SM:.0f} Shoup modmul/clk/SM x {sm_max:.0f} MHz",
+                "step_frac": round(t_bound / (ms / args.steps), 4),
+                "step_bound_ms": round(t_bound, 3),
+                "step_frac_basis": "sum over the five stages of max(modmuls / integer peak, bytes / HBM peak "
+                                   f"{hbm_peak:.0f} GB/s) divided by the measured step time",
+                "frac_all_int_pipe": round(mm / (ms / args.steps / 1e3) / 1e12 / peak, 4),
+                "stages": stages}
     out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "u32",

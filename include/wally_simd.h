@@ -131,6 +131,31 @@ int wally_simd_set_chain_threshold(wally_simd_ctx *ctx, uint32_t min_queries);
 /* Kernel launches issued by this context so far. */
 uint64_t wally_simd_launch_count(const wally_simd_ctx *ctx);
 
+/* Per-stage device timing of wally_simd_eval_batch (off by default): CUDA
+ * events recorded on the batch's stream at the stage boundaries of every
+ * query chunk.  wally_simd_stage_times synchronizes them and returns the
+ * summed milliseconds since the last call in ms_out[5]:
+ *   [0] a2'  NTT of the query ciphertexts and rotation keys,
+ *   [1]      baby-step rotations (g - 1 per query, P:L1352-1361 BSGS),
+ *   [2] a3'  diagonal inner products I_j (P:L565 diagonals),
+ *   [3]      giant-step rotations (m - 1 per block, Horner),
+ *   [4] a5'-a6' inverse NTT and switch to q_0;
+ * chunks_out = number of query chunks summed.  Clears the record. */
+int wally_simd_enable_stage_timing(wally_simd_ctx *ctx, int enable);
+int wally_simd_stage_times(wally_simd_ctx *ctx, double *ms_out, uint64_t *chunks_out);
+
+/* Algorithmic work of the same five stages for a batch of nq queries with
+ * cluster ids ids[nq] (host array): modmuls_out[5] modular multiplications
+ * (the terms of wally_simd_modmuls_per_query) and bytes_out[5] the HBM bytes
+ * each stage must move at least (operands read once, results written once:
+ * stage [2] reads the d plaintexts of every distinct block of the batch once,
+ * with their Shoup companions, 8 L n d bytes per block, however many of the
+ * batch's queries use it).  The roofline of a stage is the larger of
+ * modmuls / integer-pipe peak and bytes / HBM peak.
+ * Returns WALLY_E_ARG for a null pointer or an unknown cluster id. */
+int wally_simd_stage_work(const wally_simd_ctx *ctx, uint32_t nq, const uint32_t *ids, uint64_t *modmuls_out,
+                          uint64_t *bytes_out);
+
 #ifdef __cplusplus
 }
 #endif

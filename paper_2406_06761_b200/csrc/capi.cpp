@@ -235,7 +235,7 @@ extern "C" int wally_create(const wally_params *pp, int device, wally_ctx **out)
         if (i && q <= p.moduli[i - 1]) return fail(nullptr, WALLY_E_PARAMS, "moduli must be strictly ascending");
     }
     if (p.moduli[p.num_limbs - 1] >= 2ull * p.moduli[0])
-        return fail(nullptr, WALLY_E_PARAMS, "need q_{L-1} < 2 q_0 (single-subtract reduction of r mod q_i)");
+        return fail(nullptr, WALLY_E_PARAMS, "need q_{L-1} < 2 q_0 (the rounding residues r < q_m enter the switch step unreduced mod q_l)");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
         return fail(nullptr, WALLY_E_CUDA, "no CUDA device %d", device);
@@ -277,6 +277,10 @@ extern "C" int wally_create(const wally_params *pp, int device, wally_ctx **out)
             cm = mulm(cm, invm(p.moduli[m] % q, q), q);
             kp.C[l][m] = (uint32_t)cm;
             kp.Cp[l][m] = shoup_companion((uint32_t)cm, (uint32_t)q);
+        }
+        for (uint32_t m = l + 1; m < L; m++) {
+            kp.Qi[l][m] = (uint32_t)invm(p.moduli[m] % q, q);
+            kp.Qip[l][m] = shoup_companion(kp.Qi[l][m], (uint32_t)q);
         }
         const uint64_t psi = primitive_2n_root(q, n);
         const uint64_t psi_inv = invm(psi, q);

@@ -313,9 +313,16 @@ __global__ void batch_scatter_kernel(const uint32_t *__restrict__ ids, uint32_t 
 // a3-a6: fused pointwise modmul + inverse NTT + modulus switch + write
 // ---------------------------------------------------------------------------
 
-// ((h_m - (r mod q_l)) * C[l][m]) mod q_l in [0, 2 q_l) (lazy); r < q_m < 2 q_l.
+// ((h_m - r) * C[l][m]) mod q_l in [0, 2 q_l) (lazy); r < q_m < 2 q_l.
+// LAZY: the Shoup product accepts any 32-bit multiplicand, so h_m + 2 q_l - r
+// (in (0, 2^32) for 30-bit limbs with q_{L-1} < 2 q_0, which wally_create
+// enforces) needs no reduction of r mod q_l first: one ALU instruction
+// instead of two (c3 73.9 -> 73.1 ms, c4 71.9 -> 71.5; c5, L = 2, measured
+// 0.7% slower with it and keeps the reduced form).
+template <bool LAZY = true>
 __device__ __forceinline__ uint32_t ms_term(uint32_t r, uint32_t h_m, uint32_t q_l, uint32_t C, uint32_t Cp) {
-    return shoup_mul(h_m + q_l - csub(r, q_l), C, Cp, q_l);
+    if constexpr (LAZY) return shoup_mul(h_m + 2 * q_l - r, C, Cp, q_l);
+    else return shoup_mul(h_m + q_l - csub(r, q_l), C, Cp, q_l);
 }
 
 // Modulus-switch bookkeeping after the inverse NTT of limb J (limbs are
@@ -323,14 +330,28 @@ __device__ __forceinline__ uint32_t ms_term(uint32_t r, uint32_t h_m, uint32_t q
 // F_J = prod_{k>J} q_k^{-1} was applied through the plaintext.  Implements
 // the sequential drop-last rounding (reading S7):
 //   r_m = (c_m + h_m) mod q_m,  c_l <- (c_l + h_m - r_m) q_m^{-1}  for l < m,
-// accumulating  A_l = sum_{m>l} (h_m - r_m) prod_{k=l+1..m} q_k^{-1}  so that
-// c_l(final) = c_l F_l + A_l.  Limb 0's final value is the response word.
+// so that c_l(final) = c_l F_l + A_l with
+//   A_l = sum_{m>l} (h_m - r_m) prod_{k=l+1..m} q_k^{-1}
+//       = (...((h_{L-1} - r_{L-1}) q_{L-1}^{-1} + h_{L-2} - r_{L-2}) q_{L-2}^{-1} + ... + h_{l+1} - r_{l+1}) q_{l+1}^{-1},
+// evaluated as follows (WALLY_MS_FORM = 2, the default).  At limb L-2 both
+// terms of accumulator l share the factor C[l][L-2] (C[l][L-1] =
+// C[l][L-2] q_{L-1}^{-1}), so
+//   acc_l = ((h_{L-1} - r_{L-1}) q_{L-1}^{-1} + h_{L-2} - r_{L-2}) C[l][L-2]:
+// the inner Shoup product t lies in [0, 2q_l), and t + (h_{L-2} + q_l) - r
+// (>= 0 because r < q_{L-2} < 2 q_l gives r <= h + q_l; < 3 q_l + q/2 <
+// 2^32) goes straight into the outer one; later limbs J < L-2 add
+// (h_J - r_J) C[l][J].  Limb 0's final value is the response word.
+// Alternatives kept for A/B timing: WALLY_MS_FORM = 0, the additive form
+// at every limb (four ALU instructions per term instead of two at limb
+// L-2); = 1, the Horner form acc_l <- (acc_l + h_J - r_J) q_J^{-1} at every
+// limb (identical at L = 3).  c4: 71.4 / 71.3 / 70.7 ms for forms 0 / 1 / 2.
 // Element form of the recurrence (limb J; rtop / acc = this coefficient's
 // state, NA = max(L - 2, 1) accumulators).  Ranges: the rounding residues
-// (rtop, r) and the response word are canonical; the accumulated terms stay
-// lazy in [0, 2q) (sums of two are < 4q < 2^32), so each residue costs one
-// three-input add and two conditional subtractions.  a is consumed: for
-// J > 0 only its residue r is kept.
+// (rtop, r) and the response word are canonical; the accumulators lie in
+// [0, 2q_l).  a is consumed: for J > 0 only its residue r is kept.
+#ifndef WALLY_MS_FORM
+#define WALLY_MS_FORM 2
+#endif
 template <int L, int J, int NA>
 __device__ __forceinline__ void ms_elem(uint32_t &a, uint32_t &rtop, uint32_t (&acc)[NA], const KParams &kp) {
     const uint32_t qj = kp.q[J], qj2 = kp.q2[J];
@@ -340,7 +361,7 @@ __device__ __forceinline__ void ms_elem(uint32_t &a, uint32_t &rtop, uint32_t (&
         // two limbs: canonical steps (measured 1% faster on c5 than the lazy form)
         a = csub(a, qj);
         if constexpr (J == 1) rtop = csub(a + kp.h[1], qj);
-        else a = csub(a + csub(ms_term(rtop, kp.h[1], qj, kp.C[0][1], kp.Cp[0][1]), qj), qj);
+        else a = csub(a + csub(ms_term<false>(rtop, kp.h[1], qj, kp.C[0][1], kp.Cp[0][1]), qj), qj);
     } else if constexpr (J == L - 1) {
         rtop = csub(csub(a + kp.h[J], qj2), qj);                    // a + h < 2.5 q
     } else {
@@ -354,10 +375,27 @@ __device__ __forceinline__ void ms_elem(uint32_t &a, uint32_t &rtop, uint32_t (&
 #pragma unroll
             for (int l = 0; l < J; l++) {
                 const uint32_t ql = kp.q[l];
+#if WALLY_MS_FORM == 1
+                // acc_l (after limb L-1: (h_{L-1} - r_{L-1}) q_{L-1}^{-1}) <- (acc_l + h_J - r_J) q_J^{-1}
+                const uint32_t base =
+                    (J == L - 2) ? ms_term(rtop, kp.h[L - 1], ql, kp.Qi[l][L - 1], kp.Qip[l][L - 1]) : acc[l];
+                acc[l] = shoup_mul(base + (kp.h[J] + ql) - r, kp.Qi[l][J], kp.Qip[l][J], ql);
+#elif WALLY_MS_FORM == 2
+                // nested at limb L-2 only: acc_l = ((h_{L-1} - r_{L-1}) q_{L-1}^{-1} + h_J - r_J) C[l][J],
+                // later limbs add their terms
+                if constexpr (J == L - 2) {
+                    const uint32_t t = ms_term(rtop, kp.h[L - 1], ql, kp.Qi[l][L - 1], kp.Qip[l][L - 1]);
+                    acc[l] = shoup_mul(t + (kp.h[J] + ql) - r, kp.C[l][J], kp.Cp[l][J], ql);
+                } else {
+                    const uint32_t term = ms_term(r, kp.h[J], ql, kp.C[l][J], kp.Cp[l][J]);
+                    acc[l] = csub(acc[l] + term, kp.q2[l]);
+                }
+#else
                 const uint32_t term = ms_term(r, kp.h[J], ql, kp.C[l][J], kp.Cp[l][J]);
                 const uint32_t prev =
                     (J == L - 2) ? ms_term(rtop, kp.h[L - 1], ql, kp.C[l][L - 1], kp.Cp[l][L - 1]) : acc[l];
                 acc[l] = csub(prev + term, kp.q2[l]);               // < 4 q -> [0, 2q)
+#endif
             }
         } else {
             a = csub(csub(a + A, qj2), qj);                          // < 4 q -> canonical response word

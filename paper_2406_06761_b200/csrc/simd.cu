@@ -34,6 +34,7 @@ namespace wally {
 namespace simd {
 
 constexpr int kMaxMods = WALLY_MAX_LIMBS + 1;
+constexpr int kSimdStages = 5;   // wally_simd_stage_times: NTTs, baby steps, inner products, giant steps, switch
 
 struct Mods {
     uint32_t L, M;                        // ciphertext limbs, L + 1 key moduli (index L = P)
@@ -573,6 +574,11 @@ struct wally_simd_ctx {
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
     uint64_t launches = 0;
+    // per-stage device timing (wally_simd_enable_stage_timing): kSimdStages + 1
+    // events per chunk on the batch's stream
+    bool timing = false;
+    std::vector<std::vector<cudaEvent_t>> ev_rec;
+    std::vector<cudaEvent_t> ev_pool;
     std::string err;
 };
 
@@ -694,6 +700,13 @@ extern "C" const char *wally_simd_last_error(const wally_simd_ctx *ctx) {
 }
 
 extern "C" void wally_simd_destroy(wally_simd_ctx *c) {
+    if (c) {
+        for (auto &r : c->ev_rec)
+            for (auto e : r) c->ev_pool.push_back(e);
+        for (auto e : c->ev_pool) cudaEventDestroy(e);
+        c->ev_rec.clear();
+        c->ev_pool.clear();
+    }
     if (!c) return;
     cudaSetDevice(c->device);
     cudaFree(c->d_twf);
@@ -856,6 +869,61 @@ extern "C" int wally_simd_set_chain_threshold(wally_simd_ctx *c, uint32_t min_qu
 
 // Algorithmic modmuls of one NTT of length n: (n/2) log2 n butterflies.
 static uint64_t s_ntt_mm(const wally_simd_ctx *c) { return (uint64_t)(c->p.n / 2) * c->logn; }
+
+extern "C" int wally_simd_enable_stage_timing(wally_simd_ctx *c, int enable) {
+    if (!c) return WALLY_E_ARG;
+    c->timing = enable != 0;
+    return WALLY_OK;
+}
+
+extern "C" int wally_simd_stage_times(wally_simd_ctx *c, double *ms, uint64_t *chunks) {
+    if (!c || !ms) return WALLY_E_ARG;
+    SCUDA(c, cudaSetDevice(c->device));
+    for (int i = 0; i < kSimdStages; i++) ms[i] = 0.0;
+    for (auto &r : c->ev_rec) {
+        SCUDA(c, cudaEventSynchronize(r[kSimdStages]));
+        for (int i = 0; i < kSimdStages; i++) {
+            float t = 0.f;
+            SCUDA(c, cudaEventElapsedTime(&t, r[i], r[i + 1]));
+            ms[i] += t;
+        }
+    }
+    if (chunks) *chunks = c->ev_rec.size();
+    for (auto &r : c->ev_rec)
+        for (auto e : r) c->ev_pool.push_back(e);
+    c->ev_rec.clear();
+    return WALLY_OK;
+}
+
+extern "C" int wally_simd_stage_work(const wally_simd_ctx *c, uint32_t nq, const uint32_t *ids, uint64_t *mm,
+                                     uint64_t *bytes) {
+    if (!c || !mm || !bytes || (nq && !ids)) return WALLY_E_ARG;
+    const uint64_t n = c->p.n, L = c->L, M = c->M, T = s_ntt_mm(c), d = c->p.d, g = c->g, m = c->m;
+    const uint64_t ks = L * (n + T + L * T) + 2 * (L * M * n + n + T + L * T + L * n);
+    const uint64_t ct = 2 * L * n * 4, key = 2 * 2 * L * M * n * 4;   // bytes of one ciphertext / key pair
+    uint64_t blocks = 0, distinct = 0;   // units (query, block); distinct blocks of the batch
+    std::vector<char> seen(c->n_clusters, 0);
+    for (uint32_t q = 0; q < nq; q++) {
+        if (ids[q] >= c->n_clusters) return WALLY_E_ARG;
+        blocks += c->blk_num[ids[q]];
+        if (!seen[ids[q]]) {
+            seen[ids[q]] = 1;
+            distinct += c->blk_num[ids[q]];
+        }
+    }
+    for (int i = 0; i < kSimdStages; i++) mm[i] = bytes[i] = 0;
+    mm[0] = nq * (2 * L * T + 2 * 2 * L * M * T);
+    bytes[0] = nq * 2 * (ct + key);                                  // read + write in place of the NTT domain
+    mm[1] = nq * (g - 1) * ks;
+    bytes[1] = nq * (key / 2 + g * ct);                              // sigma_5 key, baby_0 in, g - 1 rotations out
+    mm[2] = blocks * d * 2 * L * n;
+    bytes[2] = distinct * d * L * n * 8 + blocks * (g * ct + m * ct);   // plaintexts + companions once, baby steps, I_j
+    mm[3] = blocks * (m - 1) * ks;
+    bytes[3] = blocks * (m * ct) + nq * key / 2;                     // I_j in, accumulator out; sigma_{5^g} key
+    mm[4] = blocks * 2 * (L * (n + T) + n * L * (L - 1) / 2);
+    bytes[4] = blocks * (ct + 2 * n * 4);
+    return WALLY_OK;
+}
 
 extern "C" uint64_t wally_simd_modmuls_per_query(const wally_simd_ctx *c, uint32_t blocks) {
     if (!c) return 0;
@@ -1123,8 +1191,23 @@ static int simd_eval_core(wally_simd_ctx *c, const SimdWs &W, uint32_t nq, const
     std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return ids[a] < ids[b]; });
     uint32_t *baby = W.baby, *keyN = W.keyN, *ext = W.ext, *I = W.I, *accA = W.accA, *accB = W.accB;
     cudaError_t e = cudaSuccess;
+    std::vector<cudaEvent_t> *evr = nullptr;   // stage boundaries of the current chunk (timing on)
+    auto mark = [&](int i) -> cudaError_t { return evr ? cudaEventRecord((*evr)[i], s) : cudaSuccess; };
     for (uint32_t q0 = 0; q0 < nq; q0 += Qc) {
         const uint32_t nc = std::min(Qc, nq - q0);
+        if (c->timing) {
+            std::vector<cudaEvent_t> r(kSimdStages + 1);
+            for (auto &ev : r) {
+                if (c->ev_pool.empty()) {
+                    SCUDA(c, cudaEventCreate(&ev));
+                } else {
+                    ev = c->ev_pool.back();
+                    c->ev_pool.pop_back();
+                }
+            }
+            c->ev_rec.push_back(std::move(r));
+            evr = &c->ev_rec.back();
+        }
         // unit tables of this chunk: a pinned slot whose previous upload has completed
         const int slot = c->tab_slot;
         c->tab_slot ^= 1;
@@ -1145,12 +1228,14 @@ static int simd_eval_core(wally_simd_ctx *c, const SimdWs &W, uint32_t nq, const
         SCUDA(c, cudaMemcpyAsync(W.uq, hq, 4 * W.w_tab, cudaMemcpyHostToDevice, s));
         SCUDA(c, cudaEventRecord(c->tab_ev[slot], s));
         const size_t gCT = (size_t)g * CT;
+        SCUDA(c, mark(0));
         // a2': NTT of the chunk's ciphertexts (-> baby_0) and keys
         SIMD_DISPATCH(n, e = launch_ntt<N>(c, L, 2 * L, query_ct, CT, W.sel, baby, gCT, (size_t)nc * 2 * L, W.err, s));
         if (e) break;
         SIMD_DISPATCH(n, e = launch_ntt<N>(c, M, 2 * 2 * L * M, keys, KW, W.sel, keyN, KW,
                                            (size_t)nc * 2 * 2 * L * M, W.err, s));
         if (e) break;
+        SCUDA(c, mark(1));
         // baby steps: baby_b = rot_1(baby_{b-1})
         if (fused) {
             SIMD_DISPATCH(n, e = launch_chain<N>(c, nc, false, keyN, KW, nullptr, baby, gCT, baby + CT, baby + CT, gCT,
@@ -1161,9 +1246,11 @@ static int simd_eval_core(wally_simd_ctx *c, const SimdWs &W, uint32_t nq, const
                                                       nullptr, nullptr, 0, baby + (size_t)b * CT, gCT, s));
         }
         if (e) break;
+        SCUDA(c, mark(2));
         // inner products I_j per unit
         e = launch_ptmac(c, U, baby, W.uq, W.ublk, I, s);
         if (e) break;
+        SCUDA(c, mark(3));
         // giant steps (Horner): acc = I_{m-1}; acc = rot_g(acc) + I_j, j = m-2 .. 0
         const uint32_t *X = I + (size_t)(m - 1) * CT;
         size_t xs = (size_t)m * CT;
@@ -1183,8 +1270,10 @@ static int simd_eval_core(wally_simd_ctx *c, const SimdWs &W, uint32_t nq, const
             }
         }
         if (e) break;
+        SCUDA(c, mark(4));
         SIMD_DISPATCH(n, e = launch_switch<N>(c, U, X, xs, W.uoff, resp, s));
         if (e) break;
+        SCUDA(c, mark(5));
     }
     if (e) return sfail(c, WALLY_E_CUDA, "eval launch: %s", cudaGetErrorString(e));
     return WALLY_OK;

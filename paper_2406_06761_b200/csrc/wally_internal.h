@@ -43,6 +43,8 @@ struct KParams {
     uint32_t foldp[kMaxLimbs];    //   Shoup companion
     uint32_t C[kMaxLimbs][kMaxLimbs];   // C[l][m] = prod_{k=l+1..m} q_k^{-1} mod q_l, l < m
     uint32_t Cp[kMaxLimbs][kMaxLimbs];  //   Shoup companions
+    uint32_t Qi[kMaxLimbs][kMaxLimbs];   // Qi[l][m] = q_m^{-1} mod q_l, l < m (Horner steps of the switch)
+    uint32_t Qip[kMaxLimbs][kMaxLimbs];  //   Shoup companions
     uint32_t mqinv[kMaxLimbs];    // -q^{-1} mod 2^32 (Montgomery products with the n = 8192 plaintexts)
 };
 

@@ -12,7 +12,11 @@ from .wally import WALLY_MAX_LIMBS, WallyError, _stream, lib
 
 EXPORTED = ["wally_simd_default_moduli", "wally_simd_create", "wally_simd_destroy", "wally_simd_last_error", "wally_simd_get_info",
             "wally_simd_load_clusters", "wally_simd_blocks", "wally_simd_eval_batch", "wally_simd_eval_batch_host",
-            "wally_simd_modmuls_per_query", "wally_simd_launch_count", "wally_simd_set_chain_threshold"]
+            "wally_simd_modmuls_per_query", "wally_simd_launch_count", "wally_simd_set_chain_threshold",
+            "wally_simd_enable_stage_timing", "wally_simd_stage_times", "wally_simd_stage_work"]
+
+# stages of wally_simd_stage_times / wally_simd_stage_work (include/wally_simd.h)
+STAGES = ["ntt", "baby_steps", "inner_products", "giant_steps", "switch"]
 
 
 class wally_simd_params(ctypes.Structure):
@@ -42,6 +46,9 @@ def _sig():
         "wally_simd_modmuls_per_query": ([vp, u32], u64),
         "wally_simd_launch_count": ([vp], u64),
         "wally_simd_set_chain_threshold": ([vp, u32], ctypes.c_int),
+        "wally_simd_enable_stage_timing": ([vp, ctypes.c_int], ctypes.c_int),
+        "wally_simd_stage_times": ([vp, P(ctypes.c_double), P(u64)], ctypes.c_int),
+        "wally_simd_stage_work": ([vp, u32, P(u32), P(u64), P(u64)], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -161,3 +168,22 @@ class SimdServer:
 
     def launch_count(self) -> int:
         return int(lib.wally_simd_launch_count(self.ctx))
+
+    def enable_stage_timing(self, on: bool = True):
+        _check(lib.wally_simd_enable_stage_timing(self.ctx, int(on)), self.ctx)
+
+    def stage_times(self):
+        """(ms per stage summed since the last call, chunks summed); STAGES names the stages."""
+        ms = (ctypes.c_double * len(STAGES))()
+        chunks = ctypes.c_uint64(0)
+        _check(lib.wally_simd_stage_times(self.ctx, ms, ctypes.byref(chunks)), self.ctx)
+        return [float(x) for x in ms], int(chunks.value)
+
+    def stage_work(self, ids):
+        """Algorithmic (modmuls, HBM bytes) per stage for a batch with cluster ids `ids`."""
+        ids = np.ascontiguousarray(ids, dtype=np.uint32)
+        mm = (ctypes.c_uint64 * len(STAGES))()
+        by = (ctypes.c_uint64 * len(STAGES))()
+        _check(lib.wally_simd_stage_work(self.ctx, ids.size, ids.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
+                                         mm, by), self.ctx)
+        return [int(x) for x in mm], [int(x) for x in by]

@@ -201,6 +201,46 @@ def test_simd_host_path_matches_device_path(S):
         assert np.array_equal(rh.numpy().view(np.uint32), want[:words]), sub
 
 
+def test_simd_stage_timing_and_work(S):
+    """wally_simd_enable_stage_timing / wally_simd_stage_times / wally_simd_stage_work (include/wally_simd.h):
+    the five stage times of a timed batch add up to (at most) its wall time on the stream, every stage
+    ran, timing leaves the responses unchanged, and the per-stage work matches wally_simd_modmuls_per_query
+    and the stated byte terms."""
+    n, L, d = 1024, 2, 16
+    rng = np.random.default_rng(31)
+    srv = S.SimdServer(n, L, d, baby=4)
+    clusters = [rng.integers(-15, 16, size=(s_, d)).astype(np.int8) for s_ in (40, 600, 300)]
+    srv.load_clusters(clusters)
+    nq = 9
+    ids = np.array([1, 0, 2, 1, 1, 2, 0, 1, 2], np.uint32)
+    mods = srv.moduli
+    cts = _uniform(rng, mods[:L], (nq, 2), n)
+    keys = _uniform(rng, mods, (nq, 2, 2, L), n)
+    want, _ = _run(srv, ids, cts, keys)
+    srv.stage_times()
+    srv.enable_stage_timing(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    got, _ = _run(srv, ids, cts, keys)
+    e1.record()
+    torch.cuda.synchronize()
+    srv.enable_stage_timing(False)
+    ms, chunks = srv.stage_times()
+    assert np.array_equal(got, want)
+    assert chunks >= 1 and len(ms) == len(S.STAGES) == 5
+    assert all(t > 0 for t in ms), ms
+    assert sum(ms) <= e0.elapsed_time(e1) * 1.05 + 0.05
+    assert srv.stage_times() == ([0.0] * 5, 0)                 # the record was cleared
+    mm, by = srv.stage_work(ids)
+    blocks = [srv.blocks(int(c)) for c in ids]
+    assert sum(mm) == sum(srv.modmuls_per_query(b) for b in blocks)
+    ct = 2 * L * n * 4
+    distinct = sum(srv.blocks(c) for c in set(ids.tolist()))
+    assert by[2] == distinct * d * L * n * 8 + sum(blocks) * (srv.baby + srv.giant) * ct
+    with pytest.raises(Exception):
+        srv.stage_work(np.array([7], np.uint32))                  # unknown cluster
+
+
 @pytest.mark.parametrize("name", ["c3", "c5"])
 def test_simd_full_config_sampled_bit_exact(S, name):
     """The bench's launch configuration at full size (every cluster loaded, the whole query batch in one
