@@ -352,8 +352,14 @@ __device__ __forceinline__ uint32_t ms_term(uint32_t r, uint32_t h_m, uint32_t q
 #ifndef WALLY_MS_FORM
 #define WALLY_MS_FORM 2
 #endif
-template <int L, int J, int NA>
+// the generic kernels (eval_kernel, eval_kernel_grp: up to 255 registers, both
+// components per thread) keep the additive form with reduced residues
+#ifndef WALLY_MS_FORM_GENERIC
+#define WALLY_MS_FORM_GENERIC -1
+#endif
+template <int L, int J, int NA, int FORM = WALLY_MS_FORM>
 __device__ __forceinline__ void ms_elem(uint32_t &a, uint32_t &rtop, uint32_t (&acc)[NA], const KParams &kp) {
+    constexpr bool LZ = FORM >= 0;                                   // FORM = -1: additive form, reduced residues
     const uint32_t qj = kp.q[J], qj2 = kp.q2[J];
     if constexpr (L == 1) {
         a = csub(a, qj);
@@ -367,7 +373,7 @@ __device__ __forceinline__ void ms_elem(uint32_t &a, uint32_t &rtop, uint32_t (&
     } else {
         uint32_t A;                                                  // [0, 2q)
         if constexpr (J == L - 2)
-            A = ms_term(rtop, kp.h[L - 1], qj, kp.C[J][L - 1], kp.Cp[J][L - 1]);
+            A = ms_term<LZ>(rtop, kp.h[L - 1], qj, kp.C[J][L - 1], kp.Cp[J][L - 1]);
         else
             A = acc[J];
         if constexpr (J > 0) {
@@ -375,27 +381,22 @@ __device__ __forceinline__ void ms_elem(uint32_t &a, uint32_t &rtop, uint32_t (&
 #pragma unroll
             for (int l = 0; l < J; l++) {
                 const uint32_t ql = kp.q[l];
-#if WALLY_MS_FORM == 1
-                // acc_l (after limb L-1: (h_{L-1} - r_{L-1}) q_{L-1}^{-1}) <- (acc_l + h_J - r_J) q_J^{-1}
-                const uint32_t base =
-                    (J == L - 2) ? ms_term(rtop, kp.h[L - 1], ql, kp.Qi[l][L - 1], kp.Qip[l][L - 1]) : acc[l];
-                acc[l] = shoup_mul(base + (kp.h[J] + ql) - r, kp.Qi[l][J], kp.Qip[l][J], ql);
-#elif WALLY_MS_FORM == 2
-                // nested at limb L-2 only: acc_l = ((h_{L-1} - r_{L-1}) q_{L-1}^{-1} + h_J - r_J) C[l][J],
-                // later limbs add their terms
-                if constexpr (J == L - 2) {
+                if constexpr (FORM == 1) {
+                    // acc_l (after limb L-1: (h_{L-1} - r_{L-1}) q_{L-1}^{-1}) <- (acc_l + h_J - r_J) q_J^{-1}
+                    const uint32_t base =
+                        (J == L - 2) ? ms_term(rtop, kp.h[L - 1], ql, kp.Qi[l][L - 1], kp.Qip[l][L - 1]) : acc[l];
+                    acc[l] = shoup_mul(base + (kp.h[J] + ql) - r, kp.Qi[l][J], kp.Qip[l][J], ql);
+                } else if constexpr (FORM == 2 && J == L - 2) {
+                    // nested at limb L-2 only: acc_l = ((h_{L-1} - r_{L-1}) q_{L-1}^{-1} + h_J - r_J) C[l][J],
+                    // later limbs add their terms
                     const uint32_t t = ms_term(rtop, kp.h[L - 1], ql, kp.Qi[l][L - 1], kp.Qip[l][L - 1]);
                     acc[l] = shoup_mul(t + (kp.h[J] + ql) - r, kp.C[l][J], kp.Cp[l][J], ql);
                 } else {
-                    const uint32_t term = ms_term(r, kp.h[J], ql, kp.C[l][J], kp.Cp[l][J]);
-                    acc[l] = csub(acc[l] + term, kp.q2[l]);
+                    const uint32_t term = ms_term<LZ>(r, kp.h[J], ql, kp.C[l][J], kp.Cp[l][J]);
+                    const uint32_t prev =
+                        (J == L - 2) ? ms_term<LZ>(rtop, kp.h[L - 1], ql, kp.C[l][L - 1], kp.Cp[l][L - 1]) : acc[l];
+                    acc[l] = csub(prev + term, kp.q2[l]);           // < 4 q -> [0, 2q)
                 }
-#else
-                const uint32_t term = ms_term(r, kp.h[J], ql, kp.C[l][J], kp.Cp[l][J]);
-                const uint32_t prev =
-                    (J == L - 2) ? ms_term(rtop, kp.h[L - 1], ql, kp.C[l][L - 1], kp.Cp[l][L - 1]) : acc[l];
-                acc[l] = csub(prev + term, kp.q2[l]);               // < 4 q -> [0, 2q)
-#endif
             }
         } else {
             a = csub(csub(a + A, qj2), qj);                          // < 4 q -> canonical response word
@@ -403,7 +404,7 @@ __device__ __forceinline__ void ms_elem(uint32_t &a, uint32_t &rtop, uint32_t (&
     }
 }
 
-template <int L, int J, int V, int NA>
+template <int L, int J, int V, int FORM = WALLY_MS_FORM, int NA>
 __device__ __forceinline__ void ms_step(uint32_t (&a)[V], uint32_t (&rtop)[V], uint32_t (&acc)[NA][V],
                                         const KParams &kp) {
 #pragma unroll
@@ -411,7 +412,7 @@ __device__ __forceinline__ void ms_step(uint32_t (&a)[V], uint32_t (&rtop)[V], u
         uint32_t ac[NA];
 #pragma unroll
         for (int l = 0; l < NA; l++) ac[l] = acc[l][v];
-        ms_elem<L, J, NA>(a[v], rtop[v], ac, kp);
+        ms_elem<L, J, NA, FORM>(a[v], rtop[v], ac, kp);
 #pragma unroll
         for (int l = 0; l < NA; l++) acc[l][v] = ac[l];
     }
@@ -478,7 +479,7 @@ __device__ __forceinline__ void eval_limb(EvalState<N, L, NC> &st, const BatchAr
     else
         intt_chain<N, NC>(st.a, cx.tw + (size_t)J * Gm::TW_LIMB, g, q, q2, cx.bufA, cx.bufB);
 #pragma unroll
-    for (int c = 0; c < NC; c++) ms_step<L, J, V>(st.a[c], st.rtop[c], st.acc[c], ba.kp);
+    for (int c = 0; c < NC; c++) ms_step<L, J, V, WALLY_MS_FORM_GENERIC>(st.a[c], st.rtop[c], st.acc[c], ba.kp);
 }
 
 template <int N, int L, int NC, int J, bool GRP>
