@@ -111,6 +111,11 @@ EDGE = [
     dict(n=8192, L=3, d=64, sizes=[130, 3], nq=6),
     dict(n=8192, L=2, d=128, sizes=[70], nq=5),
     dict(n=8192, L=2, d=8192, sizes=[2], nq=4),
+    # fused kernel v4 with compact responses (16 does not divide d): the instantiation whose
+    # null-pointer test read a stale register on the B200 (found by test_gpu_fuzz.py)
+    dict(n=4096, L=3, d=100, sizes=[150, 3], nq=9),
+    dict(n=4096, L=2, d=3210, sizes=[2, 5, 3], nq=56),
+    dict(n=4096, L=3, d=3210, sizes=[2], nq=1),
 ]
 
 
