@@ -3,7 +3,9 @@
 Every case draws a ring degree n, a limb count L, an embedding dimension d
 (arbitrary, or one of the values the specialised kernels key on: 16 | d,
 32 | d, d = n, d = 1), ragged clusters, a skewed query mix, extreme residues
-(0 and q_i - 1) and a response format, runs one batch through
+(0 and q_i - 1) and a response format (every fifth case a batch of 600-1,400
+queries, which takes the 32-query work items; a sample of its queries is
+compared), runs one batch through
 wally_eval_batch (every third case through the host-buffer call
 wally_eval_batch_host) and compares every word of every response with the
 oracle's pairs (Alg 4 ServerComputation).  Bar: bit-exact.
@@ -30,6 +32,7 @@ from paper_2406_06761_b200.wally import WallyError, WallyServer  # noqa: E402
 CASES = int(os.environ.get("WALLY_FUZZ_CASES", "24"))
 SEED0 = int(os.environ.get("WALLY_FUZZ_SEED", "20260601"))
 MAX_PAIRS = 700     # per case: the oracle's work
+BIG = os.environ.get("WALLY_FUZZ_BIG") == "1"     # every case a large batch (else every fifth)
 
 
 def draw_case(seed: int) -> dict:
@@ -60,6 +63,13 @@ def draw_case(seed: int) -> dict:
     Ps = [-(-s // E) for s in sizes]
     nq_max = max(1, MAX_PAIRS // max(Ps))
     nq = int(rng.integers(1, min(nq_max, 160) + 1))
+    if BIG or seed % 5 == 2:
+        # a batch large enough for 32-query work items (>= 4 queries per SM): few, small clusters
+        # (drawn from a stream of their own, so the other parameters of a seed do not depend on this)
+        rb = np.random.default_rng(seed ^ 0xB16)
+        sizes = [min((int(rb.integers(1, 4)) - 1) * E + int(rb.integers(1, E + 1)), 4096)
+                 for _ in range(int(rb.integers(1, 4)))]
+        nq = int(rb.integers(600, 1400))
     fmt = int(rng.integers(0, 3))
     bound = int(rng.choice([1, 15, 127]))
     return dict(seed=seed, n=n, L=L, d=d, sizes=sizes, nq=nq, fmt=fmt, bound=bound,
@@ -104,7 +114,11 @@ def run_case(c: dict) -> int:
         resp, off = H.run_batch(srv, ids, cts)
     pcs_by_c = [capi.encode_cluster(e, d, n) for e in clusters]
     pairs = 0
-    for q in range(nq):
+    check = range(nq)
+    if nq * max(p.shape[0] for p in pcs_by_c) > 2 * MAX_PAIRS:
+        # large batch: the first and last queries, and a random sample (the oracle's work stays bounded)
+        check = sorted(set(range(8)) | set(range(nq - 8, nq)) | set(rng.choice(nq, size=300, replace=False).tolist()))
+    for q in check:
         cl = int(ids[q])
         P = pcs_by_c[cl].shape[0]
         assert int(off[q + 1] - off[q]) == P * H.words_per_pt(n, d, fmt), c
