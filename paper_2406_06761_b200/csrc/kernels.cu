@@ -795,13 +795,15 @@ struct LimbLoopTM {
                 }
         }
         intt_chain_group<N, NC>(st.a, cx.tw + (size_t)J * Gm::TW_LIMB, g, q, q2, cx.bufA, cx.bar);
-        // mod-switch state through TMEM between limbs: L = 3 (its registers are
-        // what the chat prefetch needs).  L = 2 keeps its single 16-word state
-        // in registers: the TMEM variant (WALLY_TM_L2_TMEM = 1) raises an
-        // illegal-address fault on the B200 (scripts/tm_l2_repro.py; the
-        // investigation is in DESIGN.md section 14).
+        // mod-switch state through TMEM between limbs (its registers are what the
+        // chat prefetch needs).  At L = 2 the single 16-word state went through
+        // registers until the end of round 2, because this variant faulted on the
+        // B200; the fault was the null-pointer guard above, not tensor memory
+        // (DESIGN.md section 14), and with it fixed the TMEM state is 6% faster
+        // (c5 full responses 95.1 -> 89.1 ms).  WALLY_TM_L2_TMEM = 0 restores the
+        // register form for A/B timing.
 #ifndef WALLY_TM_L2_TMEM
-#define WALLY_TM_L2_TMEM 0
+#define WALLY_TM_L2_TMEM 1
 #endif
         constexpr uint32_t TM_STATE_COL = 96;
         if constexpr (L == 3 || (L == 2 && WALLY_TM_L2_TMEM)) {
