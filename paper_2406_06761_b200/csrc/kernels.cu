@@ -1376,7 +1376,12 @@ struct LimbLoopPR {
             else c0_tail<N, L, J>(z, cst, s_mrg + J * 256, g, mu, ba.kp);
         }
         par ^= 1u;
-        if constexpr (L == 3) {
+        // modulus-switch state through TMEM between limbs, at L = 2 (one 16-word rtop) as well:
+        // c5 61.9 -> 61.7 ms, compact responses 61.6 -> 60.9 (WALLY_PR_L2_TMEM = 0: registers, for A/B)
+#ifndef WALLY_PR_L2_TMEM
+#define WALLY_PR_L2_TMEM 1
+#endif
+        if constexpr (L == 3 || (L == 2 && WALLY_PR_L2_TMEM)) {
             if constexpr (J < L - 1) {
                 tmem_wait_st_all();
                 if constexpr (J == L - 2) {
